@@ -1,0 +1,219 @@
+/*
+ * dis_b200.h — C ABI of the B200-native Dense Inverse Search (DIS) flow path.
+ *
+ * This is the drop-in boundary for the reference's `dis_flow` hot path
+ * (reference: pkg/src/disflow/pipeline.py:150-163 `dis_flow`,
+ *  pipeline.py:136-147 `dis_flow_on_pyramids`) and for the numba operator
+ * layer underneath it (the `@njit` kernels in inverse_search.py,
+ * densification.py and variational.py, plus the numpy stages in core.py).
+ *
+ * Conventions (all entry points):
+ *  - plain pointers and sizes only; device pointers are CUDA global-memory
+ *    addresses (e.g. torch.Tensor.data_ptr()), `stream` is a cudaStream_t
+ *    passed as void* (NULL = legacy default stream).
+ *  - every call is stream-ordered and asynchronous; nothing allocates;
+ *    scratch comes from a caller-owned workspace sized by
+ *    dis_workspace_bytes().
+ *  - return value: DIS_OK or a negative status (below); a human readable
+ *    message for the last failing call on this host thread is available from
+ *    dis_last_error().  The status values mirror the reference's exception
+ *    types: ParameterError (core.py:25-26), ValueError for shapes
+ *    (core.py:68-71, 92-96, 113-119; pipeline.py:30-41), AssertionError for
+ *    densification coverage (densification.py:189-190) and RuntimeError for
+ *    non-finite refinement output (variational.py:268-274).
+ *  - numerics: IEEE float64 in the reference's exact operation order
+ *    (no FMA contraction, sequential sums), so results are bit-identical to
+ *    the reference on the same inputs.
+ *
+ * Raster layout on the device ("level layout"): every per-level raster of a
+ * pair (image, gradients, flow components) is float64, x-major:
+ * element (x, y) of a W_s x H_s level lives at [x * H_s + y]; a batch of B
+ * pairs stores B such rasters back to back.  Frames passed in and the final
+ * flow returned are row-major like the reference ((H, W) and (H, W, 2)).
+ */
+#ifndef DIS_B200_H
+#define DIS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DIS_B200_ABI_VERSION 1
+
+/* status codes */
+#define DIS_OK 0
+#define DIS_ERR_PARAMETER (-1)   /* ParameterError(ValueError)  core.py:25-26      */
+#define DIS_ERR_VALUE (-2)       /* ValueError (shapes, non-finite input frames)    */
+#define DIS_ERR_COVERAGE (-3)    /* AssertionError densification.py:189-190        */
+#define DIS_ERR_NONFINITE (-4)   /* RuntimeError variational.py:268-274            */
+#define DIS_ERR_CUDA (-5)        /* CUDA launch / runtime failure                   */
+#define DIS_ERR_WORKSPACE (-6)   /* workspace too small                             */
+
+/* residual norms: inverse_search.py:20 NORM_CODES */
+#define DIS_NORM_L2 0
+#define DIS_NORM_L1 1
+#define DIS_NORM_HUBER 2
+
+/* frame element types accepted by the entry points (as_image core.py:65-72
+ * converts any real raster to float64; these are the ones we take) */
+#define DIS_DTYPE_F32 0
+#define DIS_DTYPE_F64 1
+#define DIS_DTYPE_U8 2
+
+/* device-status bits written into the workspace status word */
+#define DIS_STATUS_NONFINITE_INPUT 1u
+#define DIS_STATUS_COVERAGE 2u
+#define DIS_STATUS_NONFINITE_FLOW 4u
+
+/*
+ * Parameter set: field-for-field the reference's DisParams (core.py:237-257)
+ * and VarParams (core.py:197-210).  Two documented extensions:
+ *  - outer_iters_fixed: > 0 overrides VarParams.outer_iters(s) = s + 1
+ *    (core.py:212-213) with a constant (BASELINE configs use 1);
+ *    <= 0 keeps the reference rule.
+ *  - mode/bidirectional are carried for validation only: this path
+ *    implements mode "flow" with bidirectional = 0 (pipeline.py:136-163).
+ */
+typedef struct dis_params_t {
+  int32_t patch_size;            /* theta_ps                          */
+  int32_t iterations;            /* theta_it                          */
+  int32_t finest_scale;          /* theta_sf                          */
+  int32_t coarsest_scale;        /* theta_ss                          */
+  int32_t downscale;             /* must be 2 on this path            */
+  int32_t use_mean_normalization;
+  int32_t use_densification;     /* carried; dense path always densifies */
+  int32_t residual_norm;         /* DIS_NORM_*                        */
+  double overlap;                /* theta_ov                          */
+  double huber_b;
+  int32_t variational;           /* 0: DisParams.variational is None  */
+  int32_t var_inner_sor_iters;   /* theta_vi                          */
+  double var_intensity_weight;   /* delta                             */
+  double var_gradient_weight;    /* gamma                             */
+  double var_smoothness_weight;  /* alpha                             */
+  double var_penalizer_eps;
+  double var_sor_omega;
+  int32_t outer_iters_fixed;     /* extension, see above              */
+  int32_t mode;                  /* 0 flow, 1 stereo (rejected here)  */
+  int32_t bidirectional;         /* must be 0 on this path            */
+  int32_t reserved;
+} dis_params_t;
+
+/* Fill `p` with DisParams() defaults (core.py:246-257, operating point 2). */
+void dis_params_default(dis_params_t* p);
+
+/* DisParams.validate + VarParams.validate (core.py:296-316, 215-223) plus
+ * this path's own restrictions (downscale == 2, mode flow, no
+ * bidirectional). */
+int dis_params_validate(const dis_params_t* p);
+
+/* Workspace bytes for dis_flow_batch on B pairs of H x W frames. */
+size_t dis_workspace_bytes(int32_t B, int32_t H, int32_t W, const dis_params_t* p);
+
+/*
+ * Fused coarse-to-fine flow for a batch of B independent pairs
+ * (dis_flow, pipeline.py:150-163, applied pair by pair).
+ *   frame1, frame2 : device, B x H x W row-major, element type `dtype`
+ *   flow_out       : device, B x H x W x 2 float64 row-major (u, v)
+ *   workspace      : device, >= dis_workspace_bytes(B, H, W, p) bytes
+ * Enqueues all work on `stream` and returns without synchronizing.  The
+ * device-side status word (non-finite input, coverage, non-finite flow) is
+ * at offset 0 of the workspace; read it with dis_read_status() after the
+ * stream completes and convert with dis_status_to_error().
+ */
+int dis_flow_batch(const void* frame1, const void* frame2, int32_t dtype,
+                   int32_t B, int32_t H, int32_t W, const dis_params_t* p,
+                   double* flow_out, void* workspace, size_t workspace_bytes,
+                   void* stream);
+
+/* Synchronous host-buffer variant (the e2e boundary): host frames in, host
+ * flow out; copies are enqueued on `stream` around dis_flow_batch and the
+ * call returns after the stream has drained, with the status word already
+ * converted to a return code. Host buffers should be pinned for speed. */
+int dis_flow_batch_host(const void* host_frame1, const void* host_frame2,
+                        int32_t dtype, int32_t B, int32_t H, int32_t W,
+                        const dis_params_t* p, double* host_flow_out,
+                        void* workspace, size_t workspace_bytes, void* stream);
+
+/* Copy the status word out of the workspace (blocking on `stream`). */
+int dis_read_status(const void* workspace, uint32_t* status_out, void* stream);
+/* Map a device status word to DIS_OK / DIS_ERR_* and set dis_last_error(). */
+int dis_status_to_error(uint32_t status);
+
+/* ------------------------------------------------------------------------
+ * Stage entry points (the operator layer), each parity-testable against the
+ * reference function named beside it.  Level rasters use the x-major level
+ * layout described at the top; `B` pairs are processed per call.
+ * ---------------------------------------------------------------------- */
+
+/* build_pyramid (core.py:106-128): levels 0..coarsest of B frames.
+ *   levels_img[s]  : device B x (W>>s) x (H>>s) float64 (x-major) for every
+ *                    s in 0..coarsest (NULL allowed for levels not wanted)
+ *   levels_gx/gy[s]: gradients (image_gradients core.py:75-85), NULL = skip
+ *   levels_dd[s]   : 4 consecutive rasters gxx, gxy, gyx, gyy
+ *                    (_second_derivatives variational.py:168-171), NULL = skip
+ *   status         : device uint32, OR-ed with DIS_STATUS_NONFINITE_INPUT */
+int dis_build_pyramid(const void* frames, int32_t dtype, int32_t B, int32_t H,
+                      int32_t W, int32_t coarsest, double* const* levels_img,
+                      double* const* levels_gx, double* const* levels_gy,
+                      double* const* levels_dd, uint32_t* status, void* stream);
+
+/* init_patches + precompute_patch_set + optimize_patch_set + reset_outliers
+ * + refresh_patch_stats for one scale (pipeline.py:54-82).
+ *   ref_img/ref_gx/ref_gy/qry_img : level s, B x W x H x-major
+ *   coarse_flow_u/v : level s+1 flow (B x Wc x Hc x-major) or NULL (zeros)
+ *   out_u/out_v/out_off/out_mar : B x P_s, P_s in grid row-major order
+ *   out_init_u/v (optional, may be NULL): B x P_s initial displacements
+ *   out_valid (optional): B x P_s uint8 */
+int dis_patch_search(const double* ref_img, const double* ref_gx,
+                     const double* ref_gy, const double* qry_img, int32_t B,
+                     int32_t W, int32_t H, const double* coarse_flow_u,
+                     const double* coarse_flow_v, int32_t Wc, int32_t Hc,
+                     const dis_params_t* p, double* out_u, double* out_v,
+                     double* out_off, double* out_mar, double* out_init_u,
+                     double* out_init_v, uint8_t* out_valid, void* stream);
+
+/* densify (densification.py:173-191): dense flow of level s. */
+int dis_densify(const double* ref_img, const double* qry_img, int32_t B,
+                int32_t W, int32_t H, const dis_params_t* p,
+                const double* patch_u, const double* patch_v,
+                const double* patch_off, double* flow_u, double* flow_v,
+                uint32_t* status, void* stream);
+
+/* Workspace for dis_refine on one level. */
+size_t dis_refine_workspace_bytes(int32_t B, int32_t W, int32_t H);
+
+/* refine (variational.py:220-275) in place on flow_u/flow_v, running
+ * `outer_iters` fixed-point iterations (pass params->outer_iters_fixed or
+ * scale_index + 1).  ref_dd/qry_dd: 4 rasters each (gxx, gxy, gyx, gyy). */
+int dis_refine(const double* ref_img, const double* ref_gx, const double* ref_gy,
+               const double* ref_dd, const double* qry_img, const double* qry_gx,
+               const double* qry_gy, const double* qry_dd, int32_t B, int32_t W,
+               int32_t H, const dis_params_t* p, int32_t outer_iters,
+               double* flow_u, double* flow_v, void* workspace,
+               size_t workspace_bytes, uint32_t* status, void* stream);
+
+/* upsample_flow (core.py:178-190) by the factor 2 from a W x H level to a
+ * Wn x Hn level (x-major in and out). */
+int dis_upsample_flow(const double* in_u, const double* in_v, int32_t B,
+                      int32_t W, int32_t H, double* out_u, double* out_v,
+                      int32_t Wn, int32_t Hn, void* stream);
+
+/* Patch grid (create_grid densification.py:58-79): number of window
+ * origins per axis and the origins themselves (host memory).  Returns the
+ * count, or a negative status. */
+int32_t dis_grid_axis(int32_t dim, int32_t patch_size, double overlap,
+                      int32_t* origins_out, int32_t max_out);
+
+/* Human-readable message of the last failing call on this host thread. */
+const char* dis_last_error(void);
+/* DIS_B200_ABI_VERSION of the loaded library. */
+int32_t dis_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DIS_B200_H */

@@ -1,0 +1,263 @@
+"""Generate golden vectors by running the REFERENCE itself (test infra).
+
+Run in the build container only (needs /root/reference):
+
+    python oracle/gen_golden.py
+
+Writes tests/golden/*.npz.  Imports the reference package from
+/root/reference/pkg/src with NUMBA_CACHE_DIR redirected to /tmp so nothing
+is written into the read-only reference tree.  Every array stored here is a
+reference output on a seeded input; tests/test_oracle_golden.py checks the C
+oracle against them bit-for-bit and tests/test_gpu_parity.py checks the CUDA
+path against the oracle (and the goldens) on the GPU box.
+
+Versions recorded in every file: numpy, numba, scipy, python.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import hashlib
+import os
+import platform
+import sys
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_golden")
+sys.dont_write_bytecode = True
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import numpy as np  # noqa: E402
+
+import disflow  # noqa: E402  (the reference)
+from disflow import core, densification, inverse_search, pipeline, variational  # noqa: E402
+
+from tools import synth  # noqa: E402
+
+OUT = os.path.join(REPO, "tests", "golden")
+
+
+@dataclasses.dataclass(frozen=True)
+class VarParamsFixed(core.VarParams):
+    """Reference-side outer-iteration override."""
+
+    fixed_outer: int = 1
+
+    def outer_iters(self, scale_index: int) -> int:
+        return self.fixed_outer
+
+
+def versions():
+    import numba
+    import scipy
+
+    return dict(numpy=np.__version__, numba=numba.__version__, scipy=scipy.__version__,
+                python=platform.python_version())
+
+
+def ref_params(cfg, outer_fixed=1, coarsest=None):
+    vp = (VarParamsFixed(fixed_outer=outer_fixed) if outer_fixed is not None
+          else core.VarParams())
+    return core.DisParams(
+        patch_size=cfg.patch_size, overlap=cfg.overlap, iterations=cfg.iterations,
+        finest_scale=cfg.finest_scale,
+        coarsest_scale=cfg.coarsest_scale if coarsest is None else coarsest,
+        variational=vp)
+
+
+def save(name, **arrays):
+    meta = versions()
+    np.savez_compressed(os.path.join(OUT, name), **arrays,
+                        **{f"meta_{k}": np.array(v) for k, v in meta.items()})
+    print("wrote", name, sorted(arrays))
+
+
+def gen_pyramid():
+    rng = np.random.default_rng(100)
+    img = rng.uniform(0, 255, size=(91, 133)).astype(np.float32)
+    pyr = core.build_pyramid(img, 4)
+    d = {"img": img}
+    for s, lvl in enumerate(pyr.levels):
+        d[f"L{s}_img"] = lvl.image
+        d[f"L{s}_gx"] = lvl.grad_x
+        d[f"L{s}_gy"] = lvl.grad_y
+        gxx, gxy, gyx, gyy = variational._second_derivatives(lvl)
+        d[f"L{s}_dd"] = np.stack([gxx, gxy, gyx, gyy])
+    # the 10^6-block box-mean order check (core.py:88-98)
+    # regenerate in the test with default_rng(1000).uniform(0, 255, (200, 400))
+    big = np.random.default_rng(1000).uniform(0, 255, size=(200, 400))
+    d["box_out"] = core._box_downsample(big, 2)
+    save("pyramid.npz", **d)
+
+
+def gen_samplers():
+    rng = np.random.default_rng(101)
+    flow = rng.normal(0, 3, size=(13, 17, 2))
+    d = {"flow": flow}
+    d["up_27x35"] = core.upsample_flow(flow, 35, 27, 2)
+    d["up_26x34"] = core.upsample_flow(flow, 34, 26, 2)
+    img = rng.uniform(0, 255, size=(11, 9))
+    xs = rng.uniform(-3, 12, size=500)
+    ys = rng.uniform(-3, 14, size=500)
+    d["bm_img"] = img
+    d["bm_x"] = xs
+    d["bm_y"] = ys
+    d["bm_np"] = core.bilinear_map(img, xs, ys)
+    d["bm_nb"] = np.array([inverse_search._bilin(img, x, y) for x, y in zip(xs, ys)])
+    # grids
+    grids = []
+    for (dim, ps, ov) in [(1024, 8, 0.3), (436, 8, 0.5), (436, 12, 0.75), (17, 8, 0.0),
+                          (12, 8, 0.999), (54, 8, 0.4), (13, 8, 0.3), (1080, 8, 0.5),
+                          (2160, 12, 0.75), (33, 5, 0.37)]:
+        g = densification.create_grid(dim, ps, ps, ov)
+        grids.append((dim, ps, ov, g.spacing, g.x_origins))
+    d["grid_dims"] = np.array([g[0] for g in grids])
+    d["grid_ps"] = np.array([g[1] for g in grids])
+    d["grid_ov"] = np.array([g[2] for g in grids])
+    d["grid_spacing"] = np.array([g[3] for g in grids])
+    d["grid_origins"] = np.concatenate([g[4] for g in grids])
+    d["grid_counts"] = np.array([len(g[4]) for g in grids])
+    save("samplers.npz", **d)
+
+
+def search_case(f1, f2, s, ps, ov, iters, coarse_flow, norm="l2", mean_norm=True):
+    """Replicates pipeline._ScaleState.search (pipeline.py:54-82) on level s
+    and returns its outputs."""
+    pyr1 = core.build_pyramid(f1, s)
+    pyr2 = core.build_pyramid(f2, s)
+    ref, qry = pyr1[s], pyr2[s]
+    grid = densification.create_grid(ref.width, ref.height, ps, ov)
+    u_init = densification.init_patches(grid, coarse_flow, 2)
+    starts = grid.starts
+    pset = inverse_search.precompute_patch_set(ref, starts[:, 0], starts[:, 1], ps)
+    pset.init_displacement = u_init
+    inverse_search.optimize_patch_set(pset, qry, iters, residual_norm=norm,
+                                      mean_normalization=mean_norm)
+    raw = pset.displacement.copy()
+    raw_off = pset.offset.copy()
+    kept = densification.reset_outliers(pset.displacement, u_init, ps)
+    was_reset = (kept != pset.displacement).any(axis=1)
+    pset.displacement = kept
+    inverse_search.refresh_patch_stats(pset, qry, was_reset, mean_norm)
+    flow = densification.densify(grid, pset.displacement, pset.offset, ref.image, qry.image)
+    return dict(x_origins=grid.x_origins, y_origins=grid.y_origins, init=u_init,
+                raw_disp=raw, raw_off=raw_off, disp=pset.displacement, off=pset.offset,
+                mar=pset.mean_abs_residual, valid=pset.valid, hinv=pset.hessian_inv,
+                mean_t=pset.template_mean, reset=was_reset, dense=flow)
+
+
+def gen_search():
+    cfg = synth.CONFIGS["c1"]
+    f1, f2, gt = synth.make_pair(7, 109, 256, 12.0, True, 10.0)
+    # level 1 (128x54) with a coarse init from the (scaled) ground truth
+    coarse = np.ascontiguousarray(gt[::4, ::4][:27, :64] * 0.25)
+    d = search_case(f1, f2, 1, 8, 0.5, 32, coarse)
+    d.update({f"in_{k}": v for k, v in dict(f1=f1, f2=f2, coarse=coarse).items()})
+    save("search_c1_like.npz", **d)
+    # ps 12 / 0.75 / 128 iterations at full resolution of a small pair
+    f1, f2, gt = synth.make_pair(8, 96, 160, 6.0, True, 6.0)
+    coarse = gt[::2, ::2] * 0.5
+    d = search_case(f1, f2, 0, 12, 0.75, 128, coarse)
+    d.update({f"in_{k}": v for k, v in dict(f1=f1, f2=f2, coarse=coarse).items()})
+    save("search_c2_like.npz", **d)
+    # no init (coarsest scale), huber norm and l1 norm
+    for norm in ("huber", "l1"):
+        d = search_case(f1, f2, 0, 8, 0.3, 16, None, norm=norm)
+        d.update({f"in_{k}": v for k, v in dict(f1=f1, f2=f2).items()})
+        save(f"search_{norm}.npz", **d)
+
+
+def gen_refine():
+    f1, f2, gt = synth.make_pair(9, 48, 80, 4.0, True, 4.0)
+    pyr1 = core.build_pyramid(f1, 0)
+    pyr2 = core.build_pyramid(f2, 0)
+    rng = np.random.default_rng(9)
+    init = gt + rng.normal(0, 0.5, size=gt.shape)
+    d = dict(f1=f1, f2=f2, init=init)
+    d["refined_s0"] = variational.refine(init, pyr1[0], pyr2[0], core.VarParams(), 0)
+    d["refined_s2"] = variational.refine(init, pyr1[0], pyr2[0], core.VarParams(), 2)
+    d["refined_fixed1"] = variational.refine(init, pyr1[0], pyr2[0],
+                                             VarParamsFixed(fixed_outer=1), 4)
+    # the packed tensors and the assembled system at the init flow
+    u = np.ascontiguousarray(init[:, :, 0])
+    v = np.ascontiguousarray(init[:, :, 1])
+    tens = variational._packed_tensors_uv(pyr1[0], pyr2[0], u, v,
+                                          variational._second_derivatives(pyr1[0]),
+                                          variational._second_derivatives(pyr2[0]))
+    h, w = u.shape
+    sysm = [np.empty((h, w)) for _ in range(6)]
+    variational._assemble_system(tens, u, v, 5.0, 10.0, 10.0, 1e-3, *sysm)
+    d["tens"] = tens
+    d["sys"] = np.stack(sysm)
+    du = np.zeros((h, w))
+    dv = np.zeros((h, w))
+    variational._sor_sweeps(u, v, du, dv, *sysm, 1.6, 5, False)
+    d["sor_du"] = du
+    d["sor_dv"] = dv
+    save("refine.npz", **d)
+
+
+def gen_e2e_small():
+    """Small end-to-end pairs with each config's operating point."""
+    cases = {
+        # name: (cfg, h, w, coarsest, outer_fixed)
+        "c0": ("c0", 112, 256, 3, 1),
+        "c0_default_outer": ("c0", 112, 256, 3, None),
+        "c1": ("c1", 109, 256, 3, 1),
+        "c2": ("c2", 96, 160, 3, 1),
+        "c3": ("c3", 135, 240, 4, 1),
+        "c4": ("c4", 135, 240, 3, 1),
+    }
+    for name, (cn, h, w, coarsest, outer) in cases.items():
+        cfg = synth.CONFIGS[cn]
+        scale = w / cfg.width
+        f1, f2, _ = synth.make_pair(11, h, w, max(2.0, cfg.maxmag * scale * 2), cfg.rects,
+                                    max(2.0, cfg.rmax * scale * 2))
+        params = ref_params(cfg, outer, coarsest)
+        flow = pipeline.dis_flow(f1, f2, params)
+        save(f"e2e_{name}.npz", f1=f1, f2=f2, flow=flow, patch_size=cfg.patch_size,
+             overlap=cfg.overlap, iterations=cfg.iterations, finest=cfg.finest_scale,
+             coarsest=coarsest, outer=-1 if outer is None else outer)
+
+
+def digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+def gen_full_hashes():
+    """Full-size config pairs through the reference: sha256 of the flow
+    bytes + summary statistics (the flows themselves are too large)."""
+    rows = []
+    plan = [("c0", 0, 1), ("c1", 0, 2), ("c2", 0, 1), ("c3", 0, 1), ("c4", 0, 1)]
+    for cn, first, count in plan:
+        cfg = synth.CONFIGS[cn]
+        f1, f2 = synth.make_batch(cfg, seed=0, count=count, first=first)
+        params = ref_params(cfg, 1)
+        for i in range(count):
+            flow = pipeline.dis_flow(f1[i], f2[i], params)
+            rows.append((cn, first + i, digest(f1[i]), digest(f2[i]), digest(flow),
+                         float(np.abs(flow).mean()), float(np.abs(flow).max())))
+            print(rows[-1])
+    save("full_hashes.npz", cfg=np.array([r[0] for r in rows]),
+         pair=np.array([r[1] for r in rows]), f1_sha=np.array([r[2] for r in rows]),
+         f2_sha=np.array([r[3] for r in rows]), flow_sha=np.array([r[4] for r in rows]),
+         flow_absmean=np.array([r[5] for r in rows]), flow_absmax=np.array([r[6] for r in rows]))
+
+
+if __name__ == "__main__":
+    os.makedirs(OUT, exist_ok=True)
+    which = sys.argv[1:] or ["pyramid", "samplers", "search", "refine", "e2e", "full"]
+    pipeline.warmup()
+    if "pyramid" in which:
+        gen_pyramid()
+    if "samplers" in which:
+        gen_samplers()
+    if "search" in which:
+        gen_search()
+    if "refine" in which:
+        gen_refine()
+    if "e2e" in which:
+        gen_e2e_small()
+    if "full" in which:
+        gen_full_hashes()
