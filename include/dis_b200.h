@@ -25,17 +25,23 @@
  *    (no FMA contraction, sequential sums), so results are bit-identical to
  *    the reference on the same inputs.
  *
- * Raster layout on the device ("level layout"): every per-level raster of a
- * pair (image, gradients, flow components) is float64, x-major:
- * element (x, y) of a W_s x H_s level lives at [x * H_s + y]; a batch of B
- * pairs stores B such rasters back to back.  Frames passed in and the final
- * flow returned are row-major like the reference ((H, W) and (H, W, 2)).
+ * Raster layout on the device: every per-level raster of a pair (image,
+ * gradients, second derivatives, dense flow components u and v) is float64
+ * row-major (H_s, W_s) exactly like the reference (core.py:1-14); a batch of
+ * B pairs stores B such rasters back to back.  Frames passed in are (B, H, W)
+ * row-major; the flow returned is (B, H, W, 2) float64 row-major (u, v).
  */
 #ifndef DIS_B200_H
 #define DIS_B200_H
 
 #include <stddef.h>
 #include <stdint.h>
+
+#if defined(__GNUC__)
+#define DIS_API __attribute__((visibility("default")))
+#else
+#define DIS_API
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -102,15 +108,15 @@ typedef struct dis_params_t {
 } dis_params_t;
 
 /* Fill `p` with DisParams() defaults (core.py:246-257, operating point 2). */
-void dis_params_default(dis_params_t* p);
+DIS_API void dis_params_default(dis_params_t* p);
 
 /* DisParams.validate + VarParams.validate (core.py:296-316, 215-223) plus
  * this path's own restrictions (downscale == 2, mode flow, no
  * bidirectional). */
-int dis_params_validate(const dis_params_t* p);
+DIS_API int dis_params_validate(const dis_params_t* p);
 
 /* Workspace bytes for dis_flow_batch on B pairs of H x W frames. */
-size_t dis_workspace_bytes(int32_t B, int32_t H, int32_t W, const dis_params_t* p);
+DIS_API size_t dis_workspace_bytes(int32_t B, int32_t H, int32_t W, const dis_params_t* p);
 
 /*
  * Fused coarse-to-fine flow for a batch of B independent pairs
@@ -123,51 +129,57 @@ size_t dis_workspace_bytes(int32_t B, int32_t H, int32_t W, const dis_params_t* 
  * at offset 0 of the workspace; read it with dis_read_status() after the
  * stream completes and convert with dis_status_to_error().
  */
-int dis_flow_batch(const void* frame1, const void* frame2, int32_t dtype,
+DIS_API int dis_flow_batch(const void* frame1, const void* frame2, int32_t dtype,
                    int32_t B, int32_t H, int32_t W, const dis_params_t* p,
                    double* flow_out, void* workspace, size_t workspace_bytes,
                    void* stream);
+
+/* Workspace bytes for dis_flow_batch_host (adds device staging for the
+ * frames and the flow). */
+DIS_API size_t dis_host_workspace_bytes(int32_t B, int32_t H, int32_t W, int32_t dtype,
+                                const dis_params_t* p);
 
 /* Synchronous host-buffer variant (the e2e boundary): host frames in, host
  * flow out; copies are enqueued on `stream` around dis_flow_batch and the
  * call returns after the stream has drained, with the status word already
  * converted to a return code. Host buffers should be pinned for speed. */
-int dis_flow_batch_host(const void* host_frame1, const void* host_frame2,
+DIS_API int dis_flow_batch_host(const void* host_frame1, const void* host_frame2,
                         int32_t dtype, int32_t B, int32_t H, int32_t W,
                         const dis_params_t* p, double* host_flow_out,
                         void* workspace, size_t workspace_bytes, void* stream);
 
 /* Copy the status word out of the workspace (blocking on `stream`). */
-int dis_read_status(const void* workspace, uint32_t* status_out, void* stream);
+DIS_API int dis_read_status(const void* workspace, uint32_t* status_out, void* stream);
 /* Map a device status word to DIS_OK / DIS_ERR_* and set dis_last_error(). */
-int dis_status_to_error(uint32_t status);
+DIS_API int dis_status_to_error(uint32_t status);
 
 /* ------------------------------------------------------------------------
  * Stage entry points (the operator layer), each parity-testable against the
- * reference function named beside it.  Level rasters use the x-major level
- * layout described at the top; `B` pairs are processed per call.
+ * reference function named beside it.  Level rasters are row-major float64
+ * as described at the top; `B` pairs are processed per call.
  * ---------------------------------------------------------------------- */
 
 /* build_pyramid (core.py:106-128): levels 0..coarsest of B frames.
- *   levels_img[s]  : device B x (W>>s) x (H>>s) float64 (x-major) for every
- *                    s in 0..coarsest (NULL allowed for levels not wanted)
+ *   levels_img[s]  : device B x (H>>s) x (W>>s) float64 for every s in
+ *                    0..coarsest (levels_img[0] may be NULL: level 1 is then
+ *                    computed from the frames directly)
  *   levels_gx/gy[s]: gradients (image_gradients core.py:75-85), NULL = skip
  *   levels_dd[s]   : 4 consecutive rasters gxx, gxy, gyx, gyy
  *                    (_second_derivatives variational.py:168-171), NULL = skip
  *   status         : device uint32, OR-ed with DIS_STATUS_NONFINITE_INPUT */
-int dis_build_pyramid(const void* frames, int32_t dtype, int32_t B, int32_t H,
+DIS_API int dis_build_pyramid(const void* frames, int32_t dtype, int32_t B, int32_t H,
                       int32_t W, int32_t coarsest, double* const* levels_img,
                       double* const* levels_gx, double* const* levels_gy,
                       double* const* levels_dd, uint32_t* status, void* stream);
 
 /* init_patches + precompute_patch_set + optimize_patch_set + reset_outliers
  * + refresh_patch_stats for one scale (pipeline.py:54-82).
- *   ref_img/ref_gx/ref_gy/qry_img : level s, B x W x H x-major
- *   coarse_flow_u/v : level s+1 flow (B x Wc x Hc x-major) or NULL (zeros)
+ *   ref_img/ref_gx/ref_gy/qry_img : level s, B x H x W
+ *   coarse_flow_u/v : level s+1 flow (B x Hc x Wc) or NULL (zeros)
  *   out_u/out_v/out_off/out_mar : B x P_s, P_s in grid row-major order
  *   out_init_u/v (optional, may be NULL): B x P_s initial displacements
  *   out_valid (optional): B x P_s uint8 */
-int dis_patch_search(const double* ref_img, const double* ref_gx,
+DIS_API int dis_patch_search(const double* ref_img, const double* ref_gx,
                      const double* ref_gy, const double* qry_img, int32_t B,
                      int32_t W, int32_t H, const double* coarse_flow_u,
                      const double* coarse_flow_v, int32_t Wc, int32_t Hc,
@@ -176,19 +188,19 @@ int dis_patch_search(const double* ref_img, const double* ref_gx,
                      double* out_init_v, uint8_t* out_valid, void* stream);
 
 /* densify (densification.py:173-191): dense flow of level s. */
-int dis_densify(const double* ref_img, const double* qry_img, int32_t B,
+DIS_API int dis_densify(const double* ref_img, const double* qry_img, int32_t B,
                 int32_t W, int32_t H, const dis_params_t* p,
                 const double* patch_u, const double* patch_v,
                 const double* patch_off, double* flow_u, double* flow_v,
                 uint32_t* status, void* stream);
 
 /* Workspace for dis_refine on one level. */
-size_t dis_refine_workspace_bytes(int32_t B, int32_t W, int32_t H);
+DIS_API size_t dis_refine_workspace_bytes(int32_t B, int32_t W, int32_t H);
 
 /* refine (variational.py:220-275) in place on flow_u/flow_v, running
  * `outer_iters` fixed-point iterations (pass params->outer_iters_fixed or
  * scale_index + 1).  ref_dd/qry_dd: 4 rasters each (gxx, gxy, gyx, gyy). */
-int dis_refine(const double* ref_img, const double* ref_gx, const double* ref_gy,
+DIS_API int dis_refine(const double* ref_img, const double* ref_gx, const double* ref_gy,
                const double* ref_dd, const double* qry_img, const double* qry_gx,
                const double* qry_gy, const double* qry_dd, int32_t B, int32_t W,
                int32_t H, const dis_params_t* p, int32_t outer_iters,
@@ -196,21 +208,33 @@ int dis_refine(const double* ref_img, const double* ref_gx, const double* ref_gy
                size_t workspace_bytes, uint32_t* status, void* stream);
 
 /* upsample_flow (core.py:178-190) by the factor 2 from a W x H level to a
- * Wn x Hn level (x-major in and out). */
-int dis_upsample_flow(const double* in_u, const double* in_v, int32_t B,
+ * Wn x Hn level (planar u, v in and out). */
+DIS_API int dis_upsample_flow(const double* in_u, const double* in_v, int32_t B,
                       int32_t W, int32_t H, double* out_u, double* out_v,
                       int32_t Wn, int32_t Hn, void* stream);
 
 /* Patch grid (create_grid densification.py:58-79): number of window
  * origins per axis and the origins themselves (host memory).  Returns the
  * count, or a negative status. */
-int32_t dis_grid_axis(int32_t dim, int32_t patch_size, double overlap,
+DIS_API int32_t dis_grid_axis(int32_t dim, int32_t patch_size, double overlap,
                       int32_t* origins_out, int32_t max_out);
 
+/* ------------------------------------------------------------------------
+ * Instrumentation (not part of the reference interface; used by bench.py).
+ * ---------------------------------------------------------------------- */
+/* Kernels this library launched since the last dis_flow_batch() began. */
+DIS_API long long dis_last_launch_count(void);
+/* Per-stage CUDA-event timing: classes 0 pyramid, 1 patch search,
+ * 2 densify, 3 tensor+assemble, 4 SOR, 5 upsample. */
+DIS_API void dis_profile_enable(int32_t on);
+DIS_API void dis_profile_reset(void);
+/* Blocks on the recorded events; writes total ms and launch counts. */
+DIS_API int dis_profile_read(double* ms_out, int64_t* count_out, int32_t n_classes);
+
 /* Human-readable message of the last failing call on this host thread. */
-const char* dis_last_error(void);
+DIS_API const char* dis_last_error(void);
 /* DIS_B200_ABI_VERSION of the loaded library. */
-int32_t dis_abi_version(void);
+DIS_API int32_t dis_abi_version(void);
 
 #ifdef __cplusplus
 }

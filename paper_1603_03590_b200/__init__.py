@@ -1,0 +1,30 @@
+"""B200-native Dense Inverse Search optical flow (arXiv 1603.03590).
+
+Drop-in for the reference package's flow path (``disflow.dis_flow``,
+pipeline.py:150-163) with the same parameter set (``DisParams``,
+``VarParams``): the coarse-to-fine pyramid, inverse patch search,
+densification and variational refinement run as hand-written sm_100a CUDA
+kernels (``libdis_b200.so``, C ABI in ``include/dis_b200.h``), float64 in the
+reference's exact operation order, so the flow is bit-identical to the
+reference's on the same inputs.
+"""
+
+from .params import (
+    DisParams,
+    ParameterError,
+    VarParams,
+    coarsest_scale_for,
+)
+from .pipeline import FlowEngine, dis_flow, dis_flow_batch
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "DisParams",
+    "VarParams",
+    "ParameterError",
+    "coarsest_scale_for",
+    "FlowEngine",
+    "dis_flow",
+    "dis_flow_batch",
+]

@@ -1,0 +1,661 @@
+// api.cu — the C ABI (include/dis_b200.h): parameter validation, workspace
+// planning and the coarse-to-fine host loop (dis_flow / _dense_scales /
+// _upscale_to_full, pipeline.py:85-163) enqueueing the sm_100a kernels on one
+// stream.  Nothing here allocates device memory; nothing synchronizes except
+// the explicitly synchronous *_host / dis_read_status entry points.
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <mutex>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace disb200;
+
+// ---- instrumentation --------------------------------------------------------
+// Launch counter: every kernel launch made by this library bumps it;
+// dis_flow_batch resets it, so dis_last_launch_count() is the number of our
+// kernels one batch enqueued.
+// Profiler: when enabled, a CUDA event pair is recorded around every stage
+// launch on the launching stream; dis_profile_read() resolves them (after the
+// stream has completed) into per-class totals.
+namespace {
+std::atomic<long long> g_launches{0};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+struct EvPair {
+  cudaEvent_t a, b;
+  int cls;
+};
+std::vector<EvPair> g_prof_pending;
+std::vector<cudaEvent_t> g_prof_free;
+cudaEvent_t g_prof_open[KC_COUNT];
+double g_prof_ms[KC_COUNT];
+long long g_prof_n[KC_COUNT];
+
+cudaEvent_t prof_event() {
+  if (!g_prof_free.empty()) {
+    cudaEvent_t e = g_prof_free.back();
+    g_prof_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+namespace disb200 {
+void note_launch(int n) { g_launches += n; }
+void prof_begin(int cls, cudaStream_t st) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  if (!g_prof_on) return;
+  cudaEvent_t e = prof_event();
+  cudaEventRecord(e, st);
+  g_prof_open[cls] = e;
+}
+void prof_end(int cls, cudaStream_t st) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  if (!g_prof_on || !g_prof_open[cls]) return;
+  cudaEvent_t e = prof_event();
+  cudaEventRecord(e, st);
+  g_prof_pending.push_back({g_prof_open[cls], e, cls});
+  g_prof_open[cls] = nullptr;
+}
+}  // namespace disb200
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int check_cuda(const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(DIS_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+  return DIS_OK;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---- workspace plan -------------------------------------------------------
+struct Plan {
+  int B, H, W, ss, sf, ps;
+  bool var;
+  int hs[32], ws[32];
+  GridAxis ax[32], ay[32];
+  size_t off_status;
+  size_t off_img[2][32], off_gx[2][32], off_gy[2][32], off_dd[2][32];
+  size_t off_pu[32], off_pv[32], off_poff[32];
+  size_t off_fu[32], off_fv[32];
+  size_t off_rec;
+  size_t total;
+};
+
+constexpr size_t kNone = ~size_t(0);
+
+size_t take(size_t& cur, size_t bytes) {
+  size_t o = (cur + 255) & ~size_t(255);
+  cur = o + bytes;
+  return o;
+}
+
+void make_plan(const dis_params_t* p, int B, int H, int W, Plan* pl) {
+  pl->B = B;
+  pl->H = H;
+  pl->W = W;
+  pl->ss = p->coarsest_scale;
+  pl->sf = p->finest_scale;
+  pl->ps = p->patch_size;
+  pl->var = p->variational != 0;
+  const int sp = grid_spacing(p->patch_size, p->overlap);
+  for (int s = 0; s <= pl->ss; ++s) {
+    pl->hs[s] = H >> s;
+    pl->ws[s] = W >> s;
+    if (s >= pl->sf) {
+      pl->ax[s] = make_axis(pl->ws[s], pl->ps, sp);
+      pl->ay[s] = make_axis(pl->hs[s], pl->ps, sp);
+    }
+  }
+  size_t cur = 0;
+  pl->off_status = take(cur, 256);
+  const size_t d = sizeof(double);
+  for (int f = 0; f < 2; ++f)
+    for (int s = 0; s <= pl->ss; ++s) {
+      const size_t n = (size_t)B * pl->hs[s] * pl->ws[s];
+      const bool need_img = s >= 1 || pl->sf == 0;
+      pl->off_img[f][s] = need_img ? take(cur, n * d) : kNone;
+      const bool used = s >= pl->sf;
+      pl->off_gx[f][s] = used ? take(cur, n * d) : kNone;
+      pl->off_gy[f][s] = used ? take(cur, n * d) : kNone;
+      pl->off_dd[f][s] = (used && pl->var) ? take(cur, 4 * n * d) : kNone;
+    }
+  for (int s = pl->sf; s <= pl->ss; ++s) {
+    const size_t P = (size_t)B * pl->ax[s].n * pl->ay[s].n;
+    pl->off_pu[s] = take(cur, P * d);
+    pl->off_pv[s] = take(cur, P * d);
+    pl->off_poff[s] = take(cur, P * d);
+  }
+  for (int s = 1; s <= pl->ss; ++s) {  // dense flow of levels >= 1 (level 0 -> output)
+    const size_t n = (size_t)B * pl->hs[s] * pl->ws[s];
+    pl->off_fu[s] = take(cur, n * d);
+    pl->off_fv[s] = take(cur, n * d);
+  }
+  pl->off_fu[0] = pl->off_fv[0] = kNone;
+  if (pl->sf == 0) {  // full-resolution dense flow before interleaving
+    const size_t n = (size_t)B * H * W;
+    pl->off_fu[0] = take(cur, n * d);
+    pl->off_fv[0] = take(cur, n * d);
+  }
+  pl->off_rec = kNone;
+  if (pl->var) {
+    size_t mx = 0;
+    for (int s = pl->sf; s <= pl->ss; ++s) {
+      size_t r = refine_scratch_doubles(B, pl->ws[s], pl->hs[s]);
+      if (r > mx) mx = r;
+    }
+    pl->off_rec = take(cur, mx * d);
+  }
+  pl->total = (cur + 255) & ~size_t(255);
+}
+
+template <typename T>
+T* at(void* base, size_t off) {
+  return off == kNone ? nullptr : reinterpret_cast<T*>(static_cast<char*>(base) + off);
+}
+
+// validation mirroring dis_flow's checks (pipeline.py:150-163; core.py:65-72,
+// 106-128; pipeline.py:30-41)
+int check_dims(const dis_params_t* p, int B, int H, int W) {
+  if (B < 1) return fail(DIS_ERR_VALUE, "batch must hold at least one pair, got %d", B);
+  if (H < 1 || W < 1)
+    return fail(DIS_ERR_VALUE, "image must be 2D and non-empty, got shape (%d, %d)", H, W);
+  if (H < 2 || W < 2) return fail(DIS_ERR_VALUE, "image must be at least 2x2");
+  for (int s = 1; s <= p->coarsest_scale; ++s) {
+    if ((H >> s) < 2 || (W >> s) < 2)
+      return fail(DIS_ERR_VALUE,
+                  "downsampled level would be %dx%d; levels below 2 pixels per axis are not "
+                  "representable",
+                  W >> s, H >> s);
+  }
+  const int hc = H >> p->coarsest_scale, wc = W >> p->coarsest_scale;
+  if (wc < p->patch_size || hc < p->patch_size)
+    return fail(DIS_ERR_VALUE,
+                "coarsest level %dx%d cannot hold a %dpx patch; lower coarsest_scale", wc, hc,
+                p->patch_size);
+  if (p->variational && (H >> p->finest_scale) > 576)
+    return fail(DIS_ERR_VALUE,
+                "variational refinement of a level taller than 576 rows is not supported by "
+                "this build (level %d is %d rows)",
+                p->finest_scale, H >> p->finest_scale);
+  return DIS_OK;
+}
+
+int run_pipeline(const Plan& pl, const dis_params_t* p, double* out, void* ws,
+                 cudaStream_t st) {
+  uint32_t* status = at<uint32_t>(ws, pl.off_status);
+  double* prev_u = nullptr;
+  double* prev_v = nullptr;
+  int prev_w = 0, prev_h = 0;
+  for (int s = pl.ss; s >= pl.sf; --s) {
+    const int h = pl.hs[s], w = pl.ws[s];
+    double* ref = at<double>(ws, pl.off_img[0][s]);
+    double* qry = at<double>(ws, pl.off_img[1][s]);
+    SearchArgs a{};
+    a.ref = ref;
+    a.rgx = at<double>(ws, pl.off_gx[0][s]);
+    a.rgy = at<double>(ws, pl.off_gy[0][s]);
+    a.qry = qry;
+    a.B = pl.B;
+    a.W = w;
+    a.H = h;
+    a.cu = prev_u;
+    a.cv = prev_v;
+    a.Wc = prev_w;
+    a.Hc = prev_h;
+    a.ax = pl.ax[s];
+    a.ay = pl.ay[s];
+    a.ps = pl.ps;
+    a.iters = p->iterations;
+    a.mean_norm = p->use_mean_normalization;
+    a.code = p->residual_norm;
+    a.hb = p->huber_b;
+    a.out_u = at<double>(ws, pl.off_pu[s]);
+    a.out_v = at<double>(ws, pl.off_pv[s]);
+    a.out_off = at<double>(ws, pl.off_poff[s]);
+    launch_patch_search(a, st);
+    double* fu = at<double>(ws, pl.off_fu[s]);
+    double* fv = at<double>(ws, pl.off_fv[s]);
+    launch_densify(ref, qry, pl.B, w, h, pl.ax[s], pl.ay[s], pl.ps, a.out_u, a.out_v,
+                   a.out_off, fu, fv, status, st);
+    if (pl.var) {
+      RefineArgs r{};
+      r.ref = ref;
+      r.rgx = a.rgx;
+      r.rgy = a.rgy;
+      r.rdd = at<double>(ws, pl.off_dd[0][s]);
+      r.qry = qry;
+      r.qgx = at<double>(ws, pl.off_gx[1][s]);
+      r.qgy = at<double>(ws, pl.off_gy[1][s]);
+      r.qdd = at<double>(ws, pl.off_dd[1][s]);
+      r.B = pl.B;
+      r.W = w;
+      r.H = h;
+      r.delta = p->var_intensity_weight;
+      r.gamma = p->var_gradient_weight;
+      r.alpha = p->var_smoothness_weight;
+      r.eps = p->var_penalizer_eps;
+      r.omega = p->var_sor_omega;
+      r.sweeps = p->var_inner_sor_iters;
+      r.outer = p->outer_iters_fixed > 0 ? p->outer_iters_fixed : s + 1;
+      r.fu = fu;
+      r.fv = fv;
+      r.rec = at<double>(ws, pl.off_rec);
+      r.status = status;
+      int rc = launch_refine(r, st);
+      if (rc) return fail(rc, "refine: level %d (%dx%d) unsupported", s, w, h);
+    }
+    prev_u = fu;
+    prev_v = fv;
+    prev_w = w;
+    prev_h = h;
+  }
+  // _upscale_to_full (pipeline.py:129-133)
+  if (pl.sf == 0) {
+    launch_interleave(prev_u, prev_v, pl.B, pl.W, pl.H, out, st);
+  } else {
+    for (int s = pl.sf; s > 0; --s) {
+      const int hn = pl.hs[s - 1], wn = pl.ws[s - 1];
+      if (s - 1 == 0) {
+        launch_upsample(prev_u, prev_v, pl.B, prev_w, prev_h, nullptr, nullptr, out, wn, hn,
+                        st);
+      } else {
+        double* nu = at<double>(ws, pl.off_fu[s - 1]);
+        double* nv = at<double>(ws, pl.off_fv[s - 1]);
+        launch_upsample(prev_u, prev_v, pl.B, prev_w, prev_h, nu, nv, nullptr, wn, hn, st);
+        prev_u = nu;
+        prev_v = nv;
+        prev_w = wn;
+        prev_h = hn;
+      }
+    }
+  }
+  return check_cuda("dis_flow_batch");
+}
+
+void build_pyramids(const Plan& pl, const void* f1, const void* f2, int dtype, void* ws,
+                    cudaStream_t st) {
+  uint32_t* status = at<uint32_t>(ws, pl.off_status);
+  for (int f = 0; f < 2; ++f) {
+    double* img[32];
+    double* gx[32];
+    double* gy[32];
+    double* dd[32];
+    for (int s = 0; s <= pl.ss; ++s) {
+      img[s] = at<double>(ws, pl.off_img[f][s]);
+      gx[s] = at<double>(ws, pl.off_gx[f][s]);
+      gy[s] = at<double>(ws, pl.off_gy[f][s]);
+      dd[s] = at<double>(ws, pl.off_dd[f][s]);
+    }
+    launch_pyramid(f ? f2 : f1, dtype, pl.B, pl.H, pl.W, pl.ss, img, gx, gy, dd, status, st);
+  }
+}
+
+size_t dtype_size(int dtype) {
+  return dtype == DIS_DTYPE_F32 ? 4 : dtype == DIS_DTYPE_F64 ? 8 : 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dis_last_error(void) { return g_last_error.c_str(); }
+
+long long dis_last_launch_count(void) { return g_launches.load(); }
+
+void dis_profile_enable(int32_t on) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof_on = on != 0;
+}
+
+void dis_profile_reset(void) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  for (auto& p : g_prof_pending) {
+    g_prof_free.push_back(p.a);
+    g_prof_free.push_back(p.b);
+  }
+  g_prof_pending.clear();
+  for (int c = 0; c < KC_COUNT; ++c) {
+    g_prof_ms[c] = 0.0;
+    g_prof_n[c] = 0;
+    g_prof_open[c] = nullptr;
+  }
+}
+
+int dis_profile_read(double* ms_out, int64_t* count_out, int32_t n_classes) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  for (auto& p : g_prof_pending) {
+    cudaError_t e = cudaEventSynchronize(p.b);
+    if (e != cudaSuccess) return fail(DIS_ERR_CUDA, "profile: %s", cudaGetErrorString(e));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    g_prof_ms[p.cls] += ms;
+    g_prof_n[p.cls] += 1;
+    g_prof_free.push_back(p.a);
+    g_prof_free.push_back(p.b);
+  }
+  g_prof_pending.clear();
+  for (int c = 0; c < n_classes && c < KC_COUNT; ++c) {
+    ms_out[c] = g_prof_ms[c];
+    count_out[c] = g_prof_n[c];
+  }
+  return DIS_OK;
+}
+int32_t dis_abi_version(void) { return DIS_B200_ABI_VERSION; }
+
+void dis_params_default(dis_params_t* p) {
+  std::memset(p, 0, sizeof *p);
+  p->patch_size = 8;
+  p->iterations = 12;
+  p->finest_scale = 3;
+  p->coarsest_scale = 5;
+  p->downscale = 2;
+  p->use_mean_normalization = 1;
+  p->use_densification = 1;
+  p->residual_norm = DIS_NORM_L2;
+  p->overlap = 0.40;
+  p->huber_b = 1.0;
+  p->variational = 1;
+  p->var_inner_sor_iters = 5;
+  p->var_intensity_weight = 5.0;
+  p->var_gradient_weight = 10.0;
+  p->var_smoothness_weight = 10.0;
+  p->var_penalizer_eps = 0.001;
+  p->var_sor_omega = 1.6;
+  p->outer_iters_fixed = 0;
+}
+
+int dis_params_validate(const dis_params_t* p) {
+  if (!p) return fail(DIS_ERR_PARAMETER, "params is NULL");
+  if (p->patch_size < 2) return fail(DIS_ERR_PARAMETER, "patch_size must be >= 2");
+  if (!(p->overlap >= 0.0 && p->overlap < 1.0))
+    return fail(DIS_ERR_PARAMETER, "overlap must lie in [0, 1)");
+  if (p->iterations < 1) return fail(DIS_ERR_PARAMETER, "iterations must be >= 1");
+  if (p->finest_scale < 0 || p->coarsest_scale < p->finest_scale)
+    return fail(DIS_ERR_PARAMETER, "need 0 <= finest_scale <= coarsest_scale");
+  if (p->coarsest_scale > 30) return fail(DIS_ERR_PARAMETER, "coarsest_scale too large");
+  if (p->downscale < 2) return fail(DIS_ERR_PARAMETER, "downscale must be an integer >= 2");
+  if (p->downscale != 2)
+    return fail(DIS_ERR_PARAMETER, "this path implements downscale == 2 only");
+  if (p->residual_norm < 0 || p->residual_norm > 2)
+    return fail(DIS_ERR_PARAMETER, "residual_norm must be one of ('l2', 'l1', 'huber')");
+  if (p->residual_norm == DIS_NORM_HUBER && !(p->huber_b > 0))
+    return fail(DIS_ERR_PARAMETER, "huber_b must be > 0");
+  if (p->mode != 0 && p->mode != 1) return fail(DIS_ERR_PARAMETER, "mode must be 'flow' or 'stereo'");
+  if (p->mode == 1 && p->bidirectional)
+    return fail(DIS_ERR_PARAMETER, "bidirectional matching is not defined for stereo mode");
+  if (p->variational) {
+    if (p->var_intensity_weight < 0 || p->var_gradient_weight < 0 ||
+        p->var_smoothness_weight < 0)
+      return fail(DIS_ERR_PARAMETER, "variational weights must be >= 0");
+    if (p->var_inner_sor_iters < 1) return fail(DIS_ERR_PARAMETER, "inner_sor_iters must be >= 1");
+    if (!(p->var_penalizer_eps > 0)) return fail(DIS_ERR_PARAMETER, "penalizer_eps must be > 0");
+    if (!(p->var_sor_omega > 0.0 && p->var_sor_omega < 2.0))
+      return fail(DIS_ERR_PARAMETER, "sor_omega must lie in (0, 2)");
+  }
+  if (p->mode == 1) return fail(DIS_ERR_VALUE, "use dis_stereo for stereo-mode parameters");
+  if (p->bidirectional)
+    return fail(DIS_ERR_PARAMETER, "bidirectional densification is not implemented by this path");
+  return DIS_OK;
+}
+
+size_t dis_workspace_bytes(int32_t B, int32_t H, int32_t W, const dis_params_t* p) {
+  if (dis_params_validate(p) || check_dims(p, B, H, W)) return 0;
+  Plan pl;
+  make_plan(p, B, H, W, &pl);
+  return pl.total;
+}
+
+size_t dis_host_workspace_bytes(int32_t B, int32_t H, int32_t W, int32_t dtype,
+                                const dis_params_t* p) {
+  size_t base = dis_workspace_bytes(B, H, W, p);
+  if (!base) return 0;
+  size_t cur = base;
+  const size_t frames = (size_t)B * H * W * dtype_size(dtype);
+  take(cur, frames);
+  take(cur, frames);
+  take(cur, (size_t)B * H * W * 2 * sizeof(double));
+  return (cur + 255) & ~size_t(255);
+}
+
+int dis_flow_batch(const void* frame1, const void* frame2, int32_t dtype, int32_t B, int32_t H,
+                   int32_t W, const dis_params_t* p, double* flow_out, void* workspace,
+                   size_t workspace_bytes, void* stream) {
+  int rc = dis_params_validate(p);
+  if (rc) return rc;
+  if (dtype < 0 || dtype > 2) return fail(DIS_ERR_VALUE, "unsupported frame dtype %d", dtype);
+  rc = check_dims(p, B, H, W);
+  if (rc) return rc;
+  Plan pl;
+  make_plan(p, B, H, W, &pl);
+  if (workspace_bytes < pl.total)
+    return fail(DIS_ERR_WORKSPACE, "workspace holds %zu bytes, need %zu", workspace_bytes,
+                pl.total);
+  cudaStream_t st = as_stream(stream);
+  g_launches = 0;
+  cudaMemsetAsync(at<char>(workspace, pl.off_status), 0, 256, st);
+  build_pyramids(pl, frame1, frame2, dtype, workspace, st);
+  rc = check_cuda("pyramid");
+  if (rc) return rc;
+  return run_pipeline(pl, p, flow_out, workspace, st);
+}
+
+int dis_read_status(const void* workspace, uint32_t* status_out, void* stream) {
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = cudaMemcpyAsync(status_out, workspace, sizeof(uint32_t),
+                                  cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return fail(DIS_ERR_CUDA, "dis_read_status: %s", cudaGetErrorString(e));
+  return DIS_OK;
+}
+
+int dis_status_to_error(uint32_t status) {
+  if (status & DIS_STATUS_NONFINITE_INPUT)
+    return fail(DIS_ERR_VALUE, "image contains non-finite values");
+  if (status & DIS_STATUS_COVERAGE)
+    return fail(DIS_ERR_COVERAGE, "pixel without a contributing patch; grid coverage broken");
+  if (status & DIS_STATUS_NONFINITE_FLOW)
+    return fail(DIS_ERR_NONFINITE, "variational refinement produced a non-finite value");
+  return DIS_OK;
+}
+
+int dis_flow_batch_host(const void* host_frame1, const void* host_frame2, int32_t dtype,
+                        int32_t B, int32_t H, int32_t W, const dis_params_t* p,
+                        double* host_flow_out, void* workspace, size_t workspace_bytes,
+                        void* stream) {
+  int rc = dis_params_validate(p);
+  if (rc) return rc;
+  if (dtype < 0 || dtype > 2) return fail(DIS_ERR_VALUE, "unsupported frame dtype %d", dtype);
+  rc = check_dims(p, B, H, W);
+  if (rc) return rc;
+  const size_t need = dis_host_workspace_bytes(B, H, W, dtype, p);
+  if (workspace_bytes < need)
+    return fail(DIS_ERR_WORKSPACE, "workspace holds %zu bytes, need %zu", workspace_bytes, need);
+  Plan pl;
+  make_plan(p, B, H, W, &pl);
+  size_t cur = pl.total;
+  const size_t fbytes = (size_t)B * H * W * dtype_size(dtype);
+  const size_t obytes = (size_t)B * H * W * 2 * sizeof(double);
+  char* base = static_cast<char*>(workspace);
+  void* d1 = base + take(cur, fbytes);
+  void* d2 = base + take(cur, fbytes);
+  double* dout = reinterpret_cast<double*>(base + take(cur, obytes));
+  cudaStream_t st = as_stream(stream);
+  cudaMemcpyAsync(d1, host_frame1, fbytes, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d2, host_frame2, fbytes, cudaMemcpyHostToDevice, st);
+  rc = dis_flow_batch(d1, d2, dtype, B, H, W, p, dout, workspace, pl.total, stream);
+  if (rc) return rc;
+  cudaMemcpyAsync(host_flow_out, dout, obytes, cudaMemcpyDeviceToHost, st);
+  uint32_t status = 0;
+  rc = dis_read_status(workspace, &status, stream);
+  if (rc) return rc;
+  return dis_status_to_error(status);
+}
+
+// ---- stage entry points -----------------------------------------------------
+
+int dis_build_pyramid(const void* frames, int32_t dtype, int32_t B, int32_t H, int32_t W,
+                      int32_t coarsest, double* const* levels_img, double* const* levels_gx,
+                      double* const* levels_gy, double* const* levels_dd, uint32_t* status,
+                      void* stream) {
+  if (coarsest < 0) return fail(DIS_ERR_PARAMETER, "coarsest_scale must be >= 0");
+  if (H < 2 || W < 2) return fail(DIS_ERR_VALUE, "image must be at least 2x2");
+  for (int s = 1; s <= coarsest; ++s)
+    if ((H >> s) < 2 || (W >> s) < 2)
+      return fail(DIS_ERR_VALUE, "downsampled level would be %dx%d", W >> s, H >> s);
+  if (!levels_img) return fail(DIS_ERR_VALUE, "levels_img is NULL");
+  for (int s = 1; s <= coarsest; ++s)
+    if (!levels_img[s]) return fail(DIS_ERR_VALUE, "levels_img[%d] is NULL", s);
+  std::vector<double*> gx(coarsest + 1, nullptr), gy(coarsest + 1, nullptr);
+  for (int s = 0; s <= coarsest; ++s) {
+    if (levels_gx) gx[s] = levels_gx[s];
+    if (levels_gy) gy[s] = levels_gy[s];
+    if ((gx[s] || gy[s] || (levels_dd && levels_dd[s])) && !levels_img[s])
+      return fail(DIS_ERR_VALUE, "gradients of level %d need its image", s);
+  }
+  launch_pyramid(frames, dtype, B, H, W, coarsest, levels_img, gx.data(), gy.data(), levels_dd,
+                 status, as_stream(stream));
+  return check_cuda("dis_build_pyramid");
+}
+
+int32_t dis_grid_axis(int32_t dim, int32_t patch_size, double overlap, int32_t* origins_out,
+                      int32_t max_out) {
+  if (!(overlap >= 0.0 && overlap < 1.0)) return fail(DIS_ERR_VALUE, "overlap must lie in [0, 1)");
+  if (dim < patch_size)
+    return fail(DIS_ERR_VALUE, "level %d is smaller than the patch size %d", dim, patch_size);
+  GridAxis a = make_axis(dim, patch_size, grid_spacing(patch_size, overlap));
+  if (origins_out)
+    for (int j = 0; j < a.n && j < max_out; ++j) origins_out[j] = a.origin(j);
+  return a.n;
+}
+
+int dis_patch_search(const double* ref_img, const double* ref_gx, const double* ref_gy,
+                     const double* qry_img, int32_t B, int32_t W, int32_t H,
+                     const double* coarse_flow_u, const double* coarse_flow_v, int32_t Wc,
+                     int32_t Hc, const dis_params_t* p, double* out_u, double* out_v,
+                     double* out_off, double* out_mar, double* out_init_u, double* out_init_v,
+                     uint8_t* out_valid, void* stream) {
+  if (dis_params_validate(p)) return DIS_ERR_PARAMETER;
+  if (W < p->patch_size || H < p->patch_size)
+    return fail(DIS_ERR_VALUE, "level %dx%d is smaller than the patch size %d", W, H,
+                p->patch_size);
+  const int sp = grid_spacing(p->patch_size, p->overlap);
+  SearchArgs a{};
+  a.ref = ref_img;
+  a.rgx = ref_gx;
+  a.rgy = ref_gy;
+  a.qry = qry_img;
+  a.B = B;
+  a.W = W;
+  a.H = H;
+  a.cu = coarse_flow_u;
+  a.cv = coarse_flow_v;
+  a.Wc = Wc;
+  a.Hc = Hc;
+  a.ax = make_axis(W, p->patch_size, sp);
+  a.ay = make_axis(H, p->patch_size, sp);
+  a.ps = p->patch_size;
+  a.iters = p->iterations;
+  a.mean_norm = p->use_mean_normalization;
+  a.code = p->residual_norm;
+  a.hb = p->huber_b;
+  a.out_u = out_u;
+  a.out_v = out_v;
+  a.out_off = out_off;
+  a.out_mar = out_mar;
+  a.out_iu = out_init_u;
+  a.out_iv = out_init_v;
+  a.out_valid = out_valid;
+  launch_patch_search(a, as_stream(stream));
+  return check_cuda("dis_patch_search");
+}
+
+int dis_densify(const double* ref_img, const double* qry_img, int32_t B, int32_t W, int32_t H,
+                const dis_params_t* p, const double* patch_u, const double* patch_v,
+                const double* patch_off, double* flow_u, double* flow_v, uint32_t* status,
+                void* stream) {
+  if (dis_params_validate(p)) return DIS_ERR_PARAMETER;
+  if (W < p->patch_size || H < p->patch_size)
+    return fail(DIS_ERR_VALUE, "level %dx%d is smaller than the patch size %d", W, H,
+                p->patch_size);
+  const int sp = grid_spacing(p->patch_size, p->overlap);
+  launch_densify(ref_img, qry_img, B, W, H, make_axis(W, p->patch_size, sp),
+                 make_axis(H, p->patch_size, sp), p->patch_size, patch_u, patch_v, patch_off,
+                 flow_u, flow_v, status, as_stream(stream));
+  return check_cuda("dis_densify");
+}
+
+size_t dis_refine_workspace_bytes(int32_t B, int32_t W, int32_t H) {
+  return refine_scratch_doubles(B, W, H) * sizeof(double);
+}
+
+int dis_refine(const double* ref_img, const double* ref_gx, const double* ref_gy,
+               const double* ref_dd, const double* qry_img, const double* qry_gx,
+               const double* qry_gy, const double* qry_dd, int32_t B, int32_t W, int32_t H,
+               const dis_params_t* p, int32_t outer_iters, double* flow_u, double* flow_v,
+               void* workspace, size_t workspace_bytes, uint32_t* status, void* stream) {
+  if (dis_params_validate(p)) return DIS_ERR_PARAMETER;
+  if (workspace_bytes < dis_refine_workspace_bytes(B, W, H))
+    return fail(DIS_ERR_WORKSPACE, "refine workspace too small");
+  if (H > 576)
+    return fail(DIS_ERR_VALUE, "variational refinement of a level taller than 576 rows is not "
+                               "supported by this build");
+  RefineArgs r{};
+  r.ref = ref_img;
+  r.rgx = ref_gx;
+  r.rgy = ref_gy;
+  r.rdd = ref_dd;
+  r.qry = qry_img;
+  r.qgx = qry_gx;
+  r.qgy = qry_gy;
+  r.qdd = qry_dd;
+  r.B = B;
+  r.W = W;
+  r.H = H;
+  r.delta = p->var_intensity_weight;
+  r.gamma = p->var_gradient_weight;
+  r.alpha = p->var_smoothness_weight;
+  r.eps = p->var_penalizer_eps;
+  r.omega = p->var_sor_omega;
+  r.sweeps = p->var_inner_sor_iters;
+  r.outer = outer_iters;
+  r.fu = flow_u;
+  r.fv = flow_v;
+  r.rec = static_cast<double*>(workspace);
+  r.status = status;
+  int rc = launch_refine(r, as_stream(stream));
+  if (rc) return fail(rc, "refine launch failed");
+  return check_cuda("dis_refine");
+}
+
+int dis_upsample_flow(const double* in_u, const double* in_v, int32_t B, int32_t W, int32_t H,
+                      double* out_u, double* out_v, int32_t Wn, int32_t Hn, void* stream) {
+  launch_upsample(in_u, in_v, B, W, H, out_u, out_v, nullptr, Wn, Hn, as_stream(stream));
+  return check_cuda("dis_upsample_flow");
+}
+
+}  // extern "C"

@@ -1,0 +1,90 @@
+// kernels.cuh — host-side launchers of the DIS kernels (one per stage).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace disb200 {
+
+// ---- instrumentation (api.cu) ----
+// Kernel classes timed by the optional per-stage CUDA-event profiler and
+// counted by the launch counter (dis_profile_*, dis_last_launch_count).
+enum KernelClass {
+  KC_PYRAMID = 0,
+  KC_SEARCH = 1,
+  KC_DENSIFY = 2,
+  KC_TENSOR = 3,
+  KC_SOR = 4,
+  KC_UPSAMPLE = 5,
+  KC_COUNT = 6
+};
+void prof_begin(int cls, cudaStream_t st);
+void prof_end(int cls, cudaStream_t st);
+void note_launch(int n = 1);
+
+// pyramid.cu
+void launch_pyramid(const void* frames, int dtype, int B, int H, int W, int coarsest,
+                    double* const* img, double* const* gx, double* const* gy,
+                    double* const* dd, uint32_t* status, cudaStream_t st);
+
+// patch_search.cu — init + precompute + condition + GN + reset + refresh
+struct SearchArgs {
+  const double* ref;
+  const double* rgx;
+  const double* rgy;
+  const double* qry;
+  int B, W, H;
+  const double* cu;  // coarse flow (level s+1), row-major planar, or null
+  const double* cv;
+  int Wc, Hc;
+  GridAxis ax, ay;
+  int ps, iters, mean_norm, code;
+  double hb;
+  double* out_u;
+  double* out_v;
+  double* out_off;
+  double* out_mar;    // optional
+  double* out_iu;     // optional
+  double* out_iv;     // optional
+  uint8_t* out_valid; // optional
+  int32_t* out_evals; // optional
+};
+void launch_patch_search(const SearchArgs& a, cudaStream_t st);
+
+// densify.cu
+void launch_densify(const double* ref, const double* qry, int B, int W, int H, GridAxis ax,
+                    GridAxis ay, int ps, const double* pu, const double* pv,
+                    const double* poff, double* fu, double* fv, uint32_t* status,
+                    cudaStream_t st);
+
+// variational.cu
+struct RefineArgs {
+  const double* ref;
+  const double* rgx;
+  const double* rgy;
+  const double* rdd;
+  const double* qry;
+  const double* qgx;
+  const double* qgy;
+  const double* qdd;
+  int B, W, H;
+  double delta, gamma, alpha, eps, omega;
+  int sweeps, outer;
+  double* fu;  // flow, row-major planar, refined in place
+  double* fv;
+  double* rec;  // 8 * B * (W + H - 1) * H doubles of scratch
+  uint32_t* status;
+};
+size_t refine_scratch_doubles(int B, int W, int H);
+int launch_refine(const RefineArgs& a, cudaStream_t st);
+
+// upsample.cu — upsample_flow by 2 (planar in, planar or interleaved out)
+void launch_upsample(const double* iu, const double* iv, int B, int W, int H, double* ou,
+                     double* ov, double* out_interleaved, int Wn, int Hn, cudaStream_t st);
+void launch_interleave(const double* u, const double* v, int B, int W, int H, double* out,
+                       cudaStream_t st);
+
+}  // namespace disb200

@@ -1,0 +1,208 @@
+// pyramid.cu — image pyramid + gradient rasters (reference core.py:65-128,
+// variational.py:168-171).
+//
+//   level 0     = the frame converted to float64 (as_image, core.py:65-72)
+//   level s > 0 = 2x2 box mean of level s-1, ((a+b)+(c+d))/4, dims floored
+//                 (_box_downsample, core.py:88-98)
+//   gx, gy      = central differences [-0.5, 0, 0.5] with one-sided borders
+//                 (image_gradients, core.py:75-85), only at the levels the
+//                 flow path reads (finest..coarsest; Appendix A.9: the
+//                 reference computes the others but never reads them)
+//   dd          = gradients of gx and gy (gxx, gxy, gyx, gyy) for the
+//                 variational stage (_second_derivatives,
+//                 variational.py:168-171), evaluated from the image with the
+//                 same border rules, so they are bit-identical.
+//
+// All rasters row-major float64; HBM-bound elementwise/stencil kernels, one
+// thread per output pixel, rows read coalesced.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace disb200 {
+
+template <typename T>
+__device__ __forceinline__ double to_f64(T v) {
+  return (double)v;
+}
+
+__device__ __forceinline__ bool finite_f64(double v) { return isfinite(v); }
+
+// level 0 (convert) from the frames; also the finiteness check of as_image
+template <typename T>
+__global__ void k_level0(const T* __restrict__ frames, int B, int H, int W,
+                         double* __restrict__ out, uint32_t* status) {
+  size_t n = (size_t)B * H * W;
+  bool bad = false;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    double v = to_f64(frames[i]);
+    bad |= !finite_f64(v);
+    if (out) out[i] = v;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) set_status(status, DIS_STATUS_NONFINITE_INPUT);
+}
+
+// level 1 straight from the frames (no float64 level-0 copy needed when the
+// finest scale is >= 1): ((a+b)+(c+d))/4 of the converted pixels
+template <typename T>
+__global__ void k_level1_from_frames(const T* __restrict__ frames, int B, int H, int W,
+                                     double* __restrict__ out) {
+  int Ho = H / 2, Wo = W / 2;
+  size_t n = (size_t)B * Ho * Wo;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    int X = (int)(i % Wo);
+    size_t t = i / Wo;
+    int Y = (int)(t % Ho);
+    int b = (int)(t / Ho);
+    const T* r0 = frames + ((size_t)b * H + 2 * Y) * W + 2 * X;
+    const T* r1 = r0 + W;
+    double a = to_f64(r0[0]), bb = to_f64(r0[1]), c = to_f64(r1[0]), d = to_f64(r1[1]);
+    out[i] = ((a + bb) + (c + d)) / 4.0;
+  }
+}
+
+// level s from level s-1 (both float64 row-major)
+__global__ void k_downsample(const double* __restrict__ in, int B, int H, int W,
+                             double* __restrict__ out) {
+  int Ho = H / 2, Wo = W / 2;
+  size_t n = (size_t)B * Ho * Wo;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    int X = (int)(i % Wo);
+    size_t t = i / Wo;
+    int Y = (int)(t % Ho);
+    int b = (int)(t / Ho);
+    const double* r0 = in + ((size_t)b * H + 2 * Y) * W + 2 * X;
+    const double* r1 = r0 + W;
+    double a = r0[0], bb = r0[1], c = r1[0], d = r1[1];
+    out[i] = ((a + bb) + (c + d)) / 4.0;
+  }
+}
+
+// gradient of a raster along x / y with the reference's border rules
+struct RowGrad {
+  const double* img;
+  int W, H;
+  __device__ __forceinline__ double v(int x, int y) const { return img[(size_t)y * W + x]; }
+  __device__ __forceinline__ double gx(int x, int y) const {
+    if (x == 0) return 0.5 * (v(1, y) - v(0, y));
+    if (x == W - 1) return 0.5 * (v(W - 1, y) - v(W - 2, y));
+    return 0.5 * (v(x + 1, y) - v(x - 1, y));
+  }
+  __device__ __forceinline__ double gy(int x, int y) const {
+    if (y == 0) return 0.5 * (v(x, 1) - v(x, 0));
+    if (y == H - 1) return 0.5 * (v(x, H - 1) - v(x, H - 2));
+    return 0.5 * (v(x, y + 1) - v(x, y - 1));
+  }
+  // x-gradient of gx, y-gradient of gx, x-gradient of gy, y-gradient of gy
+  __device__ __forceinline__ double gxx(int x, int y) const {
+    if (x == 0) return 0.5 * (gx(1, y) - gx(0, y));
+    if (x == W - 1) return 0.5 * (gx(W - 1, y) - gx(W - 2, y));
+    return 0.5 * (gx(x + 1, y) - gx(x - 1, y));
+  }
+  __device__ __forceinline__ double gxy(int x, int y) const {
+    if (y == 0) return 0.5 * (gx(x, 1) - gx(x, 0));
+    if (y == H - 1) return 0.5 * (gx(x, H - 1) - gx(x, H - 2));
+    return 0.5 * (gx(x, y + 1) - gx(x, y - 1));
+  }
+  __device__ __forceinline__ double gyx(int x, int y) const {
+    if (x == 0) return 0.5 * (gy(1, y) - gy(0, y));
+    if (x == W - 1) return 0.5 * (gy(W - 1, y) - gy(W - 2, y));
+    return 0.5 * (gy(x + 1, y) - gy(x - 1, y));
+  }
+  __device__ __forceinline__ double gyy(int x, int y) const {
+    if (y == 0) return 0.5 * (gy(x, 1) - gy(x, 0));
+    if (y == H - 1) return 0.5 * (gy(x, H - 1) - gy(x, H - 2));
+    return 0.5 * (gy(x, y + 1) - gy(x, y - 1));
+  }
+};
+
+__global__ void k_gradients(const double* __restrict__ img, int B, int H, int W,
+                            double* __restrict__ gx, double* __restrict__ gy,
+                            double* __restrict__ dd) {
+  size_t plane = (size_t)H * W;
+  size_t n = (size_t)B * plane;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    int b = (int)(i / plane);
+    size_t p = i - (size_t)b * plane;
+    int y = (int)(p / W);
+    int x = (int)(p - (size_t)y * W);
+    RowGrad g{img + (size_t)b * plane, W, H};
+    if (gx) gx[i] = g.gx(x, y);
+    if (gy) gy[i] = g.gy(x, y);
+    if (dd) {
+      double* d = dd + (size_t)b * 4 * plane + p;
+      d[0] = g.gxx(x, y);
+      d[plane] = g.gxy(x, y);
+      d[2 * plane] = g.gyx(x, y);
+      d[3 * plane] = g.gyy(x, y);
+    }
+  }
+}
+
+static inline int grid_for(size_t n, int threads) {
+  size_t blocks = (n + threads - 1) / threads;
+  size_t cap = 148 * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return (int)blocks;
+}
+
+template <typename T>
+static void launch_pyramid_t(const T* frames, int B, int H, int W, int coarsest,
+                             double* const* img, double* const* gx, double* const* gy,
+                             double* const* dd, uint32_t* status, cudaStream_t st) {
+  const int TH = 256;
+  prof_begin(KC_PYRAMID, st);
+  // level 0 (and the finiteness check over every input pixel)
+  size_t n0 = (size_t)B * H * W;
+  k_level0<T><<<grid_for(n0, TH), TH, 0, st>>>(frames, B, H, W, img[0], status);
+  note_launch();
+  int h = H, w = W;
+  for (int s = 1; s <= coarsest; ++s) {
+    int ho = h / 2, wo = w / 2;
+    size_t n = (size_t)B * ho * wo;
+    if (s == 1 && img[0] == nullptr) {
+      k_level1_from_frames<T><<<grid_for(n, TH), TH, 0, st>>>(frames, B, H, W, img[1]);
+    } else {
+      k_downsample<<<grid_for(n, TH), TH, 0, st>>>(img[s - 1], B, h, w, img[s]);
+    }
+    note_launch();
+    h = ho;
+    w = wo;
+  }
+  h = H;
+  w = W;
+  for (int s = 0; s <= coarsest; ++s) {
+    if (gx[s] || gy[s] || (dd && dd[s])) {
+      size_t n = (size_t)B * h * w;
+      k_gradients<<<grid_for(n, TH), TH, 0, st>>>(img[s], B, h, w, gx[s], gy[s],
+                                                    dd ? dd[s] : nullptr);
+      note_launch();
+    }
+    h /= 2;
+    w /= 2;
+  }
+  prof_end(KC_PYRAMID, st);
+}
+
+void launch_pyramid(const void* frames, int dtype, int B, int H, int W, int coarsest,
+                    double* const* img, double* const* gx, double* const* gy,
+                    double* const* dd, uint32_t* status, cudaStream_t st) {
+  switch (dtype) {
+    case DIS_DTYPE_F32:
+      launch_pyramid_t((const float*)frames, B, H, W, coarsest, img, gx, gy, dd, status, st);
+      break;
+    case DIS_DTYPE_F64:
+      launch_pyramid_t((const double*)frames, B, H, W, coarsest, img, gx, gy, dd, status, st);
+      break;
+    default:
+      launch_pyramid_t((const uint8_t*)frames, B, H, W, coarsest, img, gx, gy, dd, status,
+                       st);
+      break;
+  }
+}
+
+}  // namespace disb200

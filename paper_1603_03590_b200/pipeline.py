@@ -1,0 +1,216 @@
+"""Host side of the DIS flow path: the reference's public entry points
+(``dis_flow``, pipeline.py:150-163) on top of the sm_100a kernels in
+libdis_b200.so.
+
+The coarse-to-fine loop itself (pipeline.py:85-133) runs inside the C ABI
+(``dis_flow_batch``), which enqueues every kernel of every scale for a whole
+batch of pairs on one CUDA stream.  PyTorch provides device memory and
+streams only.  There is no CPU fallback: without a CUDA device and the built
+library these functions raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .params import DisParams, ParameterError, to_c
+
+_TORCH_DT = None
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _require_cuda():
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "paper_1603_03590_b200 runs on a CUDA device (B200, sm_100a); "
+            "no CUDA device is visible and there is no CPU fallback")
+    return torch
+
+
+def _dtype_code(t):
+    torch = _torch()
+    if t.dtype == torch.float32:
+        return _lib.DTYPE_F32
+    if t.dtype == torch.float64:
+        return _lib.DTYPE_F64
+    if t.dtype == torch.uint8:
+        return _lib.DTYPE_U8
+    raise TypeError(t.dtype)
+
+
+def _to_device_frames(x, device):
+    """(B, H, W) or (H, W) real raster -> contiguous CUDA tensor of a dtype the
+    kernels take (f32/f64/u8; anything else is converted to float64 exactly
+    like as_image, core.py:65-72)."""
+    torch = _torch()
+    if isinstance(x, torch.Tensor):
+        t = x
+    else:
+        a = np.asarray(x)
+        if a.dtype not in (np.float32, np.float64, np.uint8):
+            a = a.astype(np.float64)
+        t = torch.from_numpy(np.ascontiguousarray(a))
+    if t.dtype not in (torch.float32, torch.float64, torch.uint8):
+        t = t.to(torch.float64)
+    return t.to(device=device, non_blocking=True).contiguous()
+
+
+class FlowEngine:
+    """A reusable device workspace for batches of ``B`` pairs of ``H x W``
+    frames at one parameter set (the workspace layout is fixed by
+    ``dis_workspace_bytes``)."""
+
+    def __init__(self, batch: int, height: int, width: int, params: DisParams | None = None,
+                 device=None):
+        torch = _require_cuda()
+        self.params = params if params is not None else DisParams.preset(2)
+        self.params.validate()
+        if self.params.mode == "stereo":
+            raise ValueError("use dis_stereo for stereo-mode parameters")
+        self.B, self.H, self.W = int(batch), int(height), int(width)
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        self.cparams = to_c(self.params)
+        L = _lib.lib()
+        _lib.check(L.dis_params_validate(ctypes.byref(self.cparams)))
+        n = L.dis_workspace_bytes(self.B, self.H, self.W, ctypes.byref(self.cparams))
+        if n == 0:  # re-run the checks to raise the precise error
+            _lib.check(L.dis_flow_batch(None, None, 0, self.B, self.H, self.W,
+                                        ctypes.byref(self.cparams), None, None, 0, None))
+            raise ValueError("invalid problem size")
+        self.workspace_bytes = int(n)
+        self.workspace = torch.empty(self.workspace_bytes, dtype=torch.uint8,
+                                     device=self.device)
+        self._host_ws = None
+
+    # -- device-resident path ------------------------------------------------
+    def run(self, frames1, frames2, out=None, stream=None, check: bool = True):
+        """Flow of every pair: (B, H, W, 2) float64 CUDA tensor.  ``frames*``
+        are (B, H, W) CUDA tensors (f32/f64/u8).  With ``check`` the device
+        status word is read back (one small synchronising copy) and turned
+        into the reference's exception types."""
+        torch = _torch()
+        f1 = _to_device_frames(frames1, self.device)
+        f2 = _to_device_frames(frames2, self.device)
+        if f1.dim() == 2:
+            f1 = f1.unsqueeze(0)
+            f2 = f2.unsqueeze(0)
+        if tuple(f1.shape) != (self.B, self.H, self.W) or tuple(f2.shape) != tuple(f1.shape):
+            raise ValueError(
+                f"frame batch {tuple(f1.shape)} / {tuple(f2.shape)} does not match the engine "
+                f"({self.B}, {self.H}, {self.W})")
+        if f2.dtype != f1.dtype:
+            f2 = f2.to(f1.dtype)
+        if out is None:
+            out = torch.empty((self.B, self.H, self.W, 2), dtype=torch.float64,
+                              device=self.device)
+        rc = _lib.lib().dis_flow_batch(
+            f1.data_ptr(), f2.data_ptr(), _dtype_code(f1), self.B, self.H, self.W,
+            ctypes.byref(self.cparams), out.data_ptr(), self.workspace.data_ptr(),
+            self.workspace_bytes, _lib.stream_handle(stream))
+        _lib.check(rc)
+        if check:
+            self.check_status(stream)
+        return out
+
+    def check_status(self, stream=None) -> None:
+        status = ctypes.c_uint32(0)
+        L = _lib.lib()
+        _lib.check(L.dis_read_status(self.workspace.data_ptr(), ctypes.byref(status),
+                                     _lib.stream_handle(stream)))
+        _lib.check(L.dis_status_to_error(status.value))
+
+    # -- host-buffer path (the e2e boundary) ---------------------------------
+    def run_host(self, frames1: np.ndarray, frames2: np.ndarray, out: np.ndarray | None = None,
+                 stream=None) -> np.ndarray:
+        """dis_flow_batch_host: host frames in, host flow out (copies
+        included).  Pinned host buffers (torch ``pin_memory``) are fastest."""
+        torch = _torch()
+        a = np.ascontiguousarray(frames1)
+        b = np.ascontiguousarray(frames2)
+        if a.dtype not in (np.float32, np.float64, np.uint8):
+            a = a.astype(np.float64)
+            b = b.astype(np.float64)
+        b = b.astype(a.dtype, copy=False)
+        code = {np.dtype(np.float32): 0, np.dtype(np.float64): 1, np.dtype(np.uint8): 2}[a.dtype]
+        L = _lib.lib()
+        n = L.dis_host_workspace_bytes(self.B, self.H, self.W, code, ctypes.byref(self.cparams))
+        if self._host_ws is None or self._host_ws.numel() < n:
+            self._host_ws = torch.empty(int(n), dtype=torch.uint8, device=self.device)
+        if out is None:
+            out = np.empty((self.B, self.H, self.W, 2), dtype=np.float64)
+        rc = L.dis_flow_batch_host(a.ctypes.data, b.ctypes.data, code, self.B, self.H, self.W,
+                                   ctypes.byref(self.cparams), out.ctypes.data,
+                                   self._host_ws.data_ptr(), int(n),
+                                   _lib.stream_handle(stream))
+        _lib.check(rc)
+        return out
+
+
+_ENGINES: dict = {}
+
+
+def _engine(B, H, W, params):
+    key = (B, H, W, params)
+    eng = _ENGINES.get(key)
+    if eng is None:
+        if len(_ENGINES) > 8:
+            _ENGINES.clear()
+        eng = FlowEngine(B, H, W, params)
+        _ENGINES[key] = eng
+    return eng
+
+
+def _check_frame(a):
+    """as_image's shape checks (core.py:65-72); finiteness is checked on the
+    device (status word)."""
+    shape = tuple(a.shape)
+    if len(shape) != 2 or shape[0] < 1 or shape[1] < 1:
+        raise ValueError(f"image must be 2D and non-empty, got shape {shape}")
+
+
+def dis_flow_batch(frames1, frames2, params: DisParams | None = None):
+    """Flow for a batch of independent pairs: frames (B, H, W) -> (B, H, W, 2)
+    float64 CUDA tensor.  Pair i equals ``dis_flow(frames1[i], frames2[i])``
+    bit for bit."""
+    _require_cuda()
+    params = params if params is not None else DisParams.preset(2)
+    s1 = tuple(frames1.shape)
+    s2 = tuple(frames2.shape)
+    if len(s1) != 3:
+        raise ValueError(f"frame batch must be (B, H, W), got {s1}")
+    if s1 != s2:
+        raise ValueError(f"frame dimensions differ: {s1[:0:-1]} vs {s2[:0:-1]}")
+    eng = _engine(s1[0], s1[1], s1[2], params)
+    return eng.run(frames1, frames2)
+
+
+def dis_flow(frame1, frame2, params: DisParams | None = None, threads: int = 1):
+    """Dense optical flow from ``frame1`` to ``frame2`` (pipeline.py:150-163):
+    an (H, W, 2) float64 field at the input resolution, numpy in -> numpy out,
+    torch in -> torch (CUDA) out.  ``threads`` is accepted for signature
+    compatibility (the reference's numba thread count)."""
+    torch = _require_cuda()
+    params = params if params is not None else DisParams.preset(2)
+    _check_frame(frame1)
+    _check_frame(frame2)
+    if tuple(frame1.shape) != tuple(frame2.shape):
+        raise ValueError(
+            f"frame dimensions differ: {tuple(frame1.shape)[::-1]} vs "
+            f"{tuple(frame2.shape)[::-1]}")
+    if params.coarsest_scale < 0:
+        raise ParameterError("coarsest_scale must be >= 0")
+    h, w = frame1.shape
+    eng = _engine(1, int(h), int(w), params)
+    out = eng.run(frame1, frame2)[0]
+    if isinstance(frame1, torch.Tensor):
+        return out
+    return out.cpu().numpy()

@@ -1,0 +1,240 @@
+"""CUDA path vs the oracle / reference goldens — bit-exact (float64 in the
+reference's operation order; the tolerance for every comparison here is
+zero: np.array_equal).  All calls go through the C ABI (libdis_b200.so)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from paper_1603_03590_b200.params import DisParams, VarParams
+from tests.conftest import golden
+from tools import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA GPU")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def st(torch):
+    from paper_1603_03590_b200 import stages
+
+    return stages
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def test_pyramid_bit_exact(torch, st):
+    g = golden("pyramid.npz")
+    levels = st.build_pyramid(g["img"][None], 4, finest=0)
+    for s, lv in enumerate(levels):
+        assert np.array_equal(_np(lv["img"])[0], g[f"L{s}_img"]), s
+        assert np.array_equal(_np(lv["gx"])[0], g[f"L{s}_gx"]), s
+        assert np.array_equal(_np(lv["gy"])[0], g[f"L{s}_gy"]), s
+        assert np.array_equal(_np(lv["dd"])[0], g[f"L{s}_dd"]), s
+
+
+def test_pyramid_level1_from_frames_and_f64_u8_inputs(torch, st, orc):
+    rng = np.random.default_rng(5)
+    for dt in (np.float32, np.float64, np.uint8):
+        img = (rng.uniform(0, 255, size=(2, 67, 95))).astype(dt)
+        lv = st.build_pyramid(img, 3, finest=1)
+        for b in range(2):
+            ref = orc.build_pyramid(img[b].astype(np.float64), 3)
+            for s in range(1, 4):
+                assert np.array_equal(_np(lv[s]["img"])[b], ref[s][0])
+                assert np.array_equal(_np(lv[s]["gx"])[b], ref[s][1])
+                assert np.array_equal(_np(lv[s]["gy"])[b], ref[s][2])
+
+
+def test_box_mean_order(torch, st):
+    g = golden("pyramid.npz")
+    big = np.random.default_rng(1000).uniform(0, 255, size=(200, 400))
+    lv = st.build_pyramid(big[None], 1, finest=2)
+    assert np.array_equal(_np(lv[1]["img"])[0], g["box_out"])
+
+
+def test_nonfinite_input_raises(torch, st):
+    img = np.zeros((1, 16, 16), dtype=np.float32)
+    img[0, 3, 4] = np.nan
+    with pytest.raises(ValueError):
+        st.build_pyramid(img, 1)
+
+
+def test_upsample_bit_exact(torch, st):
+    g = golden("samplers.npz")
+    f = torch.tensor(g["flow"], device="cuda")
+    u, v = f[..., 0][None].contiguous(), f[..., 1][None].contiguous()
+    for key, (hn, wn) in (("up_27x35", (27, 35)), ("up_26x34", (26, 34))):
+        ou, ov = st.upsample_flow(u, v, wn, hn)
+        assert np.array_equal(np.stack([_np(ou)[0], _np(ov)[0]], -1), g[key])
+
+
+def test_grid_axis_matches_reference(torch, st):
+    g = golden("samplers.npz")
+    off = 0
+    for dim, ps, ov, cnt in zip(g["grid_dims"], g["grid_ps"], g["grid_ov"], g["grid_counts"]):
+        o = st.grid_axis(int(dim), int(ps), float(ov))
+        assert np.array_equal(o, g["grid_origins"][off:off + cnt])
+        off += cnt
+
+
+@pytest.mark.parametrize("name,s,ps,ov,iters,norm", [
+    ("search_c1_like.npz", 1, 8, 0.5, 32, "l2"),
+    ("search_c2_like.npz", 0, 12, 0.75, 128, "l2"),
+    ("search_huber.npz", 0, 8, 0.3, 16, "huber"),
+    ("search_l1.npz", 0, 8, 0.3, 16, "l1"),
+])
+def test_patch_search_and_densify_bit_exact(torch, st, name, s, ps, ov, iters, norm):
+    g = golden(name)
+    params = DisParams(patch_size=ps, overlap=ov, iterations=iters, finest_scale=0,
+                       coarsest_scale=max(s, 1), residual_norm=norm, huber_b=1.0)
+    l1 = st.build_pyramid(g["in_f1"][None], s, finest=s)[s]
+    l2 = st.build_pyramid(g["in_f2"][None], s, finest=s)[s]
+    cu = cv = None
+    if "in_coarse" in g.files:
+        c = torch.tensor(g["in_coarse"], device="cuda")
+        cu, cv = c[..., 0][None].contiguous(), c[..., 1][None].contiguous()
+    r = st.patch_search(l1, l2["img"], params, cu, cv)
+    assert np.array_equal(r["x_origins"], g["x_origins"])
+    assert np.array_equal(r["y_origins"], g["y_origins"])
+    init = np.stack([_np(r["init_u"])[0], _np(r["init_v"])[0]], -1)
+    assert np.array_equal(init, g["init"])
+    assert np.array_equal(_np(r["valid"])[0].astype(bool), g["valid"])
+    disp = np.stack([_np(r["u"])[0], _np(r["v"])[0]], -1)
+    assert np.array_equal(disp, g["disp"])
+    assert np.array_equal(_np(r["off"])[0], g["off"])
+    assert np.array_equal(_np(r["mar"])[0], g["mar"])
+    fu, fv = st.densify(l1["img"], l2["img"], params, r["u"], r["v"], r["off"])
+    assert np.array_equal(np.stack([_np(fu)[0], _np(fv)[0]], -1), g["dense"])
+
+
+def test_refine_bit_exact(torch, st):
+    g = golden("refine.npz")
+    l1 = st.build_pyramid(g["f1"][None], 0)[0]
+    l2 = st.build_pyramid(g["f2"][None], 0)[0]
+    init = torch.tensor(g["init"], device="cuda")
+    u0, v0 = init[..., 0][None].contiguous(), init[..., 1][None].contiguous()
+    p = DisParams(variational=VarParams())
+    for key, outer in (("refined_s0", 1), ("refined_s2", 3), ("refined_fixed1", 1)):
+        u, v = st.refine(u0, v0, l1, l2, p, outer)
+        assert np.array_equal(np.stack([_np(u)[0], _np(v)[0]], -1), g[key]), key
+
+
+@pytest.mark.parametrize("sweeps", [1, 3, 8, 11])
+def test_refine_sweep_counts_vs_oracle(torch, st, orc, sweeps):
+    g = golden("refine.npz")
+    l1 = st.build_pyramid(g["f1"][None], 0)[0]
+    l2 = st.build_pyramid(g["f2"][None], 0)[0]
+    init = torch.tensor(g["init"], device="cuda")
+    u0, v0 = init[..., 0][None].contiguous(), init[..., 1][None].contiguous()
+    vp = VarParams(inner_sor_iters=sweeps)
+    u, v = st.refine(u0, v0, l1, l2, DisParams(variational=vp), 2)
+    lv1 = orc.build_pyramid(g["f1"], 0)[0]
+    lv2 = orc.build_pyramid(g["f2"], 0)[0]
+    want = orc.refine(g["init"], lv1, lv2, vp, 2)
+    assert np.array_equal(np.stack([_np(u)[0], _np(v)[0]], -1), want)
+
+
+def _params_from(g):
+    outer = int(g["outer"])
+    return DisParams(
+        patch_size=int(g["patch_size"]), overlap=float(g["overlap"]),
+        iterations=int(g["iterations"]), finest_scale=int(g["finest"]),
+        coarsest_scale=int(g["coarsest"]),
+        variational=VarParams(outer_iters_fixed=None if outer < 0 else outer))
+
+
+@pytest.mark.parametrize("case", ["c0", "c0_default_outer", "c1", "c2", "c3", "c4"])
+def test_end_to_end_small_goldens(torch, case):
+    from paper_1603_03590_b200 import dis_flow
+
+    g = golden(f"e2e_{case}.npz")
+    flow = dis_flow(g["f1"], g["f2"], _params_from(g))
+    assert flow.dtype == np.float64
+    assert np.array_equal(flow, g["flow"])
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("cfg_name", ["c0", "c1", "c2", "c3"])
+def test_full_size_configs_match_reference_hashes(torch, cfg_name):
+    """BASELINE configs at full size: the CUDA flow's sha256 equals the sha256
+    of the reference's own output on the same pair (tests/golden)."""
+    from paper_1603_03590_b200 import dis_flow_batch
+
+    g = golden("full_hashes.npz")
+    rows = [i for i, c in enumerate(g["cfg"]) if str(c) == cfg_name]
+    cfg = synth.CONFIGS[cfg_name]
+    first = min(int(g["pair"][i]) for i in rows)
+    count = max(int(g["pair"][i]) for i in rows) - first + 1
+    f1, f2 = synth.make_batch(cfg, seed=0, count=count, first=first)
+    flow = dis_flow_batch(f1, f2, synth.dis_params(cfg)).cpu().numpy()
+    for i in rows:
+        k = int(g["pair"][i]) - first
+        assert _sha(flow[k]) == str(g["flow_sha"][i]), (cfg_name, k)
+
+
+@pytest.mark.parametrize("cfg_name,count", [("c1", 6), ("c2", 2), ("c3", 2)])
+def test_batched_full_size_vs_oracle(torch, orc, cfg_name, count):
+    """Several pairs in one batch (pair i uses seed i) against the oracle,
+    bit-exact; checks batching does not couple pairs."""
+    from paper_1603_03590_b200 import dis_flow_batch
+
+    cfg = synth.CONFIGS[cfg_name]
+    f1, f2 = synth.make_batch(cfg, seed=3, count=count)
+    params = synth.dis_params(cfg)
+    flow = dis_flow_batch(f1, f2, params).cpu().numpy()
+    want = orc.dis_flow_batch_f32(f1, f2, params)
+    for k in range(count):
+        assert np.array_equal(flow[k], want[k]), (cfg_name, k)
+
+
+def test_determinism_repeat_runs(torch):
+    from paper_1603_03590_b200 import dis_flow_batch
+
+    cfg = synth.CONFIGS["c1"]
+    f1, f2 = synth.make_batch(cfg, seed=9, count=3, h=218, w=512)
+    params = synth.dis_params(cfg, coarsest=4)
+    a = dis_flow_batch(f1, f2, params).cpu().numpy()
+    b = dis_flow_batch(f1, f2, params).cpu().numpy()
+    assert np.array_equal(a, b)
+
+
+def test_host_buffer_path_matches_device_path(torch):
+    from paper_1603_03590_b200 import FlowEngine
+
+    cfg = synth.CONFIGS["c0"]
+    f1, f2 = synth.make_batch(cfg, seed=4, count=2)
+    eng = FlowEngine(2, cfg.height, cfg.width, synth.dis_params(cfg))
+    dev = eng.run(torch.from_numpy(f1).cuda(), torch.from_numpy(f2).cuda()).cpu().numpy()
+    host = eng.run_host(f1, f2)
+    assert np.array_equal(dev, host)
+
+
+def test_error_types(torch):
+    from paper_1603_03590_b200 import ParameterError, dis_flow
+
+    a = np.zeros((64, 64), dtype=np.float32)
+    with pytest.raises(ValueError):
+        dis_flow(a, np.zeros((64, 65), dtype=np.float32))
+    with pytest.raises(ParameterError):
+        dis_flow(a, a, DisParams(patch_size=1))
+    with pytest.raises(ValueError):  # coarsest level cannot hold the patch
+        dis_flow(a, a, DisParams(coarsest_scale=5, finest_scale=3))
+    bad = a.copy()
+    bad[3, 3] = np.inf
+    with pytest.raises(ValueError):
+        dis_flow(bad, a, DisParams(coarsest_scale=2, finest_scale=1))
