@@ -137,176 +137,237 @@ __global__ void __launch_bounds__(256) k_tensor_assemble(RefineArgs a, size_t Ls
 }
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kLookahead = 3;  // diagonals prefetched ahead of the wavefront
+
+enum RecField { F_U = 0, F_V, F_M00, F_M01, F_M11, F_R0, F_R1, F_WS };
 
 template <int S>
-__global__ void __launch_bounds__(576) k_sor(const double* __restrict__ rec, int B, int W,
+__host__ __device__ constexpr int ring_slots() {
+  // slots in use at step k: diagonals k - 2(S-1) .. k + 1, plus the ones in
+  // flight up to k + kLookahead
+  return kLookahead + 2 * S - 1;
+}
+
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// The wavefront SOR kernel (see the file header).  RING = true stages the
+// records of the live diagonals in a shared-memory ring filled by cp.async
+// kLookahead steps ahead (levels up to ~290 rows); RING = false reads them
+// from global memory (L1/L2).  All sweeps of a step are evaluated
+// branch-free (selects), so their independent dependency chains interleave.
+template <int S, bool RING>
+__global__ void __launch_bounds__(RING ? 320 : 576) k_sor(const double* __restrict__ rec, int B, int W,
                                              int H, size_t Ls, double omega,
                                              const double* du_in, const double* dv_in,
                                              double* du_out, double* dv_out,
                                              double* __restrict__ fu,
                                              double* __restrict__ fv, uint32_t* status) {
+  extern __shared__ double smem[];
+  constexpr int R = ring_slots<S>();
   const int b = blockIdx.x;
   const int y = threadIdx.x;
+  const int Hp = blockDim.x;
   const int lane = y & 31;
   const int warp = y >> 5;
-  const int nwarps = blockDim.x >> 5;
+  const int nwarps = Hp >> 5;
   const bool row_ok = y < H;
-  const double* __restrict__ Ru = rec + (size_t)(0 * B + b) * Ls;
-  const double* __restrict__ Rv = rec + (size_t)(1 * B + b) * Ls;
-  const double* __restrict__ Rm00 = rec + (size_t)(2 * B + b) * Ls;
-  const double* __restrict__ Rm01 = rec + (size_t)(3 * B + b) * Ls;
-  const double* __restrict__ Rm11 = rec + (size_t)(4 * B + b) * Ls;
-  const double* __restrict__ Rr0 = rec + (size_t)(5 * B + b) * Ls;
-  const double* __restrict__ Rr1 = rec + (size_t)(6 * B + b) * Ls;
-  const double* __restrict__ Rws = rec + (size_t)(7 * B + b) * Ls;
+  const int ymc = y > 0 ? y - 1 : 0;               // clamped up row
+  const int ypc = y < H - 1 ? y + 1 : H - 1;       // clamped down row
+  const int ndiag = W + H - 1;
+  double* ring = smem;
+  double* xch = smem + (RING ? (size_t)R * 8 * Hp : 0);  // [2][nwarps][2][S][2]
+  const double* __restrict__ base = rec + (size_t)b * Ls;
+  const size_t fstride = (size_t)B * Ls;  // distance between record fields
   const double* Dui = du_in ? du_in + (size_t)b * Ls : nullptr;  // may alias du_out
   const double* Dvi = dv_in ? dv_in + (size_t)b * Ls : nullptr;
   const double om1 = 1.0 - omega;
 
-  // [parity][warp][0 = lane 0 (top), 1 = lane 31 (bottom)][sweep][U, V, ws]
-  __shared__ double xch[2][18][2][S][3];
+  // record field f of pixel (j - yy, yy) on diagonal j (0 <= j < ndiag)
+  auto rv = [&](int f, int j, int yy) -> double {
+    if (RING) return ring[((size_t)(j % R) * 8 + f) * Hp + yy];
+    return __ldg(base + f * fstride + (size_t)j * H + yy);
+  };
+  auto issue = [&](int j) {
+    const int x = j - y;
+    if (row_ok && x >= 0 && x < W) {
+      const size_t g = (size_t)j * H + y;
+      double* dst = ring + (size_t)(j % R) * 8 * Hp + y;
+#pragma unroll
+      for (int f = 0; f < 8; ++f) cp_async8(dst + (size_t)f * Hp, base + f * fstride + g);
+    }
+  };
+
+  if (RING) {
+#pragma unroll
+    for (int j = 0; j < kLookahead; ++j) {
+      issue(j);
+      cp_async_commit();
+    }
+    cp_async_wait<kLookahead - 2>();
+    __syncthreads();
+  }
 
   double lU[S], lV[S], lW[S], ldu[S], ldv[S], pdu[S], pdv[S];
 #pragma unroll
-  for (int t = 0; t < S; ++t) {
-    lU[t] = lV[t] = lW[t] = ldu[t] = ldv[t] = pdu[t] = pdv[t] = 0.0;
-  }
+  for (int t = 0; t < S; ++t) lU[t] = lV[t] = lW[t] = ldu[t] = ldv[t] = pdu[t] = pdv[t] = 0.0;
   bool bad = false;
-  const int nsteps = W + H - 1 + 2 * (S - 1);
+  const int nsteps = ndiag + 2 * (S - 1);
   for (int k = 0; k < nsteps; ++k) {
+    if (RING) {
+      issue(k + kLookahead);
+      cp_async_commit();
+    }
     const int rd = (k & 1) ^ 1;
 #pragma unroll
     for (int t = S - 1; t >= 0; --t) {
-      const int x = k - y - 2 * t;
+      const int j = k - 2 * t;           // diagonal of this sweep's pixel
+      const int x = j - y;
+      const bool act = row_ok && x >= 0 && x < W;
+      const int jc = j < 0 ? 0 : (j > ndiag - 1 ? ndiag - 1 : j);
+      const int jm = jc > 0 ? jc - 1 : 0;
+      const int jp = jc < ndiag - 1 ? jc + 1 : ndiag - 1;
+      // previous-step values of the neighbours (warp-synchronous)
       double upU = __shfl_up_sync(kFull, lU[t], 1);
       double upV = __shfl_up_sync(kFull, lV[t], 1);
-      double upW = __shfl_up_sync(kFull, lW[t], 1);
-      double dnU = 0.0, dnV = 0.0, dnW = 0.0;
+      double dnU = 0.0, dnV = 0.0;
       if (t > 0) {
         dnU = __shfl_down_sync(kFull, lU[t - 1], 1);
         dnV = __shfl_down_sync(kFull, lV[t - 1], 1);
-        dnW = __shfl_down_sync(kFull, lW[t - 1], 1);
       }
-      if (!row_ok) continue;
-      if (x >= 0 && x < W) {
-        if (lane == 0 && warp > 0) {
-          upU = xch[rd][warp - 1][1][t][0];
-          upV = xch[rd][warp - 1][1][t][1];
-          upW = xch[rd][warp - 1][1][t][2];
+      if (lane == 0 && warp > 0) {
+        const double* xs = xch + ((((size_t)rd * nwarps + warp - 1) * 2 + 1) * S + t) * 2;
+        upU = xs[0];
+        upV = xs[1];
+      }
+      if (t > 0 && lane == 31 && warp < nwarps - 1) {
+        const double* xs = xch + ((((size_t)rd * nwarps + warp + 1) * 2 + 0) * S + t - 1) * 2;
+        dnU = xs[0];
+        dnV = xs[1];
+      }
+      const double uc = rv(F_U, jc, y), vc = rv(F_V, jc, y), wp = rv(F_WS, jc, y);
+      const double m00 = rv(F_M00, jc, y), m01 = rv(F_M01, jc, y), m11 = rv(F_M11, jc, y);
+      const double r0 = rv(F_R0, jc, y), r1 = rv(F_R1, jc, y);
+      const double upW = rv(F_WS, jm, ymc);
+      const double dnW = rv(F_WS, jp, ypc);
+      double rU, rV, rW;
+      if (t > 0) {
+        rU = lU[t - 1];
+        rV = lV[t - 1];
+        rW = lW[t - 1];
+      } else {
+        rU = rv(F_U, jp, y) + (Dui ? Dui[(size_t)jp * H + y] : 0.0);
+        rV = rv(F_V, jp, y) + (Dvi ? Dvi[(size_t)jp * H + y] : 0.0);
+        rW = rv(F_WS, jp, y);
+        dnU = rv(F_U, jp, ypc) + (Dui ? Dui[(size_t)jp * H + ypc] : 0.0);
+        dnV = rv(F_V, jp, ypc) + (Dvi ? Dvi[(size_t)jp * H + ypc] : 0.0);
+      }
+      const bool hasL = x > 0, hasR = x < W - 1, hasU = y > 0, hasD = y < H - 1;
+      double sw = 0.0, su = 0.0, sv = 0.0, wq;
+      wq = 0.5 * (wp + lW[t]);
+      sw = hasL ? sw + wq : sw;
+      su = hasL ? su + wq * (lU[t] - uc) : su;
+      sv = hasL ? sv + wq * (lV[t] - vc) : sv;
+      wq = 0.5 * (wp + rW);
+      sw = hasR ? sw + wq : sw;
+      su = hasR ? su + wq * (rU - uc) : su;
+      sv = hasR ? sv + wq * (rV - vc) : sv;
+      wq = 0.5 * (wp + upW);
+      sw = hasU ? sw + wq : sw;
+      su = hasU ? su + wq * (upU - uc) : su;
+      sv = hasU ? sv + wq * (upV - vc) : sv;
+      wq = 0.5 * (wp + dnW);
+      sw = hasD ? sw + wq : sw;
+      su = hasD ? su + wq * (dnU - uc) : su;
+      sv = hasD ? sv + wq * (dnV - vc) : sv;
+      double du, dv;
+      if (t > 0) {
+        du = pdu[t - 1];
+        dv = pdv[t - 1];
+      } else {
+        du = Dui ? Dui[(size_t)jc * H + y] : 0.0;
+        dv = Dvi ? Dvi[(size_t)jc * H + y] : 0.0;
+      }
+      const double den_u = m00 + sw;
+      const double nu = om1 * du + omega * ((r0 + su - m01 * dv) / den_u);
+      du = den_u > 1e-12 ? nu : du;
+      const double den_v = m11 + sw;
+      const double nv = om1 * dv + omega * ((r1 + sv - m01 * du) / den_v);
+      dv = den_v > 1e-12 ? nv : dv;
+      const double U = uc + du, V = vc + dv;
+      const bool shiftp = row_ok && x >= 0 && x <= W;
+      pdu[t] = shiftp ? ldu[t] : pdu[t];
+      pdv[t] = shiftp ? ldv[t] : pdv[t];
+      ldu[t] = act ? du : ldu[t];
+      ldv[t] = act ? dv : ldv[t];
+      lU[t] = act ? U : lU[t];
+      lV[t] = act ? V : lV[t];
+      lW[t] = act ? wp : lW[t];
+      if (t == S - 1 && act) {
+        if (du_out) {
+          du_out[(size_t)b * Ls + (size_t)j * H + y] = du;
+          dv_out[(size_t)b * Ls + (size_t)j * H + y] = dv;
         }
-        if (t > 0 && lane == 31 && warp < nwarps - 1) {
-          dnU = xch[rd][warp + 1][0][t - 1][0];
-          dnV = xch[rd][warp + 1][0][t - 1][1];
-          dnW = xch[rd][warp + 1][0][t - 1][2];
+        if (fu) {
+          const size_t o = (size_t)b * W * H + (size_t)y * W + x;
+          fu[o] = U;
+          fv[o] = V;
+          bad |= !(isfinite(U) && isfinite(V));
         }
-        const size_t idx = (size_t)(x + y) * H + y;
-        const double uc = Ru[idx], vc = Rv[idx], wp = Rws[idx];
-        double sw = 0.0, su = 0.0, sv = 0.0;
-        if (x > 0) {
-          const double wq = 0.5 * (wp + lW[t]);
-          sw += wq;
-          su += wq * (lU[t] - uc);
-          sv += wq * (lV[t] - vc);
-        }
-        if (x < W - 1) {
-          double rU, rV, rW;
-          if (t > 0) {
-            rU = lU[t - 1];
-            rV = lV[t - 1];
-            rW = lW[t - 1];
-          } else {
-            const size_t q = idx + H;
-            rU = Ru[q] + (Dui ? Dui[q] : 0.0);
-            rV = Rv[q] + (Dvi ? Dvi[q] : 0.0);
-            rW = Rws[q];
-          }
-          const double wq = 0.5 * (wp + rW);
-          sw += wq;
-          su += wq * (rU - uc);
-          sv += wq * (rV - vc);
-        }
-        if (y > 0) {
-          const double wq = 0.5 * (wp + upW);
-          sw += wq;
-          su += wq * (upU - uc);
-          sv += wq * (upV - vc);
-        }
-        if (y < H - 1) {
-          if (t == 0) {
-            const size_t q = idx + H + 1;
-            dnU = Ru[q] + (Dui ? Dui[q] : 0.0);
-            dnV = Rv[q] + (Dvi ? Dvi[q] : 0.0);
-            dnW = Rws[q];
-          }
-          const double wq = 0.5 * (wp + dnW);
-          sw += wq;
-          su += wq * (dnU - uc);
-          sv += wq * (dnV - vc);
-        }
-        double du, dv;
-        if (t > 0) {
-          du = pdu[t - 1];
-          dv = pdv[t - 1];
-        } else {
-          du = Dui ? Dui[idx] : 0.0;
-          dv = Dvi ? Dvi[idx] : 0.0;
-        }
-        const double den_u = Rm00[idx] + sw;
-        const double m01 = Rm01[idx];
-        if (den_u > 1e-12) {
-          const double val = (Rr0[idx] + su - m01 * dv) / den_u;
-          du = om1 * du + omega * val;
-        }
-        const double den_v = Rm11[idx] + sw;
-        if (den_v > 1e-12) {
-          const double val = (Rr1[idx] + sv - m01 * du) / den_v;
-          dv = om1 * dv + omega * val;
-        }
-        pdu[t] = ldu[t];
-        pdv[t] = ldv[t];
-        ldu[t] = du;
-        ldv[t] = dv;
-        lU[t] = uc + du;
-        lV[t] = vc + dv;
-        lW[t] = wp;
-        if (t == S - 1) {
-          if (du_out) {
-            du_out[(size_t)b * Ls + idx] = du;
-            dv_out[(size_t)b * Ls + idx] = dv;
-          }
-          if (fu) {
-            const size_t o = (size_t)b * W * H + (size_t)y * W + x;
-            fu[o] = lU[t];
-            fv[o] = lV[t];
-            bad |= !(isfinite(lU[t]) && isfinite(lV[t]));
-          }
-        }
-      } else if (x == W) {
-        pdu[t] = ldu[t];
-        pdv[t] = ldv[t];
       }
     }
     if (row_ok && (lane == 0 || lane == 31)) {
-      const int side = lane == 31 ? 1 : 0;
+      double* xs = xch + (((size_t)(k & 1) * nwarps + warp) * 2 + (lane == 31 ? 1 : 0)) * S * 2;
 #pragma unroll
       for (int t = 0; t < S; ++t) {
-        xch[k & 1][warp][side][t][0] = lU[t];
-        xch[k & 1][warp][side][t][1] = lV[t];
-        xch[k & 1][warp][side][t][2] = lW[t];
+        xs[2 * t] = lU[t];
+        xs[2 * t + 1] = lV[t];
       }
     }
+    if (RING) cp_async_wait<kLookahead - 2>();
     __syncthreads();
   }
   if (bad) set_status(status, DIS_STATUS_NONFINITE_FLOW);
 }
 
 template <int S>
+static size_t sor_smem_bytes(int threads, bool ring) {
+  const size_t xch = (size_t)2 * (threads / 32) * 2 * S * 2 * sizeof(double);
+  return xch + (ring ? (size_t)ring_slots<S>() * 8 * threads * sizeof(double) : 0);
+}
+
+constexpr size_t kMaxSmem = 227 * 1024;
+
+template <int S>
 static void launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const double* dvi,
                          double* duo, double* dvo, bool final_pass, cudaStream_t st) {
   const int threads = (a.H + 31) / 32 * 32;
-  k_sor<S><<<a.B, threads, 0, st>>>(a.rec, a.B, a.W, a.H, Ls, a.omega, dui, dvi, duo, dvo,
-                                     final_pass ? a.fu : nullptr, final_pass ? a.fv : nullptr,
-                                     a.status);
+  const bool ring = threads <= 320 && sor_smem_bytes<S>(threads, true) <= kMaxSmem;
+  const size_t smem = sor_smem_bytes<S>(threads, ring);
+  double* fu = final_pass ? a.fu : nullptr;
+  double* fv = final_pass ? a.fv : nullptr;
+  if (ring) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_sor<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kMaxSmem);
+      attr = true;
+    }
+    k_sor<S, true><<<a.B, threads, smem, st>>>(a.rec, a.B, a.W, a.H, Ls, a.omega, dui, dvi,
+                                               duo, dvo, fu, fv, a.status);
+  } else {
+    k_sor<S, false><<<a.B, threads, smem, st>>>(a.rec, a.B, a.W, a.H, Ls, a.omega, dui, dvi,
+                                                duo, dvo, fu, fv, a.status);
+  }
 }
 
 static void launch_sor(const RefineArgs& a, size_t Ls, int S, const double* dui,
