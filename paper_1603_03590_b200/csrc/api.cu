@@ -197,9 +197,9 @@ int check_dims(const dis_params_t* p, int B, int H, int W) {
     return fail(DIS_ERR_VALUE,
                 "coarsest level %dx%d cannot hold a %dpx patch; lower coarsest_scale", wc, hc,
                 p->patch_size);
-  if (p->variational && (H >> p->finest_scale) > 576)
+  if (p->variational && (H >> p->finest_scale) > 2048)
     return fail(DIS_ERR_VALUE,
-                "variational refinement of a level taller than 576 rows is not supported by "
+                "variational refinement of a level taller than 2048 rows is not supported by "
                 "this build (level %d is %d rows)",
                 p->finest_scale, H >> p->finest_scale);
   return DIS_OK;
@@ -621,8 +621,8 @@ int dis_refine(const double* ref_img, const double* ref_gx, const double* ref_gy
   if (dis_params_validate(p)) return DIS_ERR_PARAMETER;
   if (workspace_bytes < dis_refine_workspace_bytes(B, W, H))
     return fail(DIS_ERR_WORKSPACE, "refine workspace too small");
-  if (H > 576)
-    return fail(DIS_ERR_VALUE, "variational refinement of a level taller than 576 rows is not "
+  if (H > 2048)
+    return fail(DIS_ERR_VALUE, "variational refinement of a level taller than 2048 rows is not "
                                "supported by this build");
   RefineArgs r{};
   r.ref = ref_img;

@@ -138,19 +138,23 @@ __global__ void __launch_bounds__(256) k_tensor_assemble(RefineArgs a, size_t Ls
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kLookahead = 3;  // diagonals prefetched ahead of the wavefront
+constexpr int kPitch = 9;      // doubles per ring row: 8 fields + 1 pad (72 B, conflict-free LDS.64)
+constexpr int kMaxRowsPerCta = 256;
 
 enum RecField { F_U = 0, F_V, F_M00, F_M01, F_M11, F_R0, F_R1, F_WS };
 
 template <int S>
 __host__ __device__ constexpr int ring_slots() {
-  // slots in use at step k: diagonals k - 2(S-1) .. k + 1, plus the ones in
-  // flight up to k + kLookahead
-  return kLookahead + 2 * S - 1;
+  // live at step k: diagonals k - 2(S-1) - 1 (last sweep's up-neighbour) .. k + 1,
+  // plus the ones in flight up to k + kLookahead
+  return kLookahead + 2 * S;
 }
 
-__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
+__device__ __forceinline__ void cp_async8(unsigned smem_dst, const double* gsrc, unsigned src_bytes) {
+  // src_bytes = 0 zero-fills the 8 destination bytes
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_dst), "l"(gsrc),
+               "r"(src_bytes)
+               : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -159,84 +163,129 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// store a double into the shared memory of CTA `rank` of this cluster
+__device__ __forceinline__ void st_cluster(const double* local, unsigned rank, double v) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(local), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(ra), "d"(v) : "memory");
+}
 
-// The wavefront SOR kernel (see the file header).  RING = true stages the
-// records of the live diagonals in a shared-memory ring filled by cp.async
-// kLookahead steps ahead (levels up to ~290 rows); RING = false reads them
-// from global memory (L1/L2).  All sweeps of a step are evaluated
-// branch-free (selects), so their independent dependency chains interleave.
-template <int S, bool RING>
-__global__ void __launch_bounds__(RING ? 320 : 576) k_sor(const double* __restrict__ rec, int B, int W,
-                                             int H, size_t Ls, double omega,
-                                             const double* du_in, const double* dv_in,
-                                             double* du_out, double* dv_out,
-                                             double* __restrict__ fu,
-                                             double* __restrict__ fv, uint32_t* status) {
+// The wavefront SOR kernel (see the file header).
+//
+// A pair's rows are split over a cluster of C CTAs (C = gridDim-cluster size,
+// 1..8); CTA c owns rows [c*Hc, c*Hc + Hc), one thread per row.  The records
+// of the live diagonals sit in a shared-memory ring [slot][row][kPitch]
+// filled by cp.async kLookahead steps ahead, including one halo row above
+// and below the CTA's band; entries of pixels outside the level are
+// zero-filled, so a sweep that is not active on its row (before its start
+// or after its end) computes finite garbage that is never stored — the
+// per-sweep state then needs no selects.  Boundary rows of the band exchange
+// their U, V with the neighbouring CTAs through distributed shared memory;
+// one (cluster) barrier per step.
+template <int S>
+__global__ void __launch_bounds__(kMaxRowsPerCta, 1)
+    k_sor(const double* __restrict__ rec, int B, int W, int H, int Hc, size_t Ls, double omega,
+          const double* du_in, const double* dv_in, double* du_out, double* dv_out,
+          double* __restrict__ fu, double* __restrict__ fv, uint32_t* status) {
   extern __shared__ double smem[];
   constexpr int R = ring_slots<S>();
-  const int b = blockIdx.x;
-  const int y = threadIdx.x;
+  const int C = (int)(gridDim.x / (unsigned)B) > 0 ? (int)(gridDim.x / (unsigned)B) : 1;
+  const int c = C > 1 ? (int)cluster_rank() : 0;
+  const int b = blockIdx.x / C;
+  const int ty = threadIdx.x;
   const int Hp = blockDim.x;
-  const int lane = y & 31;
-  const int warp = y >> 5;
+  const int y0 = c * Hc;
+  const int y = y0 + ty;
+  const int nrows = min(Hc, H - y0);  // rows this CTA owns
+  const int lane = ty & 31;
+  const int warp = ty >> 5;
   const int nwarps = Hp >> 5;
-  const bool row_ok = y < H;
-  const int ymc = y > 0 ? y - 1 : 0;               // clamped up row
-  const int ypc = y < H - 1 ? y + 1 : H - 1;       // clamped down row
+  const bool row_ok = ty < nrows;
   const int ndiag = W + H - 1;
-  double* ring = smem;
-  double* xch = smem + (RING ? (size_t)R * 8 * Hp : 0);  // [2][nwarps][2][S][2]
+  const int slot_rows = Hp + 2;                 // + halo above and below
+  double* ring = smem;                          // [R][slot_rows][kPitch]
+  double* xch = ring + (size_t)R * slot_rows * kPitch;   // [2][nwarps][2][S][2]
+  double* cxin = xch + (size_t)2 * nwarps * 2 * S * 2;   // [2][2][S][2]: 0 from above, 1 from below
   const double* __restrict__ base = rec + (size_t)b * Ls;
-  const size_t fstride = (size_t)B * Ls;  // distance between record fields
+  const size_t fstride = (size_t)B * Ls;
   const double* Dui = du_in ? du_in + (size_t)b * Ls : nullptr;  // may alias du_out
   const double* Dvi = dv_in ? dv_in + (size_t)b * Ls : nullptr;
   const double om1 = 1.0 - omega;
+  const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
+  const unsigned slot_bytes = (unsigned)(slot_rows * kPitch * 8);
 
-  // record field f of pixel (j - yy, yy) on diagonal j (0 <= j < ndiag)
-  auto rv = [&](int f, int j, int yy) -> double {
-    if (RING) return ring[((size_t)(j % R) * 8 + f) * Hp + yy];
-    return __ldg(base + f * fstride + (size_t)j * H + yy);
+  // load ring row r (image row y0 - 1 + r) of diagonal j
+  auto load_row = [&](int j, int r) {
+    const int yy = y0 - 1 + r;
+    const int x = j - yy;
+    const bool ok = yy >= 0 && yy < H && x >= 0 && x < W;
+    const size_t g = ok ? (size_t)j * H + yy : 0;
+    const unsigned dst = ring_s + (unsigned)(j % R) * slot_bytes + (unsigned)(r * kPitch * 8);
+#pragma unroll
+    for (int f = 0; f < 8; ++f) cp_async8(dst + 8 * f, base + f * fstride + g, ok ? 8u : 0u);
   };
   auto issue = [&](int j) {
-    const int x = j - y;
-    if (row_ok && x >= 0 && x < W) {
-      const size_t g = (size_t)j * H + y;
-      double* dst = ring + (size_t)(j % R) * 8 * Hp + y;
-#pragma unroll
-      for (int f = 0; f < 8; ++f) cp_async8(dst + (size_t)f * Hp, base + f * fstride + g);
-    }
+    if (j >= ndiag) return;
+    load_row(j, ty + 1);
+    if (ty == 0) load_row(j, 0);
+    if (ty == Hp - 1) load_row(j, Hp + 1);
   };
 
-  if (RING) {
+  {  // exchange buffers start finite (they feed inactive sweeps at step 0)
+    const int nx = 2 * nwarps * 2 * S * 2 + 2 * 2 * S * 2;
+    for (int i = ty; i < nx; i += Hp) xch[i] = 0.0;
+  }
 #pragma unroll
-    for (int j = 0; j < kLookahead; ++j) {
-      issue(j);
-      cp_async_commit();
-    }
-    cp_async_wait<kLookahead - 2>();
+  for (int j = 0; j < kLookahead; ++j) {
+    issue(j);
+    cp_async_commit();
+  }
+  cp_async_wait<kLookahead - 2>();
+  if (C > 1) {
+    cluster_arrive();
+    cluster_wait();
+  } else {
     __syncthreads();
   }
 
   double lU[S], lV[S], lW[S], ldu[S], ldv[S], pdu[S], pdv[S];
 #pragma unroll
   for (int t = 0; t < S; ++t) lU[t] = lV[t] = lW[t] = ldu[t] = ldv[t] = pdu[t] = pdv[t] = 0.0;
+  const bool hasU = y > 0, hasD = y < H - 1;
+  const bool top_row = ty == 0 && c > 0;                   // gets "up" from CTA c-1
+  const bool bot_row = ty == nrows - 1 && c < C - 1;       // gets "down" from CTA c+1
   bool bad = false;
   const int nsteps = ndiag + 2 * (S - 1);
+  int slot0 = 0;  // (k) mod R
   for (int k = 0; k < nsteps; ++k) {
-    if (RING) {
-      issue(k + kLookahead);
-      cp_async_commit();
-    }
+    issue(k + kLookahead);
+    cp_async_commit();
     const int rd = (k & 1) ^ 1;
 #pragma unroll
     for (int t = S - 1; t >= 0; --t) {
-      const int j = k - 2 * t;           // diagonal of this sweep's pixel
+      const int j = k - 2 * t;
       const int x = j - y;
-      const bool act = row_ok && x >= 0 && x < W;
-      const int jc = j < 0 ? 0 : (j > ndiag - 1 ? ndiag - 1 : j);
-      const int jm = jc > 0 ? jc - 1 : 0;
-      const int jp = jc < ndiag - 1 ? jc + 1 : ndiag - 1;
-      // previous-step values of the neighbours (warp-synchronous)
+      // ring addresses of this sweep's pixel row (slot of diagonal j) and of
+      // the neighbouring diagonals j-1 / j+1
+      int sj = slot0 - 2 * t;
+      sj += sj < 0 ? R : 0;
+      sj += sj < 0 ? R : 0;
+      const int sm = sj == 0 ? R - 1 : sj - 1;
+      const int sp = sj == R - 1 ? 0 : sj + 1;
+      const double* rp = ring + (size_t)sj * slot_rows * kPitch + (size_t)(ty + 1) * kPitch;
+      const double* rm = ring + (size_t)sm * slot_rows * kPitch + (size_t)(ty + 1) * kPitch;
+      const double* rn = ring + (size_t)sp * slot_rows * kPitch + (size_t)(ty + 1) * kPitch;
       double upU = __shfl_up_sync(kFull, lU[t], 1);
       double upV = __shfl_up_sync(kFull, lV[t], 1);
       double dnU = 0.0, dnV = 0.0;
@@ -254,48 +303,56 @@ __global__ void __launch_bounds__(RING ? 320 : 576) k_sor(const double* __restri
         dnU = xs[0];
         dnV = xs[1];
       }
-      const double uc = rv(F_U, jc, y), vc = rv(F_V, jc, y), wp = rv(F_WS, jc, y);
-      const double m00 = rv(F_M00, jc, y), m01 = rv(F_M01, jc, y), m11 = rv(F_M11, jc, y);
-      const double r0 = rv(F_R0, jc, y), r1 = rv(F_R1, jc, y);
-      const double upW = rv(F_WS, jm, ymc);
-      const double dnW = rv(F_WS, jp, ypc);
+      if (top_row) {
+        const double* xs = cxin + (((size_t)rd * 2 + 0) * S + t) * 2;
+        upU = xs[0];
+        upV = xs[1];
+      }
+      if (t > 0 && bot_row) {
+        const double* xs = cxin + (((size_t)rd * 2 + 1) * S + t - 1) * 2;
+        dnU = xs[0];
+        dnV = xs[1];
+      }
+      const double uc = rp[F_U], vc = rp[F_V], wp = rp[F_WS];
+      const double m00 = rp[F_M00], m01 = rp[F_M01], m11 = rp[F_M11];
+      const double r0 = rp[F_R0], r1 = rp[F_R1];
+      const double upW = rm[F_WS - kPitch];   // (x, y-1): diagonal j-1, row above
+      const double dnW = rn[F_WS + kPitch];   // (x, y+1): diagonal j+1, row below
       double rU, rV, rW;
       if (t > 0) {
         rU = lU[t - 1];
         rV = lV[t - 1];
         rW = lW[t - 1];
       } else {
-        rU = rv(F_U, jp, y) + (Dui ? Dui[(size_t)jp * H + y] : 0.0);
-        rV = rv(F_V, jp, y) + (Dvi ? Dvi[(size_t)jp * H + y] : 0.0);
-        rW = rv(F_WS, jp, y);
-        dnU = rv(F_U, jp, ypc) + (Dui ? Dui[(size_t)jp * H + ypc] : 0.0);
-        dnV = rv(F_V, jp, ypc) + (Dvi ? Dvi[(size_t)jp * H + ypc] : 0.0);
+        const int jp = j + 1;
+        const bool okp = jp >= 0 && jp < ndiag;
+        const size_t gq = okp ? (size_t)jp * H + y : 0;
+        const size_t gd = okp && hasD ? (size_t)jp * H + y + 1 : 0;
+        rU = rn[F_U] + (Dui ? Dui[gq] : 0.0);
+        rV = rn[F_V] + (Dvi ? Dvi[gq] : 0.0);
+        rW = rn[F_WS];
+        dnU = rn[F_U + kPitch] + (Dui ? Dui[gd] : 0.0);
+        dnV = rn[F_V + kPitch] + (Dvi ? Dvi[gd] : 0.0);
       }
-      const bool hasL = x > 0, hasR = x < W - 1, hasU = y > 0, hasD = y < H - 1;
-      double sw = 0.0, su = 0.0, sv = 0.0, wq;
-      wq = 0.5 * (wp + lW[t]);
-      sw = hasL ? sw + wq : sw;
-      su = hasL ? su + wq * (lU[t] - uc) : su;
-      sv = hasL ? sv + wq * (lV[t] - vc) : sv;
-      wq = 0.5 * (wp + rW);
-      sw = hasR ? sw + wq : sw;
-      su = hasR ? su + wq * (rU - uc) : su;
-      sv = hasR ? sv + wq * (rV - vc) : sv;
-      wq = 0.5 * (wp + upW);
-      sw = hasU ? sw + wq : sw;
-      su = hasU ? su + wq * (upU - uc) : su;
-      sv = hasU ? sv + wq * (upV - vc) : sv;
-      wq = 0.5 * (wp + dnW);
-      sw = hasD ? sw + wq : sw;
-      su = hasD ? su + wq * (dnU - uc) : su;
-      sv = hasD ? sv + wq * (dnV - vc) : sv;
+      // absent neighbours (borders) contribute wq = +0 times a finite value:
+      // adding an exact zero leaves the reference's partial sums unchanged
+      const double wqL = x > 0 ? 0.5 * (wp + lW[t]) : 0.0;
+      const double wqR = x < W - 1 ? 0.5 * (wp + rW) : 0.0;
+      const double wqU = hasU ? 0.5 * (wp + upW) : 0.0;
+      const double wqD = hasD ? 0.5 * (wp + dnW) : 0.0;
+      const double sw = (((0.0 + wqL) + wqR) + wqU) + wqD;
+      const double su = (((0.0 + wqL * (lU[t] - uc)) + wqR * (rU - uc)) + wqU * (upU - uc)) +
+                        wqD * (dnU - uc);
+      const double sv = (((0.0 + wqL * (lV[t] - vc)) + wqR * (rV - vc)) + wqU * (upV - vc)) +
+                        wqD * (dnV - vc);
       double du, dv;
       if (t > 0) {
         du = pdu[t - 1];
         dv = pdv[t - 1];
       } else {
-        du = Dui ? Dui[(size_t)jc * H + y] : 0.0;
-        dv = Dvi ? Dvi[(size_t)jc * H + y] : 0.0;
+        const bool ok = j >= 0 && j < ndiag;
+        du = Dui ? Dui[ok ? (size_t)j * H + y : 0] : 0.0;
+        dv = Dvi ? Dvi[ok ? (size_t)j * H + y : 0] : 0.0;
       }
       const double den_u = m00 + sw;
       const double nu = om1 * du + omega * ((r0 + su - m01 * dv) / den_u);
@@ -304,15 +361,14 @@ __global__ void __launch_bounds__(RING ? 320 : 576) k_sor(const double* __restri
       const double nv = om1 * dv + omega * ((r1 + sv - m01 * du) / den_v);
       dv = den_v > 1e-12 ? nv : dv;
       const double U = uc + du, V = vc + dv;
-      const bool shiftp = row_ok && x >= 0 && x <= W;
-      pdu[t] = shiftp ? ldu[t] : pdu[t];
-      pdv[t] = shiftp ? ldv[t] : pdv[t];
-      ldu[t] = act ? du : ldu[t];
-      ldv[t] = act ? dv : ldv[t];
-      lU[t] = act ? U : lU[t];
-      lV[t] = act ? V : lV[t];
-      lW[t] = act ? wp : lW[t];
-      if (t == S - 1 && act) {
+      pdu[t] = ldu[t];
+      pdv[t] = ldv[t];
+      ldu[t] = du;
+      ldv[t] = dv;
+      lU[t] = U;
+      lV[t] = V;
+      lW[t] = wp;
+      if (t == S - 1 && row_ok && x >= 0 && x < W) {
         if (du_out) {
           du_out[(size_t)b * Ls + (size_t)j * H + y] = du;
           dv_out[(size_t)b * Ls + (size_t)j * H + y] = dv;
@@ -325,7 +381,8 @@ __global__ void __launch_bounds__(RING ? 320 : 576) k_sor(const double* __restri
         }
       }
     }
-    if (row_ok && (lane == 0 || lane == 31)) {
+    // publish boundary rows for the next step
+    if (lane == 0 || lane == 31) {
       double* xs = xch + (((size_t)(k & 1) * nwarps + warp) * 2 + (lane == 31 ? 1 : 0)) * S * 2;
 #pragma unroll
       for (int t = 0; t < S; ++t) {
@@ -333,51 +390,99 @@ __global__ void __launch_bounds__(RING ? 320 : 576) k_sor(const double* __restri
         xs[2 * t + 1] = lV[t];
       }
     }
-    if (RING) cp_async_wait<kLookahead - 2>();
-    __syncthreads();
+    if (C > 1) {
+      if (ty == 0 && c > 0) {  // my first row -> CTA c-1's "from below"
+        double* xs = cxin + (((size_t)(k & 1) * 2 + 1) * S) * 2;
+#pragma unroll
+        for (int t = 0; t < S; ++t) {
+          st_cluster(xs + 2 * t, c - 1, lU[t]);
+          st_cluster(xs + 2 * t + 1, c - 1, lV[t]);
+        }
+      }
+      if (ty == nrows - 1 && c < C - 1) {  // my last row -> CTA c+1's "from above"
+        double* xs = cxin + (((size_t)(k & 1) * 2 + 0) * S) * 2;
+#pragma unroll
+        for (int t = 0; t < S; ++t) {
+          st_cluster(xs + 2 * t, c + 1, lU[t]);
+          st_cluster(xs + 2 * t + 1, c + 1, lV[t]);
+        }
+      }
+    }
+    cp_async_wait<kLookahead - 2>();
+    if (C > 1) {
+      cluster_arrive();
+      cluster_wait();
+    } else {
+      __syncthreads();
+    }
+    slot0 = slot0 == R - 1 ? 0 : slot0 + 1;
   }
   if (bad) set_status(status, DIS_STATUS_NONFINITE_FLOW);
 }
 
 template <int S>
-static size_t sor_smem_bytes(int threads, bool ring) {
+static size_t sor_smem_bytes(int threads) {
+  const size_t ring = (size_t)ring_slots<S>() * (threads + 2) * kPitch * sizeof(double);
   const size_t xch = (size_t)2 * (threads / 32) * 2 * S * 2 * sizeof(double);
-  return xch + (ring ? (size_t)ring_slots<S>() * 8 * threads * sizeof(double) : 0);
+  const size_t cx = (size_t)2 * 2 * S * 2 * sizeof(double);
+  return ring + xch + cx;
 }
 
 constexpr size_t kMaxSmem = 227 * 1024;
 
+// rows-per-CTA split: enough CTAs per pair to keep every band <= 256 rows and
+// its ring in shared memory, and, for small batches, to spread a pair over
+// several SMs (the step rate of one band is bound by its SM's FP64 pipe).
 template <int S>
-static void launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const double* dvi,
-                         double* duo, double* dvo, bool final_pass, cudaStream_t st) {
-  const int threads = (a.H + 31) / 32 * 32;
-  const bool ring = threads <= 320 && sor_smem_bytes<S>(threads, true) <= kMaxSmem;
-  const size_t smem = sor_smem_bytes<S>(threads, ring);
-  double* fu = final_pass ? a.fu : nullptr;
-  double* fv = final_pass ? a.fv : nullptr;
-  if (ring) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_sor<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)kMaxSmem);
-      attr = true;
-    }
-    k_sor<S, true><<<a.B, threads, smem, st>>>(a.rec, a.B, a.W, a.H, Ls, a.omega, dui, dvi,
-                                               duo, dvo, fu, fv, a.status);
-  } else {
-    k_sor<S, false><<<a.B, threads, smem, st>>>(a.rec, a.B, a.W, a.H, Ls, a.omega, dui, dvi,
-                                                duo, dvo, fu, fv, a.status);
-  }
+static int choose_cluster(int B, int H) {
+  int C = 1;
+  while (C < 8 && ((H + C - 1) / C > kMaxRowsPerCta ||
+                   sor_smem_bytes<S>(((H + C - 1) / C + 31) / 32 * 32) > kMaxSmem))
+    ++C;
+  while (C < 8 && B * (C + 1) <= 148 && (H + C) / (C + 1) >= 64) ++C;
+  return C;
 }
 
-static void launch_sor(const RefineArgs& a, size_t Ls, int S, const double* dui,
-                       const double* dvi, double* duo, double* dvo, bool final_pass,
-                       cudaStream_t st) {
+template <int S>
+static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const double* dvi,
+                        double* duo, double* dvo, bool final_pass, cudaStream_t st) {
+  const int C = choose_cluster<S>(a.B, a.H);
+  const int Hc = (a.H + C - 1) / C;
+  const int threads = (Hc + 31) / 32 * 32;
+  const size_t smem = sor_smem_bytes<S>(threads);
+  if (threads > kMaxRowsPerCta || smem > kMaxSmem) return DIS_ERR_VALUE;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sor<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
+    cudaFuncSetAttribute(k_sor<S>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(a.B * C));
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = (unsigned)C;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  double* fu = final_pass ? a.fu : nullptr;
+  double* fv = final_pass ? a.fv : nullptr;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_sor<S>, (const double*)a.rec, a.B, a.W, a.H, Hc,
+                                     Ls, a.omega, dui, dvi, duo, dvo, fu, fv, a.status);
+  return e == cudaSuccess ? DIS_OK : DIS_ERR_CUDA;
+}
+
+static int launch_sor(const RefineArgs& a, size_t Ls, int S, const double* dui,
+                      const double* dvi, double* duo, double* dvo, bool final_pass,
+                      cudaStream_t st) {
   switch (S) {
 #define DIS_SOR_CASE(n) \
   case n:               \
-    launch_sor_t<n>(a, Ls, dui, dvi, duo, dvo, final_pass, st); \
-    break;
+    return launch_sor_t<n>(a, Ls, dui, dvi, duo, dvo, final_pass, st);
     DIS_SOR_CASE(1)
     DIS_SOR_CASE(2)
     DIS_SOR_CASE(3)
@@ -388,12 +493,12 @@ static void launch_sor(const RefineArgs& a, size_t Ls, int S, const double* dui,
     DIS_SOR_CASE(8)
 #undef DIS_SOR_CASE
     default:
-      break;
+      return DIS_ERR_VALUE;
   }
 }
 
 int launch_refine(const RefineArgs& a, cudaStream_t st) {
-  if (a.H > 576) return DIS_ERR_VALUE;  // one CTA owns all rows of a level (see header)
+  if (a.H > 8 * kMaxRowsPerCta) return DIS_ERR_VALUE;  // at most 8 CTAs per pair
   const size_t Ls = (size_t)(a.W + a.H - 1) * a.H;
   double* carry_u = a.rec + (size_t)kRecords * a.B * Ls;
   double* carry_v = carry_u + (size_t)a.B * Ls;
@@ -414,9 +519,10 @@ int launch_refine(const RefineArgs& a, cudaStream_t st) {
       // may read and write the same buffer only at the same pixel, which it
       // reads (t = 0) before it writes (t = S - 1, two steps later or more)
       prof_begin(KC_SOR, st);
-      launch_sor(a, Ls, S, first ? nullptr : carry_u, first ? nullptr : carry_v,
-                 last ? nullptr : carry_u, last ? nullptr : carry_v, last, st);
+      int rc = launch_sor(a, Ls, S, first ? nullptr : carry_u, first ? nullptr : carry_v,
+                          last ? nullptr : carry_u, last ? nullptr : carry_v, last, st);
       prof_end(KC_SOR, st);
+      if (rc) return rc;
       note_launch();
       first = false;
     }
