@@ -82,8 +82,8 @@ __global__ void __launch_bounds__(256) k_densify(const double* __restrict__ ref_
       }
     }
     bad |= !(acc_w > 0.0);
-    fu[g] = acc_u / acc_w;
-    fv[g] = acc_v / acc_w;
+    fu[g] = exact_div_pos(acc_u, acc_w);  // acc_w > 0 (else flagged above)
+    fv[g] = exact_div_pos(acc_v, acc_w);
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) set_status(status, DIS_STATUS_COVERAGE);
 }

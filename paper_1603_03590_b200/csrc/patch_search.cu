@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(128) k_patch_search(SearchArgs a) {
     }
   }
   const double dn = (double)(ps * ps);
-  const double mean_t = tsum / dn;
+  const double mean_t = exact_div_pos(tsum, dn);
 
   // ---- _condition_hessians (inverse_search.py:255-276) ----
   const double tr = h00 + h11;
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(128) k_patch_search(SearchArgs a) {
     double wsum = 0.0;
     for (int oy = 0; oy < ps; ++oy)
       for (int ox = 0; ox < ps; ++ox) wsum += bilin_nb(qry, W, H, bx + ox, by + oy);
-    off = a.mean_norm ? wsum / dn - mean_t : 0.0;
+    off = a.mean_norm ? exact_div_pos(wsum, dn) - mean_t : 0.0;
     double ssd = 0.0, b0 = 0.0, b1 = 0.0;
     mar = 0.0;
     for (int oy = 0; oy < ps; ++oy) {
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(128) k_patch_search(SearchArgs a) {
         b1 += __ldg(rgy + row + ox) * et;
       }
     }
-    mar /= dn;
+    mar = exact_div_pos(mar, dn);
     if (evals == 0) {
       off0 = off;
       mar0 = mar;

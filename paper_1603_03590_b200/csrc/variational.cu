@@ -31,6 +31,8 @@
 //
 // Neighbour terms use U_q = fl(u_q + du_q) exactly as the reference's
 // `u[y, x-1] + du[y, x-1]`; the last sweep's U is the updated flow.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -136,10 +138,9 @@ __global__ void __launch_bounds__(256) k_tensor_assemble(RefineArgs a, size_t Ls
   rec[(7 * B + b) * Ls + s] = ws;
 }
 
-constexpr unsigned kFull = 0xffffffffu;
-constexpr int kLookahead = 3;  // diagonals prefetched ahead of the wavefront
+constexpr int kLookahead = 8;  // diagonals prefetched ahead of the wavefront (covers HBM latency)
 constexpr int kPitch = 9;      // doubles per ring row: 8 fields + 1 pad (72 B, conflict-free LDS.64)
-constexpr int kMaxRowsPerCta = 256;
+constexpr int kMaxBandRows = 128;  // rows (threads per sweep) of one CTA's band
 
 enum RecField { F_U = 0, F_V, F_M00, F_M01, F_M11, F_R0, F_R1, F_WS };
 
@@ -183,74 +184,94 @@ __device__ __forceinline__ void st_cluster(const double* local, unsigned rank, d
 
 // The wavefront SOR kernel (see the file header).
 //
-// A pair's rows are split over a cluster of C CTAs (C = gridDim-cluster size,
-// 1..8); CTA c owns rows [c*Hc, c*Hc + Hc), one thread per row.  The records
-// of the live diagonals sit in a shared-memory ring [slot][row][kPitch]
-// filled by cp.async kLookahead steps ahead, including one halo row above
-// and below the CTA's band; entries of pixels outside the level are
-// zero-filled, so a sweep that is not active on its row (before its start
-// or after its end) computes finite garbage that is never stored — the
-// per-sweep state then needs no selects.  Boundary rows of the band exchange
-// their U, V with the neighbouring CTAs through distributed shared memory;
-// one (cluster) barrier per step.
+// Thread (row y, sweep t) computes pixel x = k - y - 2t at step k.  A pair's
+// rows are split over a cluster of C CTAs (1..8); CTA c owns the band of rows
+// [c*Hc, c*Hc + Hc) and runs S x Hp threads (Hp = band rows rounded up to
+// 32).  Shared memory holds
+//   ring[R][Hp+2][kPitch] : the records of the live diagonals (+ one halo row
+//                           above and below the band), filled by cp.async
+//                           kLookahead steps ahead; entries outside the
+//                           level are zero-filled
+//   xuv[2][S][Hp+2][2]    : U, V each thread produced at the last two steps
+//   xd [3][S][Hp+2][2]    : du, dv of the last three steps (own previous)
+// The neighbours of (x, y, t): left = own registers (step k-1); up =
+// xuv[k-1][t][y-1]; right = xuv[k-1][t-1][y]; down = xuv[k-1][t-1][y+1];
+// own previous du/dv = xd[k-2][t-1][y]; for t = 0 the initial values come
+// from the ring (du = 0 or the carried du of a chained pass).  The band's
+// boundary rows write their U, V into the neighbouring CTA's halo rows of
+// xuv through distributed shared memory.  One (cluster) barrier per step.
+// A thread whose pixel is outside the level computes finite garbage from
+// zero-filled entries and never stores it, so no selects are needed.
 template <int S>
-__global__ void __launch_bounds__(kMaxRowsPerCta, 1)
+__global__ void __launch_bounds__(S * kMaxBandRows, 1)
     k_sor(const double* __restrict__ rec, int B, int W, int H, int Hc, size_t Ls, double omega,
           const double* du_in, const double* dv_in, double* du_out, double* dv_out,
           double* __restrict__ fu, double* __restrict__ fv, uint32_t* status) {
   extern __shared__ double smem[];
   constexpr int R = ring_slots<S>();
+  constexpr int kFieldsPerThread = (8 + S - 1) / S;
   const int C = (int)(gridDim.x / (unsigned)B) > 0 ? (int)(gridDim.x / (unsigned)B) : 1;
   const int c = C > 1 ? (int)cluster_rank() : 0;
   const int b = blockIdx.x / C;
-  const int ty = threadIdx.x;
-  const int Hp = blockDim.x;
+  const int Hp = blockDim.x / S;
+  const int t = threadIdx.x / Hp;       // sweep
+  const int ty = threadIdx.x - t * Hp;  // row within the band
   const int y0 = c * Hc;
   const int y = y0 + ty;
-  const int nrows = min(Hc, H - y0);  // rows this CTA owns
-  const int lane = ty & 31;
-  const int warp = ty >> 5;
-  const int nwarps = Hp >> 5;
+  const int nrows = min(Hc, H - y0);
   const bool row_ok = ty < nrows;
   const int ndiag = W + H - 1;
-  const int slot_rows = Hp + 2;                 // + halo above and below
-  double* ring = smem;                          // [R][slot_rows][kPitch]
-  double* xch = ring + (size_t)R * slot_rows * kPitch;   // [2][nwarps][2][S][2]
-  double* cxin = xch + (size_t)2 * nwarps * 2 * S * 2;   // [2][2][S][2]: 0 from above, 1 from below
+  const int rows = Hp + 2;  // + halo above and below
+  const int slot_elems = rows * kPitch;
+  double* ring = smem;                         // [R][rows][kPitch]
+  double* xuv = ring + R * slot_elems;         // [2][S][rows][2]
+  double* xd = xuv + 2 * S * rows * 2;         // [3][S][rows][2]
   const double* __restrict__ base = rec + (size_t)b * Ls;
   const size_t fstride = (size_t)B * Ls;
   const double* Dui = du_in ? du_in + (size_t)b * Ls : nullptr;  // may alias du_out
   const double* Dvi = dv_in ? dv_in + (size_t)b * Ls : nullptr;
   const double om1 = 1.0 - omega;
   const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
-  const unsigned slot_bytes = (unsigned)(slot_rows * kPitch * 8);
+  const unsigned slot_bytes = (unsigned)(slot_elems * 8);
+  const int me = ty + 1;  // my row index in ring / xuv / xd
 
-  // load ring row r (image row y0 - 1 + r) of diagonal j
-  auto load_row = [&](int j, int r) {
-    const int yy = y0 - 1 + r;
-    const int x = j - yy;
-    const bool ok = yy >= 0 && yy < H && x >= 0 && x < W;
-    const size_t g = ok ? (size_t)j * H + yy : 0;
-    const unsigned dst = ring_s + (unsigned)(j % R) * slot_bytes + (unsigned)(r * kPitch * 8);
+  // cp.async of this thread's record fields (t, t+S, ...) of one ring row;
+  // src = &record[field 0] of the pixel, ok = pixel inside the level
+  auto fetch = [&](unsigned dst, const double* src, bool ok) {
+    const double* g = ok ? src : base;
 #pragma unroll
-    for (int f = 0; f < 8; ++f) cp_async8(dst + 8 * f, base + f * fstride + g, ok ? 8u : 0u);
-  };
-  auto issue = [&](int j) {
-    if (j >= ndiag) return;
-    load_row(j, ty + 1);
-    if (ty == 0) load_row(j, 0);
-    if (ty == Hp - 1) load_row(j, Hp + 1);
+    for (int i = 0; i < kFieldsPerThread; ++i) {
+      const int f = t + i * S;
+      if (f < 8) cp_async8(dst + 8 * f, g + f * fstride, ok ? 8u : 0u);
+    }
   };
 
-  {  // exchange buffers start finite (they feed inactive sweeps at step 0)
-    const int nx = 2 * nwarps * 2 * S * 2 + 2 * 2 * S * 2;
-    for (int i = ty; i < nx; i += Hp) xch[i] = 0.0;
+  {  // exchange buffers start at zero (they feed inactive threads)
+    const int nx = (2 + 3) * S * rows * 2;
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) xuv[i] = 0.0;
   }
-#pragma unroll
-  for (int j = 0; j < kLookahead; ++j) {
-    issue(j);
+  // prefetch state for diagonal jn = k + kLookahead (own row, and the halo
+  // rows for the first / last thread of the band)
+  int jn = 0;
+  unsigned sin_s = ring_s;  // smem slot address of diagonal jn
+  const double* gsrc = base + y;  // &record[jn * H + y]
+  auto issue_next = [&]() {
+    if (jn < ndiag) {
+      const int x = jn - y;
+      fetch(sin_s + (unsigned)(me * kPitch * 8), gsrc, y < H && x >= 0 && x < W);
+      if (ty == 0)
+        fetch(sin_s, gsrc - 1, y0 > 0 && x + 1 >= 0 && x + 1 < W);
+      if (ty == Hp - 1)
+        fetch(sin_s + (unsigned)((Hp + 1) * kPitch * 8), gsrc + 1,
+              y + 1 < H && x - 1 >= 0 && x - 1 < W);
+    }
     cp_async_commit();
-  }
+    ++jn;
+    gsrc += H;
+    sin_s += slot_bytes;
+    if (sin_s == ring_s + (unsigned)R * slot_bytes) sin_s = ring_s;
+  };
+  for (int j = 0; j < kLookahead; ++j) issue_next();
   cp_async_wait<kLookahead - 2>();
   if (C > 1) {
     cluster_arrive();
@@ -259,153 +280,124 @@ __global__ void __launch_bounds__(kMaxRowsPerCta, 1)
     __syncthreads();
   }
 
-  double lU[S], lV[S], lW[S], ldu[S], ldv[S], pdu[S], pdv[S];
-#pragma unroll
-  for (int t = 0; t < S; ++t) lU[t] = lV[t] = lW[t] = ldu[t] = ldv[t] = pdu[t] = pdv[t] = 0.0;
+  double lU = 0.0, lV = 0.0, lW = 0.0;  // this thread's previous pixel (left neighbour)
   const bool hasU = y > 0, hasD = y < H - 1;
-  const bool top_row = ty == 0 && c > 0;                   // gets "up" from CTA c-1
-  const bool bot_row = ty == nrows - 1 && c < C - 1;       // gets "down" from CTA c+1
   bool bad = false;
   const int nsteps = ndiag + 2 * (S - 1);
-  int slot0 = 0;  // (k) mod R
+  // ring slot (element offset) of this sweep's diagonal j = k - 2t, and of j +- 1
+  int sj = ((-2 * t) % R + R) % R;
+  int offj = sj * slot_elems;
+  const int ring_elems = R * slot_elems;
+  // xuv / xd element offsets of (t, me) for each parity / phase
+  const int uv_me = (t * rows + me) * 2;
+  const int uv_par = S * rows * 2;
+  const int d_ph = S * rows * 2;
+  int m3 = 0;  // k mod 3
+  int x = -y - 2 * t;  // pixel of this thread at step k
+  const size_t fplane = (size_t)W * H;
+  const bool top_cx = C > 1 && ty == 0 && c > 0;
+  const bool bot_cx = C > 1 && ty == nrows - 1 && c < C - 1;
   for (int k = 0; k < nsteps; ++k) {
-    issue(k + kLookahead);
-    cp_async_commit();
-    const int rd = (k & 1) ^ 1;
-#pragma unroll
-    for (int t = S - 1; t >= 0; --t) {
-      const int j = k - 2 * t;
-      const int x = j - y;
-      // ring addresses of this sweep's pixel row (slot of diagonal j) and of
-      // the neighbouring diagonals j-1 / j+1
-      int sj = slot0 - 2 * t;
-      sj += sj < 0 ? R : 0;
-      sj += sj < 0 ? R : 0;
-      const int sm = sj == 0 ? R - 1 : sj - 1;
-      const int sp = sj == R - 1 ? 0 : sj + 1;
-      const double* rp = ring + (size_t)sj * slot_rows * kPitch + (size_t)(ty + 1) * kPitch;
-      const double* rm = ring + (size_t)sm * slot_rows * kPitch + (size_t)(ty + 1) * kPitch;
-      const double* rn = ring + (size_t)sp * slot_rows * kPitch + (size_t)(ty + 1) * kPitch;
-      double upU = __shfl_up_sync(kFull, lU[t], 1);
-      double upV = __shfl_up_sync(kFull, lV[t], 1);
-      double dnU = 0.0, dnV = 0.0;
-      if (t > 0) {
-        dnU = __shfl_down_sync(kFull, lU[t - 1], 1);
-        dnV = __shfl_down_sync(kFull, lV[t - 1], 1);
-      }
-      if (lane == 0 && warp > 0) {
-        const double* xs = xch + ((((size_t)rd * nwarps + warp - 1) * 2 + 1) * S + t) * 2;
-        upU = xs[0];
-        upV = xs[1];
-      }
-      if (t > 0 && lane == 31 && warp < nwarps - 1) {
-        const double* xs = xch + ((((size_t)rd * nwarps + warp + 1) * 2 + 0) * S + t - 1) * 2;
-        dnU = xs[0];
-        dnV = xs[1];
-      }
-      if (top_row) {
-        const double* xs = cxin + (((size_t)rd * 2 + 0) * S + t) * 2;
-        upU = xs[0];
-        upV = xs[1];
-      }
-      if (t > 0 && bot_row) {
-        const double* xs = cxin + (((size_t)rd * 2 + 1) * S + t - 1) * 2;
-        dnU = xs[0];
-        dnV = xs[1];
-      }
-      const double uc = rp[F_U], vc = rp[F_V], wp = rp[F_WS];
-      const double m00 = rp[F_M00], m01 = rp[F_M01], m11 = rp[F_M11];
-      const double r0 = rp[F_R0], r1 = rp[F_R1];
-      const double upW = rm[F_WS - kPitch];   // (x, y-1): diagonal j-1, row above
-      const double dnW = rn[F_WS + kPitch];   // (x, y+1): diagonal j+1, row below
-      double rU, rV, rW;
-      if (t > 0) {
-        rU = lU[t - 1];
-        rV = lV[t - 1];
-        rW = lW[t - 1];
-      } else {
+    issue_next();
+    const int j = k - 2 * t;
+    const int offm = (offj == 0 ? ring_elems : offj) - slot_elems;
+    const int offp = offj + slot_elems == ring_elems ? 0 : offj + slot_elems;
+    const double* rp = ring + offj + me * kPitch;        // (x, y)
+    const double* rm = ring + offm + (me - 1) * kPitch;  // (x, y-1)
+    const double* rn = ring + offp + me * kPitch;        // (x+1, y); +kPitch: (x, y+1)
+    const int wpar = k & 1;
+    const double* uvp = xuv + (wpar ? 0 : uv_par) + uv_me;  // step k-1 values at (t, me)
+    const double uc = rp[F_U], vc = rp[F_V], wp = rp[F_WS];
+    const double m00 = rp[F_M00], m01 = rp[F_M01], m11 = rp[F_M11];
+    const double r0 = rp[F_R0], r1 = rp[F_R1];
+    const double upU = uvp[-2], upV = uvp[-1];
+    const double upW = rm[F_WS];
+    const double rW = rn[F_WS];
+    const double dnW = rn[F_WS + kPitch];
+    double rU, rV, dnU, dnV, du, dv;
+    if (t > 0) {
+      const double* q = uvp - rows * 2;  // (t-1, me), (t-1, me+1)
+      rU = q[0];
+      rV = q[1];
+      dnU = q[2];
+      dnV = q[3];
+      const int q2 = m3 == 2 ? 0 : m3 + 1;  // (k-2) mod 3
+      const double* d = xd + q2 * d_ph + uv_me - rows * 2;
+      du = d[0];
+      dv = d[1];
+    } else {
+      rU = rn[F_U];
+      rV = rn[F_V];
+      dnU = rn[F_U + kPitch];
+      dnV = rn[F_V + kPitch];
+      du = 0.0;
+      dv = 0.0;
+      if (Dui) {  // chained pass: the carried du/dv of the previous sweeps
         const int jp = j + 1;
         const bool okp = jp >= 0 && jp < ndiag;
-        const size_t gq = okp ? (size_t)jp * H + y : 0;
-        const size_t gd = okp && hasD ? (size_t)jp * H + y + 1 : 0;
-        rU = rn[F_U] + (Dui ? Dui[gq] : 0.0);
-        rV = rn[F_V] + (Dvi ? Dvi[gq] : 0.0);
-        rW = rn[F_WS];
-        dnU = rn[F_U + kPitch] + (Dui ? Dui[gd] : 0.0);
-        dnV = rn[F_V + kPitch] + (Dvi ? Dvi[gd] : 0.0);
-      }
-      // absent neighbours (borders) contribute wq = +0 times a finite value:
-      // adding an exact zero leaves the reference's partial sums unchanged
-      const double wqL = x > 0 ? 0.5 * (wp + lW[t]) : 0.0;
-      const double wqR = x < W - 1 ? 0.5 * (wp + rW) : 0.0;
-      const double wqU = hasU ? 0.5 * (wp + upW) : 0.0;
-      const double wqD = hasD ? 0.5 * (wp + dnW) : 0.0;
-      const double sw = (((0.0 + wqL) + wqR) + wqU) + wqD;
-      const double su = (((0.0 + wqL * (lU[t] - uc)) + wqR * (rU - uc)) + wqU * (upU - uc)) +
-                        wqD * (dnU - uc);
-      const double sv = (((0.0 + wqL * (lV[t] - vc)) + wqR * (rV - vc)) + wqU * (upV - vc)) +
-                        wqD * (dnV - vc);
-      double du, dv;
-      if (t > 0) {
-        du = pdu[t - 1];
-        dv = pdv[t - 1];
-      } else {
         const bool ok = j >= 0 && j < ndiag;
-        du = Dui ? Dui[ok ? (size_t)j * H + y : 0] : 0.0;
-        dv = Dvi ? Dvi[ok ? (size_t)j * H + y : 0] : 0.0;
-      }
-      const double den_u = m00 + sw;
-      const double nu = om1 * du + omega * ((r0 + su - m01 * dv) / den_u);
-      du = den_u > 1e-12 ? nu : du;
-      const double den_v = m11 + sw;
-      const double nv = om1 * dv + omega * ((r1 + sv - m01 * du) / den_v);
-      dv = den_v > 1e-12 ? nv : dv;
-      const double U = uc + du, V = vc + dv;
-      pdu[t] = ldu[t];
-      pdv[t] = ldv[t];
-      ldu[t] = du;
-      ldv[t] = dv;
-      lU[t] = U;
-      lV[t] = V;
-      lW[t] = wp;
-      if (t == S - 1 && row_ok && x >= 0 && x < W) {
-        if (du_out) {
-          du_out[(size_t)b * Ls + (size_t)j * H + y] = du;
-          dv_out[(size_t)b * Ls + (size_t)j * H + y] = dv;
-        }
-        if (fu) {
-          const size_t o = (size_t)b * W * H + (size_t)y * W + x;
-          fu[o] = U;
-          fv[o] = V;
-          bad |= !(isfinite(U) && isfinite(V));
-        }
+        rU = rU + Dui[okp ? (size_t)jp * H + y : 0];
+        rV = rV + Dvi[okp ? (size_t)jp * H + y : 0];
+        dnU = dnU + Dui[okp && hasD ? (size_t)jp * H + y + 1 : 0];
+        dnV = dnV + Dvi[okp && hasD ? (size_t)jp * H + y + 1 : 0];
+        du = Dui[ok ? (size_t)j * H + y : 0];
+        dv = Dvi[ok ? (size_t)j * H + y : 0];
+      } else {
+        rU = rU + 0.0;  // u + du with du = 0 (reference: u[q] + du[q])
+        rV = rV + 0.0;
+        dnU = dnU + 0.0;
+        dnV = dnV + 0.0;
       }
     }
-    // publish boundary rows for the next step
-    if (lane == 0 || lane == 31) {
-      double* xs = xch + (((size_t)(k & 1) * nwarps + warp) * 2 + (lane == 31 ? 1 : 0)) * S * 2;
-#pragma unroll
-      for (int t = 0; t < S; ++t) {
-        xs[2 * t] = lU[t];
-        xs[2 * t + 1] = lV[t];
+    // absent neighbours (borders) contribute wq = +0 times a finite value:
+    // adding an exact zero leaves the reference's partial sums unchanged
+    const double wqL = x > 0 ? 0.5 * (wp + lW) : 0.0;
+    const double wqR = x < W - 1 ? 0.5 * (wp + rW) : 0.0;
+    const double wqU = hasU ? 0.5 * (wp + upW) : 0.0;
+    const double wqD = hasD ? 0.5 * (wp + dnW) : 0.0;
+    const double sw = (((0.0 + wqL) + wqR) + wqU) + wqD;
+    const double su =
+        (((0.0 + wqL * (lU - uc)) + wqR * (rU - uc)) + wqU * (upU - uc)) + wqD * (dnU - uc);
+    const double sv =
+        (((0.0 + wqL * (lV - vc)) + wqR * (rV - vc)) + wqU * (upV - vc)) + wqD * (dnV - vc);
+    const double den_u = m00 + sw;
+    const double nu = om1 * du + omega * exact_div_pos(r0 + su - m01 * dv, den_u);
+    du = den_u > 1e-12 ? nu : du;
+    const double den_v = m11 + sw;
+    const double nv = om1 * dv + omega * exact_div_pos(r1 + sv - m01 * du, den_v);
+    dv = den_v > 1e-12 ? nv : dv;
+    const double U = uc + du, V = vc + dv;
+    lU = U;
+    lV = V;
+    lW = wp;
+    {
+      double* o = xuv + (wpar ? uv_par : 0) + uv_me;
+      o[0] = U;
+      o[1] = V;
+      double* od = xd + m3 * d_ph + uv_me;
+      od[0] = du;
+      od[1] = dv;
+      if (top_cx) {  // my band's first row -> CTA c-1's row below its band
+        double* h = o + (Hc + 1 - me) * 2;
+        st_cluster(h, c - 1, U);
+        st_cluster(h + 1, c - 1, V);
+      }
+      if (bot_cx) {  // my band's last row -> CTA c+1's row above its band
+        double* h = o - me * 2;
+        st_cluster(h, c + 1, U);
+        st_cluster(h + 1, c + 1, V);
       }
     }
-    if (C > 1) {
-      if (ty == 0 && c > 0) {  // my first row -> CTA c-1's "from below"
-        double* xs = cxin + (((size_t)(k & 1) * 2 + 1) * S) * 2;
-#pragma unroll
-        for (int t = 0; t < S; ++t) {
-          st_cluster(xs + 2 * t, c - 1, lU[t]);
-          st_cluster(xs + 2 * t + 1, c - 1, lV[t]);
-        }
+    if (t == S - 1 && row_ok && x >= 0 && x < W) {
+      if (du_out) {
+        du_out[(size_t)b * Ls + (size_t)j * H + y] = du;
+        dv_out[(size_t)b * Ls + (size_t)j * H + y] = dv;
       }
-      if (ty == nrows - 1 && c < C - 1) {  // my last row -> CTA c+1's "from above"
-        double* xs = cxin + (((size_t)(k & 1) * 2 + 0) * S) * 2;
-#pragma unroll
-        for (int t = 0; t < S; ++t) {
-          st_cluster(xs + 2 * t, c + 1, lU[t]);
-          st_cluster(xs + 2 * t + 1, c + 1, lV[t]);
-        }
+      if (fu) {
+        const size_t o = (size_t)b * fplane + (size_t)y * W + x;
+        fu[o] = U;
+        fv[o] = V;
+        bad |= !(isfinite(U) && isfinite(V));
       }
     }
     cp_async_wait<kLookahead - 2>();
@@ -415,17 +407,18 @@ __global__ void __launch_bounds__(kMaxRowsPerCta, 1)
     } else {
       __syncthreads();
     }
-    slot0 = slot0 == R - 1 ? 0 : slot0 + 1;
+    offj = offp;
+    m3 = m3 == 2 ? 0 : m3 + 1;
+    ++x;
   }
   if (bad) set_status(status, DIS_STATUS_NONFINITE_FLOW);
 }
 
 template <int S>
-static size_t sor_smem_bytes(int threads) {
-  const size_t ring = (size_t)ring_slots<S>() * (threads + 2) * kPitch * sizeof(double);
-  const size_t xch = (size_t)2 * (threads / 32) * 2 * S * 2 * sizeof(double);
-  const size_t cx = (size_t)2 * 2 * S * 2 * sizeof(double);
-  return ring + xch + cx;
+static size_t sor_smem_bytes(int hp) {
+  const size_t rows = (size_t)hp + 2;
+  return ((size_t)ring_slots<S>() * rows * kPitch + (size_t)(2 + 3) * S * rows * 2) *
+         sizeof(double);
 }
 
 constexpr size_t kMaxSmem = 227 * 1024;
@@ -435,11 +428,14 @@ constexpr size_t kMaxSmem = 227 * 1024;
 // several SMs (the step rate of one band is bound by its SM's FP64 pipe).
 template <int S>
 static int choose_cluster(int B, int H) {
+  static const int forced = [] {
+    const char* e = getenv("DIS_SOR_CLUSTER");  // experiments only
+    return e ? atoi(e) : 0;
+  }();
+  if (forced > 0) return forced;
+  auto hp = [&](int C) { return ((H + C - 1) / C + 31) / 32 * 32; };
   int C = 1;
-  while (C < 8 && ((H + C - 1) / C > kMaxRowsPerCta ||
-                   sor_smem_bytes<S>(((H + C - 1) / C + 31) / 32 * 32) > kMaxSmem))
-    ++C;
-  while (C < 8 && B * (C + 1) <= 148 && (H + C) / (C + 1) >= 64) ++C;
+  while (C < 16 && (hp(C) > kMaxBandRows || sor_smem_bytes<S>(hp(C)) > kMaxSmem)) ++C;
   return C;
 }
 
@@ -448,9 +444,10 @@ static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const
                         double* duo, double* dvo, bool final_pass, cudaStream_t st) {
   const int C = choose_cluster<S>(a.B, a.H);
   const int Hc = (a.H + C - 1) / C;
-  const int threads = (Hc + 31) / 32 * 32;
-  const size_t smem = sor_smem_bytes<S>(threads);
-  if (threads > kMaxRowsPerCta || smem > kMaxSmem) return DIS_ERR_VALUE;
+  const int hp = (Hc + 31) / 32 * 32;
+  const int threads = hp * S;
+  const size_t smem = sor_smem_bytes<S>(hp);
+  if (hp > kMaxBandRows || smem > kMaxSmem) return DIS_ERR_VALUE;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_sor<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
@@ -498,7 +495,7 @@ static int launch_sor(const RefineArgs& a, size_t Ls, int S, const double* dui,
 }
 
 int launch_refine(const RefineArgs& a, cudaStream_t st) {
-  if (a.H > 8 * kMaxRowsPerCta) return DIS_ERR_VALUE;  // at most 8 CTAs per pair
+  if (a.H > 2048) return DIS_ERR_VALUE;  // at most 8 CTAs of <= 256 rows per pair
   const size_t Ls = (size_t)(a.W + a.H - 1) * a.H;
   double* carry_u = a.rec + (size_t)kRecords * a.B * Ls;
   double* carry_v = carry_u + (size_t)a.B * Ls;
