@@ -185,7 +185,11 @@ DIS_API int dis_patch_search(const double* ref_img, const double* ref_gx,
                      const double* coarse_flow_v, int32_t Wc, int32_t Hc,
                      const dis_params_t* p, double* out_u, double* out_v,
                      double* out_off, double* out_mar, double* out_init_u,
-                     double* out_init_v, uint8_t* out_valid, void* stream);
+                     double* out_init_v, uint8_t* out_valid, void* workspace,
+                     size_t workspace_bytes, void* stream);
+/* Scratch for dis_patch_search (per-patch prep records + work counter). */
+DIS_API size_t dis_patch_search_workspace_bytes(int32_t B, int32_t W, int32_t H,
+                                                const dis_params_t* p);
 
 /* densify (densification.py:173-191): dense flow of level s. */
 DIS_API int dis_densify(const double* ref_img, const double* qry_img, int32_t B,

@@ -29,7 +29,8 @@ DTYPE_F32, DTYPE_F64, DTYPE_U8 = 0, 1, 2
 EXPORTED = (
     "dis_params_default", "dis_params_validate", "dis_workspace_bytes", "dis_flow_batch",
     "dis_host_workspace_bytes", "dis_flow_batch_host", "dis_read_status",
-    "dis_status_to_error", "dis_build_pyramid", "dis_patch_search", "dis_densify",
+    "dis_status_to_error", "dis_build_pyramid", "dis_patch_search",
+    "dis_patch_search_workspace_bytes", "dis_densify",
     "dis_refine_workspace_bytes", "dis_refine", "dis_upsample_flow", "dis_grid_axis",
     "dis_last_error", "dis_abi_version", "dis_last_launch_count", "dis_profile_enable",
     "dis_profile_reset", "dis_profile_read",
@@ -75,7 +76,9 @@ def lib() -> ctypes.CDLL:
                                     _vp, _vp]
     L.dis_build_pyramid.restype = ctypes.c_int
     L.dis_patch_search.argtypes = [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _i32, _i32,
-                                   _pp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+                                   _pp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
+    L.dis_patch_search_workspace_bytes.argtypes = [_i32, _i32, _i32, _pp]
+    L.dis_patch_search_workspace_bytes.restype = _sz
     L.dis_patch_search.restype = ctypes.c_int
     L.dis_densify.argtypes = [_vp, _vp, _i32, _i32, _i32, _pp, _vp, _vp, _vp, _vp, _vp, _vp,
                               _vp]

@@ -103,6 +103,7 @@ struct Plan {
   size_t off_pu[32], off_pv[32], off_poff[32];
   size_t off_fu[32], off_fv[32];
   size_t off_rec;
+  size_t off_search;
   size_t total;
 };
 
@@ -160,6 +161,14 @@ void make_plan(const dis_params_t* p, int B, int H, int W, Plan* pl) {
     const size_t n = (size_t)B * H * W;
     pl->off_fu[0] = take(cur, n * d);
     pl->off_fv[0] = take(cur, n * d);
+  }
+  {
+    size_t mx = 0;
+    for (int s = pl->sf; s <= pl->ss; ++s) {
+      size_t r = patch_search_scratch_bytes(B, pl->ax[s].n * pl->ay[s].n);
+      if (r > mx) mx = r;
+    }
+    pl->off_search = take(cur, mx);
   }
   pl->off_rec = kNone;
   if (pl->var) {
@@ -237,7 +246,7 @@ int run_pipeline(const Plan& pl, const dis_params_t* p, double* out, void* ws,
     a.out_u = at<double>(ws, pl.off_pu[s]);
     a.out_v = at<double>(ws, pl.off_pv[s]);
     a.out_off = at<double>(ws, pl.off_poff[s]);
-    launch_patch_search(a, st);
+    launch_patch_search(a, at<char>(ws, pl.off_search), st);
     double* fu = at<double>(ws, pl.off_fu[s]);
     double* fv = at<double>(ws, pl.off_fv[s]);
     launch_densify(ref, qry, pl.B, w, h, pl.ax[s], pl.ay[s], pl.ps, a.out_u, a.out_v,
@@ -553,13 +562,24 @@ int32_t dis_grid_axis(int32_t dim, int32_t patch_size, double overlap, int32_t* 
   return a.n;
 }
 
+size_t dis_patch_search_workspace_bytes(int32_t B, int32_t W, int32_t H,
+                                        const dis_params_t* p) {
+  if (dis_params_validate(p) || W < p->patch_size || H < p->patch_size) return 0;
+  const int sp = grid_spacing(p->patch_size, p->overlap);
+  return patch_search_scratch_bytes(
+      B, make_axis(W, p->patch_size, sp).n * make_axis(H, p->patch_size, sp).n);
+}
+
 int dis_patch_search(const double* ref_img, const double* ref_gx, const double* ref_gy,
                      const double* qry_img, int32_t B, int32_t W, int32_t H,
                      const double* coarse_flow_u, const double* coarse_flow_v, int32_t Wc,
                      int32_t Hc, const dis_params_t* p, double* out_u, double* out_v,
                      double* out_off, double* out_mar, double* out_init_u, double* out_init_v,
-                     uint8_t* out_valid, void* stream) {
+                     uint8_t* out_valid, void* workspace, size_t workspace_bytes,
+                     void* stream) {
   if (dis_params_validate(p)) return DIS_ERR_PARAMETER;
+  if (workspace_bytes < dis_patch_search_workspace_bytes(B, W, H, p))
+    return fail(DIS_ERR_WORKSPACE, "patch search workspace too small");
   if (W < p->patch_size || H < p->patch_size)
     return fail(DIS_ERR_VALUE, "level %dx%d is smaller than the patch size %d", W, H,
                 p->patch_size);
@@ -590,7 +610,7 @@ int dis_patch_search(const double* ref_img, const double* ref_gx, const double* 
   a.out_iu = out_init_u;
   a.out_iv = out_init_v;
   a.out_valid = out_valid;
-  launch_patch_search(a, as_stream(stream));
+  launch_patch_search(a, workspace, as_stream(stream));
   return check_cuda("dis_patch_search");
 }
 

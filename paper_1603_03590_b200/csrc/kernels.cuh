@@ -52,7 +52,8 @@ struct SearchArgs {
   uint8_t* out_valid; // optional
   int32_t* out_evals; // optional
 };
-void launch_patch_search(const SearchArgs& a, cudaStream_t st);
+size_t patch_search_scratch_bytes(int B, int P);
+void launch_patch_search(const SearchArgs& a, void* scratch, cudaStream_t st);
 
 // densify.cu
 void launch_densify(const double* ref, const double* qry, int B, int W, int H, GridAxis ax,

@@ -65,11 +65,21 @@ __device__ __forceinline__ bool hypot_gt(double a, double b, int ps) {
   return (s - t_hi) + (lo - t_lo) > 0.0;
 }
 
-__global__ void __launch_bounds__(128) k_patch_search(SearchArgs a) {
+// ---------------------------------------------------------------------------
+// Stage 1 — per-patch prep (one thread per patch): init_patches,
+// _patch_precompute and _condition_hessians.  Writes the kPrep record the
+// Gauss-Newton stage needs; resets the GN work counter.
+// ---------------------------------------------------------------------------
+enum PrepField { PR_U0 = 0, PR_V0, PR_MEAN, PR_I00, PR_I01, PR_I11, PR_VALID, kPrep };
+
+__global__ void __launch_bounds__(128) k_patch_prep(SearchArgs a, double* __restrict__ prep,
+                                                     unsigned* counter) {
   const int nx = a.ax.n;
   const int P = nx * a.ay.n;
+  const size_t N = (size_t)a.B * P;
   const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (size_t)a.B * P) return;
+  if (gid == 0) *counter = 0u;
+  if (gid >= N) return;
   const int b = (int)(gid / P);
   const int i = (int)(gid - (size_t)b * P);
   const int iy = i / nx;
@@ -77,26 +87,24 @@ __global__ void __launch_bounds__(128) k_patch_search(SearchArgs a) {
   const int ps = a.ps, W = a.W, H = a.H;
   const int x0i = a.ax.origin(ix);
   const int y0i = a.ay.origin(iy);
-  const double x0 = (double)x0i;
-  const double y0 = (double)y0i;
   const size_t plane = (size_t)W * H;
   const double* __restrict__ ref = a.ref + b * plane;
   const double* __restrict__ rgx = a.rgx + b * plane;
   const double* __restrict__ rgy = a.rgy + b * plane;
-  const double* __restrict__ qry = a.qry + b * plane;
 
   // ---- init_patches (densification.py:82-95) ----
   double u0 = 0.0, v0 = 0.0;
   if (a.cu) {
     const size_t cplane = (size_t)a.Wc * a.Hc;
     const double half = 0.5 * ps;
-    const double xs = (x0 + half) / 2.0;
-    const double ys = (y0 + half) / 2.0;
+    const double xs = ((double)x0i + half) / 2.0;
+    const double ys = ((double)y0i + half) / 2.0;
     u0 = bilin_np(a.cu + b * cplane, a.Wc, a.Hc, xs, ys) * 2.0;
     v0 = bilin_np(a.cv + b * cplane, a.Wc, a.Hc, xs, ys) * 2.0;
   }
 
   // ---- _patch_precompute (inverse_search.py:75-98) ----
+  // samples at integer coordinates: the reference's _bilin returns the pixel
   double tsum = 0.0, h00 = 0.0, h01 = 0.0, h11 = 0.0;
   for (int oy = 0; oy < ps; ++oy) {
     const size_t row = (size_t)(y0i + oy) * W + x0i;
@@ -123,102 +131,320 @@ __global__ void __launch_bounds__(128) k_patch_search(SearchArgs a) {
   const double lmin = 0.5 * (tr - disc);
   const double lmax = 0.5 * (tr + disc);
   const bool valid = (det > 1e-6 * rel) && (lmin > 0.0) && (lmax <= 1e6 * lmin);
-  const double i00 = valid ? h11 / det : 0.0;
-  const double i01 = valid ? -h01 / det : 0.0;
-  const double i11 = valid ? h00 / det : 0.0;
+  prep[PR_U0 * N + gid] = u0;
+  prep[PR_V0 * N + gid] = v0;
+  prep[PR_MEAN * N + gid] = mean_t;
+  prep[PR_I00 * N + gid] = valid ? h11 / det : 0.0;
+  prep[PR_I01 * N + gid] = valid ? -h01 / det : 0.0;
+  prep[PR_I11 * N + gid] = valid ? h00 / det : 0.0;
+  prep[PR_VALID * N + gid] = valid ? 1.0 : 0.0;
+  if (a.out_iu) a.out_iu[gid] = u0;
+  if (a.out_iv) a.out_iv[gid] = v0;
+  if (a.out_valid) a.out_valid[gid] = valid ? 1 : 0;
+}
 
-  // ---- _patch_optimize (inverse_search.py:113-189) ----
-  double u = u0, v = v0;
-  double prev_ssd = 1e300, prev_u = u, prev_v = v, prev_off = 0.0, prev_mar = 0.0;
-  bool stop_after_eval = !valid;
-  int k = 0;
-  double off = 0.0, mar = 0.0, off0 = 0.0, mar0 = 0.0;
-  int evals = 0;
-  const int code = a.code;
-  const double hb = a.hb;
-  for (;;) {
-    const double bx = x0 + u;
-    const double by = y0 + v;
-    double wsum = 0.0;
-    for (int oy = 0; oy < ps; ++oy)
-      for (int ox = 0; ox < ps; ++ox) wsum += bilin_nb(qry, W, H, bx + ox, by + oy);
-    off = a.mean_norm ? exact_div_pos(wsum, dn) - mean_t : 0.0;
-    double ssd = 0.0, b0 = 0.0, b1 = 0.0;
-    mar = 0.0;
-    for (int oy = 0; oy < ps; ++oy) {
-      const size_t row = (size_t)(y0i + oy) * W + x0i;
+// ---------------------------------------------------------------------------
+// Stage 2 — inverse-compositional Gauss-Newton (_patch_optimize,
+// inverse_search.py:113-189) + reset_outliers + refresh.
+//
+// Persistent lanes pulling patches from a work queue (warp-aggregated
+// atomicAdd on a counter): a lane whose patch exits early (rollback,
+// convergence) takes the next patch instead of idling until the slowest lane
+// of its warp is done (mean 3-5.5 window evaluations, p99 up
+// to 22).  Which lane computes which patch never affects a patch's result.
+//
+// One window evaluation = the reference's two passes over the ps x ps
+// samples (sum for the mean offset; then residuals, SSD and the steepest
+// descent products), sequential in row-major order.  Each sample's
+// coordinate is (bx + ox, by + oy): its clamp, integer part and fraction
+// depend on ox alone or oy alone, so they are computed once per column /
+// row of the window (bit-identical to clamping every sample).
+// ---------------------------------------------------------------------------
+struct Axis1 {
+  int i0, i1;
+  double f;
+};
+__device__ __forceinline__ Axis1 axis_sample(double c, int n) {
+  if (!(c >= 0.0))
+    c = 0.0;
+  else if (c > n - 1.0)
+    c = n - 1.0;
+  Axis1 a;
+  a.i0 = (int)c;
+  a.i1 = a.i0 + 1 > n - 1 ? n - 1 : a.i0 + 1;
+  a.f = c - (double)a.i0;
+  return a;
+}
+
+struct Lane {
+  int pid;  // patch (b * P + i) or -1
+  int b, x0i, y0i;
+  double u, v, u0, v0, prev_ssd, prev_u, prev_v, prev_off, prev_mar, off0, mar0;
+  double mean_t, i00, i01, i11;
+  int k, evals;
+  bool stop;
+};
+
+// window evaluation at (bx, by); PS > 0: compile-time patch size
+template <int PS>
+__device__ __forceinline__ void eval_window(const double* __restrict__ qry,
+                                            const double* __restrict__ ref,
+                                            const double* __restrict__ rgx,
+                                            const double* __restrict__ rgy, int W, int H,
+                                            int ps_rt, int x0i, int y0i, double bx, double by,
+                                            double mean_t, bool mean_norm, int code, double hb,
+                                            double& off, double& ssd, double& b0, double& b1,
+                                            double& mar) {
+  constexpr int MAXC = PS > 0 ? PS : 1;
+  const int ps = PS > 0 ? PS : ps_rt;
+  const double dn = (double)(ps * ps);
+  int X0[MAXC], X1[MAXC];
+  double FX[MAXC];
+  if (PS > 0) {
+#pragma unroll
+    for (int ox = 0; ox < MAXC; ++ox) {
+      const Axis1 ax = axis_sample(bx + ox, W);
+      X0[ox] = ax.i0;
+      X1[ox] = ax.i1;
+      FX[ox] = ax.f;
+    }
+  }
+  double wsum = 0.0;
+  for (int oy = 0; oy < ps; ++oy) {
+    const Axis1 ay = axis_sample(by + oy, H);
+    const double* r0 = qry + (size_t)ay.i0 * W;
+    const double* r1 = qry + (size_t)ay.i1 * W;
+    if (PS > 0) {
+#pragma unroll
+      for (int ox = 0; ox < MAXC; ++ox) {
+        const double i00 = __ldg(r0 + X0[ox]), i01 = __ldg(r0 + X1[ox]);
+        const double i10 = __ldg(r1 + X0[ox]), i11 = __ldg(r1 + X1[ox]);
+        const double a = i00 + FX[ox] * (i01 - i00);
+        const double bb = i10 + FX[ox] * (i11 - i10);
+        wsum += a + ay.f * (bb - a);
+      }
+    } else {
       for (int ox = 0; ox < ps; ++ox) {
-        const double val = bilin_nb(qry, W, H, bx + ox, by + oy);
-        const double e = val - off - __ldg(ref + row + ox);
+        const Axis1 ax = axis_sample(bx + ox, W);
+        const double i00 = __ldg(r0 + ax.i0), i01 = __ldg(r0 + ax.i1);
+        const double i10 = __ldg(r1 + ax.i0), i11 = __ldg(r1 + ax.i1);
+        const double a = i00 + ax.f * (i01 - i00);
+        const double bb = i10 + ax.f * (i11 - i10);
+        wsum += a + ay.f * (bb - a);
+      }
+    }
+  }
+  off = mean_norm ? exact_div_pos(wsum, dn) - mean_t : 0.0;
+  ssd = 0.0;
+  b0 = 0.0;
+  b1 = 0.0;
+  mar = 0.0;
+  for (int oy = 0; oy < ps; ++oy) {
+    const Axis1 ay = axis_sample(by + oy, H);
+    const double* r0 = qry + (size_t)ay.i0 * W;
+    const double* r1 = qry + (size_t)ay.i1 * W;
+    const size_t row = (size_t)(y0i + oy) * W + x0i;
+    const double* tr = ref + row;
+    const double* gxr = rgx + row;
+    const double* gyr = rgy + row;
+#pragma unroll
+    for (int ox = 0; ox < (PS > 0 ? MAXC : 1); ++ox) {
+      for (int oxr = 0; oxr < (PS > 0 ? 1 : ps); ++oxr) {
+        const int c = PS > 0 ? ox : oxr;
+        int xi0, xi1;
+        double fx;
+        if (PS > 0) {
+          xi0 = X0[ox];
+          xi1 = X1[ox];
+          fx = FX[ox];
+        } else {
+          const Axis1 ax = axis_sample(bx + oxr, W);
+          xi0 = ax.i0;
+          xi1 = ax.i1;
+          fx = ax.f;
+        }
+        const double i00 = __ldg(r0 + xi0), i01 = __ldg(r0 + xi1);
+        const double i10 = __ldg(r1 + xi0), i11 = __ldg(r1 + xi1);
+        const double a = i00 + fx * (i01 - i00);
+        const double bb = i10 + fx * (i11 - i10);
+        const double val = a + ay.f * (bb - a);
+        const double e = val - off - __ldg(tr + c);
         mar += fabs(e);
         const double et = transform_residual(e, code, hb);
         ssd += et * et;
-        b0 += __ldg(rgx + row + ox) * et;
-        b1 += __ldg(rgy + row + ox) * et;
+        b0 += __ldg(gxr + c) * et;
+        b1 += __ldg(gyr + c) * et;
       }
     }
-    mar = exact_div_pos(mar, dn);
-    if (evals == 0) {
-      off0 = off;
-      mar0 = mar;
-    }
-    ++evals;
-    if (ssd > prev_ssd) {
-      u = prev_u;
-      v = prev_v;
-      off = prev_off;
-      mar = prev_mar;
-      break;
-    }
-    if (stop_after_eval || k >= a.iters) break;
-    prev_ssd = ssd;
-    prev_u = u;
-    prev_v = v;
-    prev_off = off;
-    prev_mar = mar;
-    const double du = i00 * b0 + i01 * b1;
-    const double dv = i01 * b0 + i11 * b1;
-    u -= du;
-    v -= dv;
-    k += 1;
-    if (sqrt(du * du + dv * dv) < 1e-2) stop_after_eval = true;
-    const double cx = x0 + u + 0.5 * ps;
-    const double cy = y0 + v + 0.5 * ps;
-    if (cx < (double)(-W) || cx > 2.0 * W || cy < (double)(-H) || cy > 2.0 * H) {
-      u = u0;
-      v = v0;
-      prev_ssd = 1e300;
-      stop_after_eval = true;
-    }
   }
-
-  // ---- reset_outliers + refresh_patch_stats ----
-  if (hypot_gt(u - u0, v - v0, ps)) {
-    u = u0;
-    v = v0;
-    off = a.mean_norm ? off0 : 0.0;
-    mar = mar0;
-  }
-
-  const size_t o = (size_t)b * P + i;
-  a.out_u[o] = u;
-  a.out_v[o] = v;
-  a.out_off[o] = off;
-  if (a.out_mar) a.out_mar[o] = mar;
-  if (a.out_iu) a.out_iu[o] = u0;
-  if (a.out_iv) a.out_iv[o] = v0;
-  if (a.out_valid) a.out_valid[o] = valid ? 1 : 0;
-  if (a.out_evals) a.out_evals[o] = evals;
+  mar = exact_div_pos(mar, dn);
 }
 
-void launch_patch_search(const SearchArgs& a, cudaStream_t st) {
+template <int PS>
+__global__ void __launch_bounds__(256) k_patch_gn(SearchArgs a, const double* __restrict__ prep,
+                                                   unsigned* counter) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int nx = a.ax.n;
+  const int P = nx * a.ay.n;
+  const unsigned N = (unsigned)(a.B * P);
+  const int W = a.W, H = a.H, ps = PS > 0 ? PS : a.ps;
+  const size_t plane = (size_t)W * H;
+  const bool mean_norm = a.mean_norm != 0;
+  Lane L;
+  L.pid = -1;
+  bool done = false;
+  for (;;) {
+    // ---- fetch: lanes without a patch take the next ones from the queue ----
+    const bool need = !done && L.pid < 0;
+    const unsigned mask = __ballot_sync(FULL, need);
+    if (mask) {
+      const int leader = __ffs(mask) - 1;
+      unsigned base = 0;
+      if (lane == leader) base = atomicAdd(counter, (unsigned)__popc(mask));
+      base = __shfl_sync(FULL, base, leader);
+      if (need) {
+        const unsigned g = base + (unsigned)__popc(mask & ((1u << lane) - 1u));
+        if (g >= N) {
+          done = true;
+        } else {
+          L.pid = (int)g;
+          L.b = (int)(g / (unsigned)P);
+          const int i = (int)(g - (unsigned)L.b * (unsigned)P);
+          const int iy = i / nx;
+          L.x0i = a.ax.origin(i - iy * nx);
+          L.y0i = a.ay.origin(iy);
+          L.u0 = prep[PR_U0 * (size_t)N + g];
+          L.v0 = prep[PR_V0 * (size_t)N + g];
+          L.mean_t = prep[PR_MEAN * (size_t)N + g];
+          L.i00 = prep[PR_I00 * (size_t)N + g];
+          L.i01 = prep[PR_I01 * (size_t)N + g];
+          L.i11 = prep[PR_I11 * (size_t)N + g];
+          L.stop = !(prep[PR_VALID * (size_t)N + g] != 0.0);
+          L.u = L.u0;
+          L.v = L.v0;
+          L.prev_ssd = 1e300;
+          L.prev_u = L.u;
+          L.prev_v = L.v;
+          L.prev_off = 0.0;
+          L.prev_mar = 0.0;
+          L.k = 0;
+          L.evals = 0;
+        }
+      }
+    }
+    if (__all_sync(FULL, done)) break;
+    if (done) continue;
+
+    // ---- one window evaluation + Gauss-Newton update (inverse_search.py:124-188) ----
+    const double x0 = (double)L.x0i, y0 = (double)L.y0i;
+    const size_t po = (size_t)L.b * plane;
+    double off, ssd, b0, b1, mar;
+    eval_window<PS>(a.qry + po, a.ref + po, a.rgx + po, a.rgy + po, W, H, ps, L.x0i, L.y0i,
+                    x0 + L.u, y0 + L.v, L.mean_t, mean_norm, a.code, a.hb, off, ssd, b0, b1,
+                    mar);
+    if (L.evals == 0) {
+      L.off0 = off;
+      L.mar0 = mar;
+    }
+    ++L.evals;
+    bool finished = false;
+    double u = L.u, v = L.v;
+    if (ssd > L.prev_ssd) {
+      u = L.prev_u;
+      v = L.prev_v;
+      off = L.prev_off;
+      mar = L.prev_mar;
+      finished = true;
+    } else if (L.stop || L.k >= a.iters) {
+      finished = true;
+    } else {
+      L.prev_ssd = ssd;
+      L.prev_u = u;
+      L.prev_v = v;
+      L.prev_off = off;
+      L.prev_mar = mar;
+      const double du = L.i00 * b0 + L.i01 * b1;
+      const double dv = L.i01 * b0 + L.i11 * b1;
+      u -= du;
+      v -= dv;
+      L.k += 1;
+      if (sqrt(du * du + dv * dv) < 1e-2) L.stop = true;
+      const double cx = x0 + u + 0.5 * ps;
+      const double cy = y0 + v + 0.5 * ps;
+      if (cx < (double)(-W) || cx > 2.0 * W || cy < (double)(-H) || cy > 2.0 * H) {
+        u = L.u0;
+        v = L.v0;
+        L.prev_ssd = 1e300;
+        L.stop = true;
+      }
+      L.u = u;
+      L.v = v;
+    }
+    if (finished) {
+      // ---- reset_outliers + refresh_patch_stats ----
+      if (hypot_gt(u - L.u0, v - L.v0, ps)) {
+        u = L.u0;
+        v = L.v0;
+        off = mean_norm ? L.off0 : 0.0;
+        mar = L.mar0;
+      }
+      const size_t o = (size_t)L.pid;
+      a.out_u[o] = u;
+      a.out_v[o] = v;
+      a.out_off[o] = off;
+      if (a.out_mar) a.out_mar[o] = mar;
+      if (a.out_evals) a.out_evals[o] = L.evals;
+      L.pid = -1;
+    }
+  }
+}
+
+static int gn_blocks(const void* fn) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return (per_sm > 0 ? per_sm : 1) * sms;
+}
+
+size_t patch_search_scratch_bytes(int B, int P) {
+  return ((size_t)kPrep * B * P) * sizeof(double) + 256;
+}
+
+void launch_patch_search(const SearchArgs& a, void* scratch, cudaStream_t st) {
   const size_t n = (size_t)a.B * a.ax.n * a.ay.n;
-  const int TH = 128;
-  const unsigned blocks = (unsigned)((n + TH - 1) / TH);
+  double* prep = static_cast<double*>(scratch);
+  unsigned* counter = reinterpret_cast<unsigned*>(static_cast<char*>(scratch) +
+                                                  (size_t)kPrep * n * sizeof(double));
   prof_begin(KC_SEARCH, st);
-  k_patch_search<<<blocks, TH, 0, st>>>(a);
-  prof_end(KC_SEARCH, st);
+  const int TH = 128;
+  k_patch_prep<<<(unsigned)((n + TH - 1) / TH), TH, 0, st>>>(a, prep, counter);
   note_launch();
+  int blocks;
+  static int nb8 = 0, nb12 = 0, nb0 = 0;
+  if (a.ps == 8) {
+    if (!nb8) nb8 = gn_blocks((const void*)k_patch_gn<8>);
+    blocks = nb8;
+  } else if (a.ps == 12) {
+    if (!nb12) nb12 = gn_blocks((const void*)k_patch_gn<12>);
+    blocks = nb12;
+  } else {
+    if (!nb0) nb0 = gn_blocks((const void*)k_patch_gn<0>);
+    blocks = nb0;
+  }
+  const size_t need = (n + 255) / 256;
+  if ((size_t)blocks > need) blocks = (int)need;
+  if (blocks < 1) blocks = 1;
+  if (a.ps == 8)
+    k_patch_gn<8><<<blocks, 256, 0, st>>>(a, prep, counter);
+  else if (a.ps == 12)
+    k_patch_gn<12><<<blocks, 256, 0, st>>>(a, prep, counter);
+  else
+    k_patch_gn<0><<<blocks, 256, 0, st>>>(a, prep, counter);
+  note_launch();
+  prof_end(KC_SEARCH, st);
 }
 
 }  // namespace disb200

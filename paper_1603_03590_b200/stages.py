@@ -76,11 +76,14 @@ def patch_search(ref: dict, qry_img, params: DisParams, coarse_u=None, coarse_v=
     if coarse_u is not None:
         Hc, Wc = coarse_u.shape[-2:]
     cp = to_c(params)
+    nbytes = int(_lib.lib().dis_patch_search_workspace_bytes(B, W, H, ctypes.byref(cp)))
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
     rc = _lib.lib().dis_patch_search(
         ref["img"].data_ptr(), ref["gx"].data_ptr(), ref["gy"].data_ptr(), qry_img.data_ptr(),
         B, W, H, _lib.ptr(coarse_u), _lib.ptr(coarse_v), Wc, Hc, ctypes.byref(cp),
         out["u"].data_ptr(), out["v"].data_ptr(), out["off"].data_ptr(), out["mar"].data_ptr(),
-        out["init_u"].data_ptr(), out["init_v"].data_ptr(), out["valid"].data_ptr(), None)
+        out["init_u"].data_ptr(), out["init_v"].data_ptr(), out["valid"].data_ptr(),
+        ws.data_ptr(), nbytes, None)
     _lib.check(rc)
     out["x_origins"] = xo
     out["y_origins"] = yo
