@@ -185,7 +185,22 @@ struct Lane {
   bool stop;
 };
 
-// window evaluation at (bx, by); PS > 0: compile-time patch size
+// bilinear sample of a row pair at column c of a contiguous segment
+// (regular windows: column ox reads segment entries ox and ox+1)
+__device__ __forceinline__ double seg_sample(double i00, double i01, double i10, double i11,
+                                             double fx, double fy) {
+  const double a = i00 + fx * (i01 - i00);
+  const double bb = i10 + fx * (i11 - i10);
+  return a + fy * (bb - a);
+}
+
+// window evaluation at (bx, by); PS > 0: compile-time patch size.
+// Fast path ("regular" window: the ps sample columns are ps consecutive
+// pixels X0 .. X0+ps-1, each with its right neighbour unclamped): every row
+// pair is loaded once as a contiguous segment of ps+1 pixels with
+// immediate-offset loads.  Otherwise (window clamped at a border, or a
+// column fraction that rounds onto the next integer) each sample gathers its
+// own four pixels.  Both compute exactly bilin_nb's arithmetic.
 template <int PS>
 __device__ __forceinline__ void eval_window(const double* __restrict__ qry,
                                             const double* __restrict__ ref,
@@ -198,39 +213,43 @@ __device__ __forceinline__ void eval_window(const double* __restrict__ qry,
   constexpr int MAXC = PS > 0 ? PS : 1;
   const int ps = PS > 0 ? PS : ps_rt;
   const double dn = (double)(ps * ps);
-  int X0[MAXC], X1[MAXC];
   double FX[MAXC];
+  int xbase = 0;
+  bool regular = PS > 0;
   if (PS > 0) {
 #pragma unroll
     for (int ox = 0; ox < MAXC; ++ox) {
       const Axis1 ax = axis_sample(bx + ox, W);
-      X0[ox] = ax.i0;
-      X1[ox] = ax.i1;
+      if (ox == 0) xbase = ax.i0;
+      regular = regular && ax.i0 == xbase + ox && ax.i1 == ax.i0 + 1;
       FX[ox] = ax.f;
     }
   }
   double wsum = 0.0;
-  for (int oy = 0; oy < ps; ++oy) {
-    const Axis1 ay = axis_sample(by + oy, H);
-    const double* r0 = qry + (size_t)ay.i0 * W;
-    const double* r1 = qry + (size_t)ay.i1 * W;
-    if (PS > 0) {
+  if (regular) {
+    for (int oy = 0; oy < ps; ++oy) {
+      const Axis1 ay = axis_sample(by + oy, H);
+      const double* r0 = qry + (size_t)ay.i0 * W + xbase;
+      const double* r1 = qry + (size_t)ay.i1 * W + xbase;
+      double s0[MAXC + 1], s1[MAXC + 1];
 #pragma unroll
-      for (int ox = 0; ox < MAXC; ++ox) {
-        const double i00 = __ldg(r0 + X0[ox]), i01 = __ldg(r0 + X1[ox]);
-        const double i10 = __ldg(r1 + X0[ox]), i11 = __ldg(r1 + X1[ox]);
-        const double a = i00 + FX[ox] * (i01 - i00);
-        const double bb = i10 + FX[ox] * (i11 - i10);
-        wsum += a + ay.f * (bb - a);
+      for (int c = 0; c <= MAXC; ++c) {
+        s0[c] = __ldg(r0 + c);
+        s1[c] = __ldg(r1 + c);
       }
-    } else {
+#pragma unroll
+      for (int ox = 0; ox < MAXC; ++ox)
+        wsum += seg_sample(s0[ox], s0[ox + 1], s1[ox], s1[ox + 1], FX[ox], ay.f);
+    }
+  } else {
+    for (int oy = 0; oy < ps; ++oy) {
+      const Axis1 ay = axis_sample(by + oy, H);
+      const double* r0 = qry + (size_t)ay.i0 * W;
+      const double* r1 = qry + (size_t)ay.i1 * W;
       for (int ox = 0; ox < ps; ++ox) {
         const Axis1 ax = axis_sample(bx + ox, W);
-        const double i00 = __ldg(r0 + ax.i0), i01 = __ldg(r0 + ax.i1);
-        const double i10 = __ldg(r1 + ax.i0), i11 = __ldg(r1 + ax.i1);
-        const double a = i00 + ax.f * (i01 - i00);
-        const double bb = i10 + ax.f * (i11 - i10);
-        wsum += a + ay.f * (bb - a);
+        wsum += seg_sample(__ldg(r0 + ax.i0), __ldg(r0 + ax.i1), __ldg(r1 + ax.i0),
+                           __ldg(r1 + ax.i1), ax.f, ay.f);
       }
     }
   }
@@ -239,41 +258,45 @@ __device__ __forceinline__ void eval_window(const double* __restrict__ qry,
   b0 = 0.0;
   b1 = 0.0;
   mar = 0.0;
-  for (int oy = 0; oy < ps; ++oy) {
-    const Axis1 ay = axis_sample(by + oy, H);
-    const double* r0 = qry + (size_t)ay.i0 * W;
-    const double* r1 = qry + (size_t)ay.i1 * W;
-    const size_t row = (size_t)(y0i + oy) * W + x0i;
-    const double* tr = ref + row;
-    const double* gxr = rgx + row;
-    const double* gyr = rgy + row;
+  auto accumulate = [&](double val, double t, double gxv, double gyv) {
+    const double e = val - off - t;
+    mar += fabs(e);
+    const double et = transform_residual(e, code, hb);
+    ssd += et * et;
+    b0 += gxv * et;
+    b1 += gyv * et;
+  };
+  if (regular) {
+    for (int oy = 0; oy < ps; ++oy) {
+      const Axis1 ay = axis_sample(by + oy, H);
+      const double* r0 = qry + (size_t)ay.i0 * W + xbase;
+      const double* r1 = qry + (size_t)ay.i1 * W + xbase;
+      const size_t row = (size_t)(y0i + oy) * W + x0i;
+      const double* tr = ref + row;
+      const double* gxr = rgx + row;
+      const double* gyr = rgy + row;
+      double s0[MAXC + 1], s1[MAXC + 1];
 #pragma unroll
-    for (int ox = 0; ox < (PS > 0 ? MAXC : 1); ++ox) {
-      for (int oxr = 0; oxr < (PS > 0 ? 1 : ps); ++oxr) {
-        const int c = PS > 0 ? ox : oxr;
-        int xi0, xi1;
-        double fx;
-        if (PS > 0) {
-          xi0 = X0[ox];
-          xi1 = X1[ox];
-          fx = FX[ox];
-        } else {
-          const Axis1 ax = axis_sample(bx + oxr, W);
-          xi0 = ax.i0;
-          xi1 = ax.i1;
-          fx = ax.f;
-        }
-        const double i00 = __ldg(r0 + xi0), i01 = __ldg(r0 + xi1);
-        const double i10 = __ldg(r1 + xi0), i11 = __ldg(r1 + xi1);
-        const double a = i00 + fx * (i01 - i00);
-        const double bb = i10 + fx * (i11 - i10);
-        const double val = a + ay.f * (bb - a);
-        const double e = val - off - __ldg(tr + c);
-        mar += fabs(e);
-        const double et = transform_residual(e, code, hb);
-        ssd += et * et;
-        b0 += __ldg(gxr + c) * et;
-        b1 += __ldg(gyr + c) * et;
+      for (int c = 0; c <= MAXC; ++c) {
+        s0[c] = __ldg(r0 + c);
+        s1[c] = __ldg(r1 + c);
+      }
+#pragma unroll
+      for (int ox = 0; ox < MAXC; ++ox)
+        accumulate(seg_sample(s0[ox], s0[ox + 1], s1[ox], s1[ox + 1], FX[ox], ay.f),
+                   __ldg(tr + ox), __ldg(gxr + ox), __ldg(gyr + ox));
+    }
+  } else {
+    for (int oy = 0; oy < ps; ++oy) {
+      const Axis1 ay = axis_sample(by + oy, H);
+      const double* r0 = qry + (size_t)ay.i0 * W;
+      const double* r1 = qry + (size_t)ay.i1 * W;
+      const size_t row = (size_t)(y0i + oy) * W + x0i;
+      for (int ox = 0; ox < ps; ++ox) {
+        const Axis1 ax = axis_sample(bx + ox, W);
+        accumulate(seg_sample(__ldg(r0 + ax.i0), __ldg(r0 + ax.i1), __ldg(r1 + ax.i0),
+                              __ldg(r1 + ax.i1), ax.f, ay.f),
+                   __ldg(ref + row + ox), __ldg(rgx + row + ox), __ldg(rgy + row + ox));
       }
     }
   }
@@ -281,7 +304,7 @@ __device__ __forceinline__ void eval_window(const double* __restrict__ qry,
 }
 
 template <int PS>
-__global__ void __launch_bounds__(256) k_patch_gn(SearchArgs a, const double* __restrict__ prep,
+__global__ void __launch_bounds__(256, 2) k_patch_gn(SearchArgs a, const double* __restrict__ prep,
                                                    unsigned* counter) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
