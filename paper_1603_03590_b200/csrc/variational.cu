@@ -246,10 +246,13 @@ __global__ void __launch_bounds__(S * kMaxBandRows, 1)
     }
   };
 
-  {  // exchange buffers start at zero (they feed inactive threads)
-    const int nx = (2 + 3) * S * rows * 2;
-    for (int i = threadIdx.x; i < nx; i += blockDim.x) xuv[i] = 0.0;
+  {  // the ring and the exchange buffers start at zero: inactive threads read
+     // slots whose diagonal is not loaded yet, and their garbage must stay
+     // finite (it is multiplied by an exact zero weight at the row starts)
+    const int nx = R * slot_elems + (2 + 3) * S * rows * 2;
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) ring[i] = 0.0;
   }
+  __syncthreads();
   // prefetch state for diagonal jn = k + kLookahead (own row, and the halo
   // rows for the first / last thread of the band)
   int jn = 0;
