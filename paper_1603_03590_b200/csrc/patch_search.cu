@@ -423,6 +423,236 @@ __global__ void __launch_bounds__(256, 2) k_patch_gn(SearchArgs a, const double*
   }
 }
 
+// ---------------------------------------------------------------------------
+// Stage 2, coarse levels — the same Gauss-Newton loop with a GROUP of G lanes
+// per patch (lane r owns window row r).  Small levels have too few patches to
+// fill the GPU, so a lane-per-patch kernel is bound by one lane's serial
+// latency (two passes x ps rows of loads and sums).  Here the rows' loads and
+// bilinear samples run in parallel; the reference's row-major sums stay
+// exactly sequential: row r's lane adds its ps values to the running sums it
+// receives from row r-1's lane (warp shuffle), so every sum is formed in the
+// same order as the reference's loop.  All lanes of a group hold the same
+// patch state and apply the same update.
+// ---------------------------------------------------------------------------
+template <int PS, int G>
+__global__ void __launch_bounds__(128) k_patch_gn_group(SearchArgs a,
+                                                         const double* __restrict__ prep,
+                                                         unsigned* counter) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int r = lane & (G - 1);  // my window row
+  const int gbase = lane - r;
+  const int nx = a.ax.n;
+  const int P = nx * a.ay.n;
+  const unsigned N = (unsigned)(a.B * P);
+  const int W = a.W, H = a.H;
+  const size_t plane = (size_t)W * H;
+  const bool mean_norm = a.mean_norm != 0;
+  const double dn = (double)(PS * PS);
+  Lane L;
+  L.pid = -1;
+  L.b = L.x0i = L.y0i = 0;  // an idle group evaluates a harmless in-bounds window
+  L.u = L.v = 0.0;
+  bool done = false;
+  for (;;) {
+    // ---- fetch (one patch per group; the group's lane 0 asks) ----
+    const bool need = !done && L.pid < 0;
+    const unsigned mask = __ballot_sync(FULL, need && r == 0);
+    if (mask) {
+      const int leader = __ffs(mask) - 1;
+      unsigned base = 0;
+      if (lane == leader) base = atomicAdd(counter, (unsigned)__popc(mask));
+      base = __shfl_sync(FULL, base, leader);
+      const unsigned g = base + (unsigned)__popc(mask & ((1u << gbase) - 1u));
+      if (need) {
+        if (g >= N) {
+          done = true;
+        } else {
+          L.pid = (int)g;
+          L.b = (int)(g / (unsigned)P);
+          const int i = (int)(g - (unsigned)L.b * (unsigned)P);
+          const int iy = i / nx;
+          L.x0i = a.ax.origin(i - iy * nx);
+          L.y0i = a.ay.origin(iy);
+          L.u0 = prep[PR_U0 * (size_t)N + g];
+          L.v0 = prep[PR_V0 * (size_t)N + g];
+          L.mean_t = prep[PR_MEAN * (size_t)N + g];
+          L.i00 = prep[PR_I00 * (size_t)N + g];
+          L.i01 = prep[PR_I01 * (size_t)N + g];
+          L.i11 = prep[PR_I11 * (size_t)N + g];
+          L.stop = !(prep[PR_VALID * (size_t)N + g] != 0.0);
+          L.u = L.u0;
+          L.v = L.v0;
+          L.prev_ssd = 1e300;
+          L.prev_u = L.u;
+          L.prev_v = L.v;
+          L.prev_off = 0.0;
+          L.prev_mar = 0.0;
+          L.k = 0;
+          L.evals = 0;
+        }
+      }
+    }
+    if (__all_sync(FULL, done)) break;
+    const bool live = !done;  // whole group agrees
+
+    // ---- window evaluation: my row's samples ----
+    const double x0 = (double)L.x0i, y0 = (double)L.y0i;
+    const size_t po = (size_t)(live ? L.b : 0) * plane;
+    const double* __restrict__ qry = a.qry + po;
+    const double bx = x0 + L.u, by = y0 + L.v;
+    double FX[PS];
+    int xbase = 0;
+    bool regx = true;
+#pragma unroll
+    for (int o = 0; o < PS; ++o) {
+      const Axis1 ax = axis_sample(bx + o, W);
+      if (o == 0) xbase = ax.i0;
+      regx = regx && ax.i0 == xbase + o && ax.i1 == ax.i0 + 1;
+      FX[o] = ax.f;
+    }
+    const int rr_row = r < PS ? r : PS - 1;
+    const Axis1 ay = axis_sample(by + rr_row, H);
+    double val[PS];
+    if (regx) {
+      const double* r0 = qry + (size_t)ay.i0 * W + xbase;
+      const double* r1 = qry + (size_t)ay.i1 * W + xbase;
+      double s0[PS + 1], s1[PS + 1];
+#pragma unroll
+      for (int c = 0; c <= PS; ++c) {
+        s0[c] = __ldg(r0 + c);
+        s1[c] = __ldg(r1 + c);
+      }
+#pragma unroll
+      for (int c = 0; c < PS; ++c) val[c] = seg_sample(s0[c], s0[c + 1], s1[c], s1[c + 1], FX[c], ay.f);
+    } else {
+      const double* r0 = qry + (size_t)ay.i0 * W;
+      const double* r1 = qry + (size_t)ay.i1 * W;
+#pragma unroll
+      for (int c = 0; c < PS; ++c) {
+        const Axis1 ax = axis_sample(bx + c, W);
+        val[c] = seg_sample(__ldg(r0 + ax.i0), __ldg(r0 + ax.i1), __ldg(r1 + ax.i0),
+                            __ldg(r1 + ax.i1), ax.f, ay.f);
+      }
+    }
+    // pass 1: wsum over rows in order (row rr's lane continues the chain)
+    double wsum = 0.0;
+#pragma unroll
+    for (int rr = 0; rr < PS; ++rr) {
+      double acc = wsum;
+#pragma unroll
+      for (int c = 0; c < PS; ++c) acc += val[c];
+      wsum = __shfl_sync(FULL, acc, gbase + rr);
+    }
+    double off = mean_norm ? exact_div_pos(wsum, dn) - L.mean_t : 0.0;
+    // pass 2: the addends of my row, then the four sums in row order
+    const size_t row = po + (size_t)(L.y0i + rr_row) * W + L.x0i;
+    double EA[PS], E2[PS], EX[PS], EY[PS];
+#pragma unroll
+    for (int c = 0; c < PS; ++c) {
+      const double e = val[c] - off - __ldg(a.ref + row + c);
+      EA[c] = fabs(e);
+      const double et = transform_residual(e, a.code, a.hb);
+      E2[c] = et * et;
+      EX[c] = __ldg(a.rgx + row + c) * et;
+      EY[c] = __ldg(a.rgy + row + c) * et;
+    }
+    double mar = 0.0, ssd = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+    for (int rr = 0; rr < PS; ++rr) {
+      double am = mar, as = ssd, a0 = b0, a1 = b1;
+#pragma unroll
+      for (int c = 0; c < PS; ++c) {
+        am += EA[c];
+        as += E2[c];
+        a0 += EX[c];
+        a1 += EY[c];
+      }
+      mar = __shfl_sync(FULL, am, gbase + rr);
+      ssd = __shfl_sync(FULL, as, gbase + rr);
+      b0 = __shfl_sync(FULL, a0, gbase + rr);
+      b1 = __shfl_sync(FULL, a1, gbase + rr);
+    }
+    mar = exact_div_pos(mar, dn);
+    if (!live) continue;
+
+    // ---- Gauss-Newton update (replicated in the group) ----
+    if (L.evals == 0) {
+      L.off0 = off;
+      L.mar0 = mar;
+    }
+    ++L.evals;
+    bool finished = false;
+    double u = L.u, v = L.v;
+    if (ssd > L.prev_ssd) {
+      u = L.prev_u;
+      v = L.prev_v;
+      off = L.prev_off;
+      mar = L.prev_mar;
+      finished = true;
+    } else if (L.stop || L.k >= a.iters) {
+      finished = true;
+    } else {
+      L.prev_ssd = ssd;
+      L.prev_u = u;
+      L.prev_v = v;
+      L.prev_off = off;
+      L.prev_mar = mar;
+      const double du = L.i00 * b0 + L.i01 * b1;
+      const double dv = L.i01 * b0 + L.i11 * b1;
+      u -= du;
+      v -= dv;
+      L.k += 1;
+      if (sqrt(du * du + dv * dv) < 1e-2) L.stop = true;
+      const double cx = x0 + u + 0.5 * PS;
+      const double cy = y0 + v + 0.5 * PS;
+      if (cx < (double)(-W) || cx > 2.0 * W || cy < (double)(-H) || cy > 2.0 * H) {
+        u = L.u0;
+        v = L.v0;
+        L.prev_ssd = 1e300;
+        L.stop = true;
+      }
+      L.u = u;
+      L.v = v;
+    }
+    if (finished) {
+      if (hypot_gt(u - L.u0, v - L.v0, PS)) {
+        u = L.u0;
+        v = L.v0;
+        off = mean_norm ? L.off0 : 0.0;
+        mar = L.mar0;
+      }
+      if (r == 0) {
+        const size_t o = (size_t)L.pid;
+        a.out_u[o] = u;
+        a.out_v[o] = v;
+        a.out_off[o] = off;
+        if (a.out_mar) a.out_mar[o] = mar;
+        if (a.out_evals) a.out_evals[o] = L.evals;
+      }
+      L.pid = -1;
+    }
+  }
+}
+
+template <int PS, int G>
+static void launch_gn_group(const SearchArgs& a, const double* prep, unsigned* counter,
+                            size_t n, cudaStream_t st) {
+  static int cap = 0;
+  if (!cap) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_patch_gn_group<PS, G>, 128, 0);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cap = (per_sm > 0 ? per_sm : 1) * sms;
+  }
+  const size_t need = (n * G + 127) / 128;
+  int blocks = (int)(need < (size_t)cap ? need : (size_t)cap);
+  if (blocks < 1) blocks = 1;
+  k_patch_gn_group<PS, G><<<blocks, 128, 0, st>>>(a, prep, counter);
+}
+
 static int gn_blocks(const void* fn) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
@@ -431,6 +661,8 @@ static int gn_blocks(const void* fn) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   return (per_sm > 0 ? per_sm : 1) * sms;
 }
+
+constexpr size_t kGroupLanes = 148 * 2048;  // lanes a fully occupied B200 holds
 
 size_t patch_search_scratch_bytes(int B, int P) {
   return ((size_t)kPrep * B * P) * sizeof(double) + 256;
@@ -445,27 +677,37 @@ void launch_patch_search(const SearchArgs& a, void* scratch, cudaStream_t st) {
   const int TH = 128;
   k_patch_prep<<<(unsigned)((n + TH - 1) / TH), TH, 0, st>>>(a, prep, counter);
   note_launch();
-  int blocks;
-  static int nb8 = 0, nb12 = 0, nb0 = 0;
-  if (a.ps == 8) {
-    if (!nb8) nb8 = gn_blocks((const void*)k_patch_gn<8>);
-    blocks = nb8;
-  } else if (a.ps == 12) {
-    if (!nb12) nb12 = gn_blocks((const void*)k_patch_gn<12>);
-    blocks = nb12;
+  // coarse levels (few patches): a group of lanes per patch; fine levels: a
+  // lane per patch
+  const bool group = (a.ps == 8 && n * 8 <= kGroupLanes) || (a.ps == 12 && n * 16 <= kGroupLanes);
+  if (group) {
+    if (a.ps == 8)
+      launch_gn_group<8, 8>(a, prep, counter, n, st);
+    else
+      launch_gn_group<12, 16>(a, prep, counter, n, st);
   } else {
-    if (!nb0) nb0 = gn_blocks((const void*)k_patch_gn<0>);
-    blocks = nb0;
+    int blocks;
+    static int nb8 = 0, nb12 = 0, nb0 = 0;
+    if (a.ps == 8) {
+      if (!nb8) nb8 = gn_blocks((const void*)k_patch_gn<8>);
+      blocks = nb8;
+    } else if (a.ps == 12) {
+      if (!nb12) nb12 = gn_blocks((const void*)k_patch_gn<12>);
+      blocks = nb12;
+    } else {
+      if (!nb0) nb0 = gn_blocks((const void*)k_patch_gn<0>);
+      blocks = nb0;
+    }
+    const size_t need = (n + 255) / 256;
+    if ((size_t)blocks > need) blocks = (int)need;
+    if (blocks < 1) blocks = 1;
+    if (a.ps == 8)
+      k_patch_gn<8><<<blocks, 256, 0, st>>>(a, prep, counter);
+    else if (a.ps == 12)
+      k_patch_gn<12><<<blocks, 256, 0, st>>>(a, prep, counter);
+    else
+      k_patch_gn<0><<<blocks, 256, 0, st>>>(a, prep, counter);
   }
-  const size_t need = (n + 255) / 256;
-  if ((size_t)blocks > need) blocks = (int)need;
-  if (blocks < 1) blocks = 1;
-  if (a.ps == 8)
-    k_patch_gn<8><<<blocks, 256, 0, st>>>(a, prep, counter);
-  else if (a.ps == 12)
-    k_patch_gn<12><<<blocks, 256, 0, st>>>(a, prep, counter);
-  else
-    k_patch_gn<0><<<blocks, 256, 0, st>>>(a, prep, counter);
   note_launch();
   prof_end(KC_SEARCH, st);
 }
