@@ -25,6 +25,7 @@
 // u_init — so the kernel keeps the first evaluation's (offset, residual)
 // instead of a second pass (bit-identical).
 #include <cfloat>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -78,7 +79,11 @@ __global__ void __launch_bounds__(128) k_patch_prep(SearchArgs a, double* __rest
   const int P = nx * a.ay.n;
   const size_t N = (size_t)a.B * P;
   const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid == 0) *counter = 0u;
+  if (gid == 0) {
+    counter[0] = 0u;  // work queue
+    counter[1] = 0u;  // parked patches
+    counter[2] = 0u;  // parked-patch queue
+  }
   if (gid >= N) return;
   const int b = (int)(gid / P);
   const int i = (int)(gid - (size_t)b * P);
@@ -176,6 +181,9 @@ __device__ __forceinline__ Axis1 axis_sample(double c, int n) {
   return a;
 }
 
+constexpr unsigned kPool = 64;   // patches per warp-pool refill
+constexpr int kSpillStride = 16;  // doubles per parked patch state
+
 struct Lane {
   int pid;  // patch (b * P + i) or -1
   int b, x0i, y0i;
@@ -185,8 +193,134 @@ struct Lane {
   bool stop;
 };
 
-// bilinear sample of a row pair at column c of a contiguous segment
-// (regular windows: column ox reads segment entries ox and ox+1)
+__device__ __forceinline__ void lane_start(Lane& L, const SearchArgs& a,
+                                           const double* __restrict__ prep, unsigned N, int P,
+                                           int nx, unsigned g) {
+  L.pid = (int)g;
+  L.b = (int)(g / (unsigned)P);
+  const int i = (int)(g - (unsigned)L.b * (unsigned)P);
+  const int iy = i / nx;
+  L.x0i = a.ax.origin(i - iy * nx);
+  L.y0i = a.ay.origin(iy);
+  L.u0 = prep[PR_U0 * (size_t)N + g];
+  L.v0 = prep[PR_V0 * (size_t)N + g];
+  L.mean_t = prep[PR_MEAN * (size_t)N + g];
+  L.i00 = prep[PR_I00 * (size_t)N + g];
+  L.i01 = prep[PR_I01 * (size_t)N + g];
+  L.i11 = prep[PR_I11 * (size_t)N + g];
+  L.stop = !(prep[PR_VALID * (size_t)N + g] != 0.0);
+  L.u = L.u0;
+  L.v = L.v0;
+  L.prev_ssd = 1e300;
+  L.prev_u = L.u;
+  L.prev_v = L.v;
+  L.prev_off = 0.0;
+  L.prev_mar = 0.0;
+  L.k = 0;
+  L.evals = 0;
+}
+
+// park / resume the dynamic part of a lane's state (prep fields are reloaded)
+__device__ __forceinline__ void lane_park(const Lane& L, double* e) {
+  e[0] = (double)L.pid;
+  e[1] = L.u;
+  e[2] = L.v;
+  e[3] = L.prev_ssd;
+  e[4] = L.prev_u;
+  e[5] = L.prev_v;
+  e[6] = L.prev_off;
+  e[7] = L.prev_mar;
+  e[8] = L.off0;
+  e[9] = L.mar0;
+  e[10] = (double)L.k;
+  e[11] = (double)L.evals;
+  e[12] = L.stop ? 1.0 : 0.0;
+}
+__device__ __forceinline__ void lane_resume(Lane& L, const SearchArgs& a,
+                                            const double* __restrict__ prep, unsigned N, int P,
+                                            int nx, const double* e) {
+  lane_start(L, a, prep, N, P, nx, (unsigned)e[0]);
+  L.u = e[1];
+  L.v = e[2];
+  L.prev_ssd = e[3];
+  L.prev_u = e[4];
+  L.prev_v = e[5];
+  L.prev_off = e[6];
+  L.prev_mar = e[7];
+  L.off0 = e[8];
+  L.mar0 = e[9];
+  L.k = (int)e[10];
+  L.evals = (int)e[11];
+  L.stop = e[12] != 0.0;
+}
+
+// Gauss-Newton bookkeeping after one window evaluation
+// (inverse_search.py:153-188) + reset_outliers / refresh on exit.  Returns
+// true (and writes the patch's outputs) when the patch is finished.
+__device__ __forceinline__ bool gn_update(Lane& L, const SearchArgs& a, int ps, double off,
+                                          double ssd, double b0, double b1, double mar,
+                                          bool writer = true) {
+  const double x0 = (double)L.x0i, y0 = (double)L.y0i;
+  const int W = a.W, H = a.H;
+  if (L.evals == 0) {
+    L.off0 = off;
+    L.mar0 = mar;
+  }
+  ++L.evals;
+  bool finished = false;
+  double u = L.u, v = L.v;
+  if (ssd > L.prev_ssd) {
+    u = L.prev_u;
+    v = L.prev_v;
+    off = L.prev_off;
+    mar = L.prev_mar;
+    finished = true;
+  } else if (L.stop || L.k >= a.iters) {
+    finished = true;
+  } else {
+    L.prev_ssd = ssd;
+    L.prev_u = u;
+    L.prev_v = v;
+    L.prev_off = off;
+    L.prev_mar = mar;
+    const double du = L.i00 * b0 + L.i01 * b1;
+    const double dv = L.i01 * b0 + L.i11 * b1;
+    u -= du;
+    v -= dv;
+    L.k += 1;
+    if (sqrt(du * du + dv * dv) < 1e-2) L.stop = true;
+    const double cx = x0 + u + 0.5 * ps;
+    const double cy = y0 + v + 0.5 * ps;
+    if (cx < (double)(-W) || cx > 2.0 * W || cy < (double)(-H) || cy > 2.0 * H) {
+      u = L.u0;
+      v = L.v0;
+      L.prev_ssd = 1e300;
+      L.stop = true;
+    }
+    L.u = u;
+    L.v = v;
+  }
+  if (finished) {
+    if (hypot_gt(u - L.u0, v - L.v0, ps)) {
+      u = L.u0;
+      v = L.v0;
+      off = a.mean_norm ? L.off0 : 0.0;
+      mar = L.mar0;
+    }
+    if (writer) {
+      const size_t o = (size_t)L.pid;
+      a.out_u[o] = u;
+      a.out_v[o] = v;
+      a.out_off[o] = off;
+      if (a.out_mar) a.out_mar[o] = mar;
+      if (a.out_evals) a.out_evals[o] = L.evals;
+    }
+    L.pid = -1;
+  }
+  return finished;
+}
+
+// bilinear sample from four pixels, the reference's _bilin arithmetic
 __device__ __forceinline__ double seg_sample(double i00, double i01, double i10, double i11,
                                              double fx, double fy) {
   const double a = i00 + fx * (i01 - i00);
@@ -194,63 +328,60 @@ __device__ __forceinline__ double seg_sample(double i00, double i01, double i10,
   return a + fy * (bb - a);
 }
 
-// window evaluation at (bx, by); PS > 0: compile-time patch size.
-// Fast path ("regular" window: the ps sample columns are ps consecutive
-// pixels X0 .. X0+ps-1, each with its right neighbour unclamped): every row
-// pair is loaded once as a contiguous segment of ps+1 pixels with
-// immediate-offset loads.  Otherwise (window clamped at a border, or a
-// column fraction that rounds onto the next integer) each sample gathers its
-// own four pixels.  Both compute exactly bilin_nb's arithmetic.
+// Is the window at (bx, by) "regular": its ps sample columns (rows) are the ps
+// consecutive pixels xbase.. (ybase..), each with its right (lower)
+// neighbour unclamped?  Then each sample's bilinear operands are segment
+// entries c, c+1 of the rows ybase.. ybase+ps.  (Not regular: the window is
+// clamped at a border, or a coordinate rounds onto the next integer.)
 template <int PS>
-__device__ __forceinline__ void eval_window(const double* __restrict__ qry,
-                                            const double* __restrict__ ref,
-                                            const double* __restrict__ rgx,
-                                            const double* __restrict__ rgy, int W, int H,
-                                            int ps_rt, int x0i, int y0i, double bx, double by,
-                                            double mean_t, bool mean_norm, int code, double hb,
-                                            double& off, double& ssd, double& b0, double& b1,
-                                            double& mar) {
-  constexpr int MAXC = PS > 0 ? PS : 1;
-  const int ps = PS > 0 ? PS : ps_rt;
-  const double dn = (double)(ps * ps);
-  double FX[MAXC];
-  int xbase = 0;
-  bool regular = PS > 0;
-  if (PS > 0) {
+__device__ __forceinline__ bool window_regular(double bx, double by, int W, int H, double* FX,
+                                               int& xbase, int& ybase) {
+  bool regular = true;
 #pragma unroll
-    for (int ox = 0; ox < MAXC; ++ox) {
-      const Axis1 ax = axis_sample(bx + ox, W);
-      if (ox == 0) xbase = ax.i0;
-      regular = regular && ax.i0 == xbase + ox && ax.i1 == ax.i0 + 1;
-      FX[ox] = ax.f;
+  for (int o = 0; o < PS; ++o) {
+    const Axis1 ax = axis_sample(bx + o, W);
+    const Axis1 ay = axis_sample(by + o, H);
+    if (o == 0) {
+      xbase = ax.i0;
+      ybase = ay.i0;
     }
+    regular = regular && ax.i0 == xbase + o && ax.i1 == ax.i0 + 1 && ay.i0 == ybase + o &&
+              ay.i1 == ay.i0 + 1;
+    FX[o] = ax.f;
   }
+  return regular;
+}
+
+// One window evaluation (the reference's two passes, inverse_search.py:
+// 130-152) for a regular window: rows loaded once each as contiguous
+// segments with immediate-offset loads and carried to the next row pair.
+template <int PS>
+__device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
+                                             const double* __restrict__ ref,
+                                             const double* __restrict__ rgx,
+                                             const double* __restrict__ rgy, int W, int H,
+                                             int x0i, int y0i, double by, const double* FX,
+                                             int xbase, int ybase, double mean_t, bool mean_norm,
+                                             int code, double hb, bool tmpl128, double& off,
+                                             double& ssd, double& b0, double& b1, double& mar) {
+  constexpr int S1 = PS + 1;
+  const double dn = (double)(PS * PS);
   double wsum = 0.0;
-  if (regular) {
-    for (int oy = 0; oy < ps; ++oy) {
-      const Axis1 ay = axis_sample(by + oy, H);
-      const double* r0 = qry + (size_t)ay.i0 * W + xbase;
-      const double* r1 = qry + (size_t)ay.i1 * W + xbase;
-      double s0[MAXC + 1], s1[MAXC + 1];
+  {
+    const double* g = qry + (size_t)ybase * W + xbase;
+    double s0[S1], s1[S1];
 #pragma unroll
-      for (int c = 0; c <= MAXC; ++c) {
-        s0[c] = __ldg(r0 + c);
-        s1[c] = __ldg(r1 + c);
-      }
+    for (int c = 0; c < S1; ++c) s0[c] = __ldg(g + c);
+    for (int oy = 0; oy < PS; ++oy) {
+      const double fy = axis_sample(by + oy, H).f;
+      g += W;
 #pragma unroll
-      for (int ox = 0; ox < MAXC; ++ox)
-        wsum += seg_sample(s0[ox], s0[ox + 1], s1[ox], s1[ox + 1], FX[ox], ay.f);
-    }
-  } else {
-    for (int oy = 0; oy < ps; ++oy) {
-      const Axis1 ay = axis_sample(by + oy, H);
-      const double* r0 = qry + (size_t)ay.i0 * W;
-      const double* r1 = qry + (size_t)ay.i1 * W;
-      for (int ox = 0; ox < ps; ++ox) {
-        const Axis1 ax = axis_sample(bx + ox, W);
-        wsum += seg_sample(__ldg(r0 + ax.i0), __ldg(r0 + ax.i1), __ldg(r1 + ax.i0),
-                           __ldg(r1 + ax.i1), ax.f, ay.f);
-      }
+      for (int c = 0; c < S1; ++c) s1[c] = __ldg(g + c);
+#pragma unroll
+      for (int ox = 0; ox < PS; ++ox)
+        wsum += seg_sample(s0[ox], s0[ox + 1], s1[ox], s1[ox + 1], FX[ox], fy);
+#pragma unroll
+      for (int c = 0; c < S1; ++c) s0[c] = s1[c];
     }
   }
   off = mean_norm ? exact_div_pos(wsum, dn) - mean_t : 0.0;
@@ -266,159 +397,195 @@ __device__ __forceinline__ void eval_window(const double* __restrict__ qry,
     b0 += gxv * et;
     b1 += gyv * et;
   };
-  if (regular) {
-    for (int oy = 0; oy < ps; ++oy) {
-      const Axis1 ay = axis_sample(by + oy, H);
-      const double* r0 = qry + (size_t)ay.i0 * W + xbase;
-      const double* r1 = qry + (size_t)ay.i1 * W + xbase;
-      const size_t row = (size_t)(y0i + oy) * W + x0i;
-      const double* tr = ref + row;
-      const double* gxr = rgx + row;
-      const double* gyr = rgy + row;
-      double s0[MAXC + 1], s1[MAXC + 1];
+  {
+    const double* g = qry + (size_t)ybase * W + xbase;
+    double s0[S1], s1[S1];
 #pragma unroll
-      for (int c = 0; c <= MAXC; ++c) {
-        s0[c] = __ldg(r0 + c);
-        s1[c] = __ldg(r1 + c);
+    for (int c = 0; c < S1; ++c) s0[c] = __ldg(g + c);
+    const double* tr = ref + (size_t)y0i * W + x0i;
+    const double* gxr = rgx + (size_t)y0i * W + x0i;
+    const double* gyr = rgy + (size_t)y0i * W + x0i;
+    for (int oy = 0; oy < PS; ++oy) {
+      const double fy = axis_sample(by + oy, H).f;
+      g += W;
+#pragma unroll
+      for (int c = 0; c < S1; ++c) s1[c] = __ldg(g + c);
+      if (tmpl128) {
+#pragma unroll
+        for (int ox = 0; ox < PS; ox += 2) {
+          const double2 t = __ldg(reinterpret_cast<const double2*>(tr + ox));
+          const double2 gx = __ldg(reinterpret_cast<const double2*>(gxr + ox));
+          const double2 gy = __ldg(reinterpret_cast<const double2*>(gyr + ox));
+          accumulate(seg_sample(s0[ox], s0[ox + 1], s1[ox], s1[ox + 1], FX[ox], fy), t.x, gx.x,
+                     gy.x);
+          accumulate(seg_sample(s0[ox + 1], s0[ox + 2], s1[ox + 1], s1[ox + 2], FX[ox + 1], fy),
+                     t.y, gx.y, gy.y);
+        }
+      } else {
+#pragma unroll
+        for (int ox = 0; ox < PS; ++ox)
+          accumulate(seg_sample(s0[ox], s0[ox + 1], s1[ox], s1[ox + 1], FX[ox], fy),
+                     __ldg(tr + ox), __ldg(gxr + ox), __ldg(gyr + ox));
       }
 #pragma unroll
-      for (int ox = 0; ox < MAXC; ++ox)
-        accumulate(seg_sample(s0[ox], s0[ox + 1], s1[ox], s1[ox + 1], FX[ox], ay.f),
-                   __ldg(tr + ox), __ldg(gxr + ox), __ldg(gyr + ox));
-    }
-  } else {
-    for (int oy = 0; oy < ps; ++oy) {
-      const Axis1 ay = axis_sample(by + oy, H);
-      const double* r0 = qry + (size_t)ay.i0 * W;
-      const double* r1 = qry + (size_t)ay.i1 * W;
-      const size_t row = (size_t)(y0i + oy) * W + x0i;
-      for (int ox = 0; ox < ps; ++ox) {
-        const Axis1 ax = axis_sample(bx + ox, W);
-        accumulate(seg_sample(__ldg(r0 + ax.i0), __ldg(r0 + ax.i1), __ldg(r1 + ax.i0),
-                              __ldg(r1 + ax.i1), ax.f, ay.f),
-                   __ldg(ref + row + ox), __ldg(rgx + row + ox), __ldg(rgy + row + ox));
-      }
+      for (int c = 0; c < S1; ++c) s0[c] = s1[c];
+      tr += W;
+      gxr += W;
+      gyr += W;
     }
   }
   mar = exact_div_pos(mar, dn);
 }
 
+// One window evaluation for any window and patch size: every sample gathers
+// its own four pixels with the reference's clamping.
+__device__ __forceinline__ void eval_general(const double* __restrict__ qry,
+                                             const double* __restrict__ ref,
+                                             const double* __restrict__ rgx,
+                                             const double* __restrict__ rgy, int W, int H,
+                                             int ps, int x0i, int y0i, double bx, double by,
+                                             double mean_t, bool mean_norm, int code, double hb,
+                                             double& off, double& ssd, double& b0, double& b1,
+                                             double& mar) {
+  const double dn = (double)(ps * ps);
+  double wsum = 0.0;
+  for (int oy = 0; oy < ps; ++oy) {
+    const Axis1 ay = axis_sample(by + oy, H);
+    const double* r0 = qry + (size_t)ay.i0 * W;
+    const double* r1 = qry + (size_t)ay.i1 * W;
+    for (int ox = 0; ox < ps; ++ox) {
+      const Axis1 ax = axis_sample(bx + ox, W);
+      wsum += seg_sample(__ldg(r0 + ax.i0), __ldg(r0 + ax.i1), __ldg(r1 + ax.i0),
+                         __ldg(r1 + ax.i1), ax.f, ay.f);
+    }
+  }
+  off = mean_norm ? exact_div_pos(wsum, dn) - mean_t : 0.0;
+  ssd = 0.0;
+  b0 = 0.0;
+  b1 = 0.0;
+  mar = 0.0;
+  for (int oy = 0; oy < ps; ++oy) {
+    const Axis1 ay = axis_sample(by + oy, H);
+    const double* r0 = qry + (size_t)ay.i0 * W;
+    const double* r1 = qry + (size_t)ay.i1 * W;
+    const size_t row = (size_t)(y0i + oy) * W + x0i;
+    for (int ox = 0; ox < ps; ++ox) {
+      const Axis1 ax = axis_sample(bx + ox, W);
+      const double val = seg_sample(__ldg(r0 + ax.i0), __ldg(r0 + ax.i1), __ldg(r1 + ax.i0),
+                                    __ldg(r1 + ax.i1), ax.f, ay.f);
+      const double e = val - off - __ldg(ref + row + ox);
+      mar += fabs(e);
+      const double et = transform_residual(e, code, hb);
+      ssd += et * et;
+      b0 += __ldg(rgx + row + ox) * et;
+      b1 += __ldg(rgy + row + ox) * et;
+    }
+  }
+  mar = exact_div_pos(mar, dn);
+}
+
+// Fine levels: one lane per patch, regular windows only.  Lanes refill from
+// a warp pool of consecutive patches (one grid-row segment, so neighbouring
+// lanes read the same image rows and share L1 lines).  A patch whose next
+// window is not regular is parked (state to the spill list) and finished by
+// k_patch_gn_general — this keeps the warp on one code path.
 template <int PS>
-__global__ void __launch_bounds__(256, 2) k_patch_gn(SearchArgs a, const double* __restrict__ prep,
-                                                   unsigned* counter) {
+__global__ void __launch_bounds__(256, 2) k_patch_gn(SearchArgs a,
+                                                     const double* __restrict__ prep,
+                                                     unsigned* counter, double* spill,
+                                                     unsigned* spill_count) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int nx = a.ax.n;
   const int P = nx * a.ay.n;
   const unsigned N = (unsigned)(a.B * P);
-  const int W = a.W, H = a.H, ps = PS > 0 ? PS : a.ps;
+  const int W = a.W, H = a.H;
   const size_t plane = (size_t)W * H;
   const bool mean_norm = a.mean_norm != 0;
   Lane L;
   L.pid = -1;
   bool done = false;
+  unsigned pool_next = 0, pool_end = 0;  // warp-uniform
   for (;;) {
-    // ---- fetch: lanes without a patch take the next ones from the queue ----
     const bool need = !done && L.pid < 0;
-    const unsigned mask = __ballot_sync(FULL, need);
-    if (mask) {
-      const int leader = __ffs(mask) - 1;
-      unsigned base = 0;
-      if (lane == leader) base = atomicAdd(counter, (unsigned)__popc(mask));
-      base = __shfl_sync(FULL, base, leader);
-      if (need) {
-        const unsigned g = base + (unsigned)__popc(mask & ((1u << lane) - 1u));
-        if (g >= N) {
-          done = true;
-        } else {
-          L.pid = (int)g;
-          L.b = (int)(g / (unsigned)P);
-          const int i = (int)(g - (unsigned)L.b * (unsigned)P);
-          const int iy = i / nx;
-          L.x0i = a.ax.origin(i - iy * nx);
-          L.y0i = a.ay.origin(iy);
-          L.u0 = prep[PR_U0 * (size_t)N + g];
-          L.v0 = prep[PR_V0 * (size_t)N + g];
-          L.mean_t = prep[PR_MEAN * (size_t)N + g];
-          L.i00 = prep[PR_I00 * (size_t)N + g];
-          L.i01 = prep[PR_I01 * (size_t)N + g];
-          L.i11 = prep[PR_I11 * (size_t)N + g];
-          L.stop = !(prep[PR_VALID * (size_t)N + g] != 0.0);
-          L.u = L.u0;
-          L.v = L.v0;
-          L.prev_ssd = 1e300;
-          L.prev_u = L.u;
-          L.prev_v = L.v;
-          L.prev_off = 0.0;
-          L.prev_mar = 0.0;
-          L.k = 0;
-          L.evals = 0;
-        }
+    unsigned mask = __ballot_sync(FULL, need);
+    unsigned g = 0xffffffffu;
+    while (mask) {
+      if (pool_next >= pool_end) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(counter, kPool);
+        base = __shfl_sync(FULL, base, 0);
+        if (base >= N) break;
+        pool_next = base;
+        pool_end = base + kPool < N ? base + kPool : N;
       }
+      const unsigned avail = pool_end - pool_next;
+      const unsigned rank = (unsigned)__popc(mask & ((1u << lane) - 1u));
+      const bool mine = ((mask >> lane) & 1u) && rank < avail;
+      if (mine) g = pool_next + rank;
+      const unsigned took = __ballot_sync(FULL, mine);
+      pool_next += (unsigned)__popc(took);
+      mask &= ~took;
+    }
+    if (need) {
+      if (g == 0xffffffffu)
+        done = true;
+      else
+        lane_start(L, a, prep, N, P, nx, g);
     }
     if (__all_sync(FULL, done)) break;
     if (done) continue;
 
-    // ---- one window evaluation + Gauss-Newton update (inverse_search.py:124-188) ----
-    const double x0 = (double)L.x0i, y0 = (double)L.y0i;
+    const double bx = (double)L.x0i + L.u, by = (double)L.y0i + L.v;
+    double FX[PS];
+    int xbase, ybase;
+    if (!window_regular<PS>(bx, by, W, H, FX, xbase, ybase)) {
+      const unsigned slot = atomicAdd(spill_count, 1u);
+      lane_park(L, spill + (size_t)slot * kSpillStride);
+      L.pid = -1;
+      continue;
+    }
+    const bool tal = ((((size_t)L.y0i * W + L.x0i) | (size_t)W) & 1) == 0;
+    const bool tmpl128 = (PS & 1) == 0 && __all_sync(__activemask(), tal);
     const size_t po = (size_t)L.b * plane;
     double off, ssd, b0, b1, mar;
-    eval_window<PS>(a.qry + po, a.ref + po, a.rgx + po, a.rgy + po, W, H, ps, L.x0i, L.y0i,
-                    x0 + L.u, y0 + L.v, L.mean_t, mean_norm, a.code, a.hb, off, ssd, b0, b1,
-                    mar);
-    if (L.evals == 0) {
-      L.off0 = off;
-      L.mar0 = mar;
-    }
-    ++L.evals;
-    bool finished = false;
-    double u = L.u, v = L.v;
-    if (ssd > L.prev_ssd) {
-      u = L.prev_u;
-      v = L.prev_v;
-      off = L.prev_off;
-      mar = L.prev_mar;
-      finished = true;
-    } else if (L.stop || L.k >= a.iters) {
-      finished = true;
-    } else {
-      L.prev_ssd = ssd;
-      L.prev_u = u;
-      L.prev_v = v;
-      L.prev_off = off;
-      L.prev_mar = mar;
-      const double du = L.i00 * b0 + L.i01 * b1;
-      const double dv = L.i01 * b0 + L.i11 * b1;
-      u -= du;
-      v -= dv;
-      L.k += 1;
-      if (sqrt(du * du + dv * dv) < 1e-2) L.stop = true;
-      const double cx = x0 + u + 0.5 * ps;
-      const double cy = y0 + v + 0.5 * ps;
-      if (cx < (double)(-W) || cx > 2.0 * W || cy < (double)(-H) || cy > 2.0 * H) {
-        u = L.u0;
-        v = L.v0;
-        L.prev_ssd = 1e300;
-        L.stop = true;
-      }
-      L.u = u;
-      L.v = v;
-    }
-    if (finished) {
-      // ---- reset_outliers + refresh_patch_stats ----
-      if (hypot_gt(u - L.u0, v - L.v0, ps)) {
-        u = L.u0;
-        v = L.v0;
-        off = mean_norm ? L.off0 : 0.0;
-        mar = L.mar0;
-      }
-      const size_t o = (size_t)L.pid;
-      a.out_u[o] = u;
-      a.out_v[o] = v;
-      a.out_off[o] = off;
-      if (a.out_mar) a.out_mar[o] = mar;
-      if (a.out_evals) a.out_evals[o] = L.evals;
-      L.pid = -1;
+    eval_regular<PS>(a.qry + po, a.ref + po, a.rgx + po, a.rgy + po, W, H, L.x0i, L.y0i, by,
+                     FX, xbase, ybase, L.mean_t, mean_norm, a.code, a.hb, tmpl128, off, ssd, b0,
+                     b1, mar);
+    gn_update(L, a, PS, off, ssd, b0, b1, mar);
+  }
+}
+
+// Any patch size / parked patches: one lane per patch, general windows.
+// from_spill = true: resume the parked patches k_patch_gn left behind;
+// false: run every patch of the level from its start (patch sizes without a
+// specialised fast kernel).
+__global__ void __launch_bounds__(128) k_patch_gn_general(SearchArgs a,
+                                                          const double* __restrict__ prep,
+                                                          const double* __restrict__ spill,
+                                                          const unsigned* spill_count,
+                                                          bool from_spill) {
+  const int nx = a.ax.n;
+  const int P = nx * a.ay.n;
+  const unsigned N = (unsigned)(a.B * P);
+  const unsigned count = from_spill ? *spill_count : N;
+  const int W = a.W, H = a.H;
+  const size_t plane = (size_t)W * H;
+  const bool mean_norm = a.mean_norm != 0;
+  for (unsigned idx = blockIdx.x * blockDim.x + threadIdx.x; idx < count;
+       idx += gridDim.x * blockDim.x) {
+    Lane L;
+    if (from_spill)
+      lane_resume(L, a, prep, N, P, nx, spill + (size_t)idx * kSpillStride);
+    else
+      lane_start(L, a, prep, N, P, nx, idx);
+    const size_t po = (size_t)L.b * plane;
+    for (;;) {
+      double off, ssd, b0, b1, mar;
+      eval_general(a.qry + po, a.ref + po, a.rgx + po, a.rgy + po, W, H, a.ps, L.x0i, L.y0i,
+                   (double)L.x0i + L.u, (double)L.y0i + L.v, L.mean_t, mean_norm, a.code, a.hb,
+                   off, ssd, b0, b1, mar);
+      if (gn_update(L, a, a.ps, off, ssd, b0, b1, mar)) break;
     }
   }
 }
@@ -437,7 +604,10 @@ __global__ void __launch_bounds__(256, 2) k_patch_gn(SearchArgs a, const double*
 template <int PS, int G>
 __global__ void __launch_bounds__(128) k_patch_gn_group(SearchArgs a,
                                                          const double* __restrict__ prep,
-                                                         unsigned* counter) {
+                                                         unsigned* counter,
+                                                         const double* __restrict__ spill,
+                                                         const unsigned* spill_count,
+                                                         bool from_spill) {
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int r = lane & (G - 1);  // my window row
@@ -445,6 +615,8 @@ __global__ void __launch_bounds__(128) k_patch_gn_group(SearchArgs a,
   const int nx = a.ax.n;
   const int P = nx * a.ay.n;
   const unsigned N = (unsigned)(a.B * P);
+  const unsigned limit = from_spill ? *spill_count : N;
+  unsigned* queue = from_spill ? counter + 2 : counter;
   const int W = a.W, H = a.H;
   const size_t plane = (size_t)W * H;
   const bool mean_norm = a.mean_norm != 0;
@@ -461,46 +633,25 @@ __global__ void __launch_bounds__(128) k_patch_gn_group(SearchArgs a,
     if (mask) {
       const int leader = __ffs(mask) - 1;
       unsigned base = 0;
-      if (lane == leader) base = atomicAdd(counter, (unsigned)__popc(mask));
+      if (lane == leader) base = atomicAdd(queue, (unsigned)__popc(mask));
       base = __shfl_sync(FULL, base, leader);
       const unsigned g = base + (unsigned)__popc(mask & ((1u << gbase) - 1u));
       if (need) {
-        if (g >= N) {
+        if (g >= limit)
           done = true;
-        } else {
-          L.pid = (int)g;
-          L.b = (int)(g / (unsigned)P);
-          const int i = (int)(g - (unsigned)L.b * (unsigned)P);
-          const int iy = i / nx;
-          L.x0i = a.ax.origin(i - iy * nx);
-          L.y0i = a.ay.origin(iy);
-          L.u0 = prep[PR_U0 * (size_t)N + g];
-          L.v0 = prep[PR_V0 * (size_t)N + g];
-          L.mean_t = prep[PR_MEAN * (size_t)N + g];
-          L.i00 = prep[PR_I00 * (size_t)N + g];
-          L.i01 = prep[PR_I01 * (size_t)N + g];
-          L.i11 = prep[PR_I11 * (size_t)N + g];
-          L.stop = !(prep[PR_VALID * (size_t)N + g] != 0.0);
-          L.u = L.u0;
-          L.v = L.v0;
-          L.prev_ssd = 1e300;
-          L.prev_u = L.u;
-          L.prev_v = L.v;
-          L.prev_off = 0.0;
-          L.prev_mar = 0.0;
-          L.k = 0;
-          L.evals = 0;
-        }
+        else if (from_spill)
+          lane_resume(L, a, prep, N, P, nx, spill + (size_t)g * kSpillStride);
+        else
+          lane_start(L, a, prep, N, P, nx, g);
       }
     }
     if (__all_sync(FULL, done)) break;
     const bool live = !done;  // whole group agrees
 
     // ---- window evaluation: my row's samples ----
-    const double x0 = (double)L.x0i, y0 = (double)L.y0i;
     const size_t po = (size_t)(live ? L.b : 0) * plane;
     const double* __restrict__ qry = a.qry + po;
-    const double bx = x0 + L.u, by = y0 + L.v;
+    const double bx = (double)L.x0i + L.u, by = (double)L.y0i + L.v;
     double FX[PS];
     int xbase = 0;
     bool regx = true;
@@ -524,7 +675,8 @@ __global__ void __launch_bounds__(128) k_patch_gn_group(SearchArgs a,
         s1[c] = __ldg(r1 + c);
       }
 #pragma unroll
-      for (int c = 0; c < PS; ++c) val[c] = seg_sample(s0[c], s0[c + 1], s1[c], s1[c + 1], FX[c], ay.f);
+      for (int c = 0; c < PS; ++c)
+        val[c] = seg_sample(s0[c], s0[c + 1], s1[c], s1[c + 1], FX[c], ay.f);
     } else {
       const double* r0 = qry + (size_t)ay.i0 * W;
       const double* r1 = qry + (size_t)ay.i1 * W;
@@ -544,7 +696,7 @@ __global__ void __launch_bounds__(128) k_patch_gn_group(SearchArgs a,
       for (int c = 0; c < PS; ++c) acc += val[c];
       wsum = __shfl_sync(FULL, acc, gbase + rr);
     }
-    double off = mean_norm ? exact_div_pos(wsum, dn) - L.mean_t : 0.0;
+    const double off = mean_norm ? exact_div_pos(wsum, dn) - L.mean_t : 0.0;
     // pass 2: the addends of my row, then the four sums in row order
     const size_t row = po + (size_t)(L.y0i + rr_row) * W + L.x0i;
     double EA[PS], E2[PS], EX[PS], EY[PS];
@@ -575,69 +727,15 @@ __global__ void __launch_bounds__(128) k_patch_gn_group(SearchArgs a,
     }
     mar = exact_div_pos(mar, dn);
     if (!live) continue;
-
-    // ---- Gauss-Newton update (replicated in the group) ----
-    if (L.evals == 0) {
-      L.off0 = off;
-      L.mar0 = mar;
-    }
-    ++L.evals;
-    bool finished = false;
-    double u = L.u, v = L.v;
-    if (ssd > L.prev_ssd) {
-      u = L.prev_u;
-      v = L.prev_v;
-      off = L.prev_off;
-      mar = L.prev_mar;
-      finished = true;
-    } else if (L.stop || L.k >= a.iters) {
-      finished = true;
-    } else {
-      L.prev_ssd = ssd;
-      L.prev_u = u;
-      L.prev_v = v;
-      L.prev_off = off;
-      L.prev_mar = mar;
-      const double du = L.i00 * b0 + L.i01 * b1;
-      const double dv = L.i01 * b0 + L.i11 * b1;
-      u -= du;
-      v -= dv;
-      L.k += 1;
-      if (sqrt(du * du + dv * dv) < 1e-2) L.stop = true;
-      const double cx = x0 + u + 0.5 * PS;
-      const double cy = y0 + v + 0.5 * PS;
-      if (cx < (double)(-W) || cx > 2.0 * W || cy < (double)(-H) || cy > 2.0 * H) {
-        u = L.u0;
-        v = L.v0;
-        L.prev_ssd = 1e300;
-        L.stop = true;
-      }
-      L.u = u;
-      L.v = v;
-    }
-    if (finished) {
-      if (hypot_gt(u - L.u0, v - L.v0, PS)) {
-        u = L.u0;
-        v = L.v0;
-        off = mean_norm ? L.off0 : 0.0;
-        mar = L.mar0;
-      }
-      if (r == 0) {
-        const size_t o = (size_t)L.pid;
-        a.out_u[o] = u;
-        a.out_v[o] = v;
-        a.out_off[o] = off;
-        if (a.out_mar) a.out_mar[o] = mar;
-        if (a.out_evals) a.out_evals[o] = L.evals;
-      }
-      L.pid = -1;
-    }
+    // ---- Gauss-Newton update (replicated in the group; lane 0 writes) ----
+    gn_update(L, a, PS, off, ssd, b0, b1, mar, r == 0);
   }
 }
 
 template <int PS, int G>
 static void launch_gn_group(const SearchArgs& a, const double* prep, unsigned* counter,
-                            size_t n, cudaStream_t st) {
+                            size_t n, cudaStream_t st, const double* spill = nullptr,
+                            const unsigned* spill_count = nullptr, bool from_spill = false) {
   static int cap = 0;
   if (!cap) {
     int per_sm = 0;
@@ -650,65 +748,79 @@ static void launch_gn_group(const SearchArgs& a, const double* prep, unsigned* c
   const size_t need = (n * G + 127) / 128;
   int blocks = (int)(need < (size_t)cap ? need : (size_t)cap);
   if (blocks < 1) blocks = 1;
-  k_patch_gn_group<PS, G><<<blocks, 128, 0, st>>>(a, prep, counter);
+  k_patch_gn_group<PS, G><<<blocks, 128, 0, st>>>(a, prep, counter, spill, spill_count,
+                                                   from_spill);
 }
 
-static int gn_blocks(const void* fn) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, 0);
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return (per_sm > 0 ? per_sm : 1) * sms;
+static int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
 }
 
-constexpr size_t kGroupLanes = 148 * 2048;  // lanes a fully occupied B200 holds
+constexpr size_t kGroupLanes = (size_t)148 * 2048 * 4;  // group kernel up to ~4 waves
 
 size_t patch_search_scratch_bytes(int B, int P) {
-  return ((size_t)kPrep * B * P) * sizeof(double) + 256;
+  return ((size_t)(kPrep + kSpillStride) * B * P) * sizeof(double) + 256;
 }
 
 void launch_patch_search(const SearchArgs& a, void* scratch, cudaStream_t st) {
   const size_t n = (size_t)a.B * a.ax.n * a.ay.n;
   double* prep = static_cast<double*>(scratch);
-  unsigned* counter = reinterpret_cast<unsigned*>(static_cast<char*>(scratch) +
-                                                  (size_t)kPrep * n * sizeof(double));
+  double* spill = prep + (size_t)kPrep * n;
+  unsigned* counter = reinterpret_cast<unsigned*>(spill + (size_t)kSpillStride * n);
+  unsigned* spill_count = counter + 1;
   prof_begin(KC_SEARCH, st);
   const int TH = 128;
   k_patch_prep<<<(unsigned)((n + TH - 1) / TH), TH, 0, st>>>(a, prep, counter);
   note_launch();
+  static const size_t glanes = [] {
+    const char* e = getenv("DIS_GROUP_LANES");  // experiments only
+    return e ? (size_t)atoll(e) : kGroupLanes;
+  }();
   // coarse levels (few patches): a group of lanes per patch; fine levels: a
-  // lane per patch
-  const bool group = (a.ps == 8 && n * 8 <= kGroupLanes) || (a.ps == 12 && n * 16 <= kGroupLanes);
+  // lane per patch (+ the general kernel for the parked, irregular windows)
+  const bool group = (a.ps == 8 && n * 8 <= glanes) || (a.ps == 12 && n * 16 <= glanes);
   if (group) {
     if (a.ps == 8)
       launch_gn_group<8, 8>(a, prep, counter, n, st);
     else
       launch_gn_group<12, 16>(a, prep, counter, n, st);
-  } else {
-    int blocks;
-    static int nb8 = 0, nb12 = 0, nb0 = 0;
-    if (a.ps == 8) {
-      if (!nb8) nb8 = gn_blocks((const void*)k_patch_gn<8>);
-      blocks = nb8;
-    } else if (a.ps == 12) {
-      if (!nb12) nb12 = gn_blocks((const void*)k_patch_gn<12>);
-      blocks = nb12;
-    } else {
-      if (!nb0) nb0 = gn_blocks((const void*)k_patch_gn<0>);
-      blocks = nb0;
+    note_launch();
+  } else if (a.ps == 8 || a.ps == 12) {
+    static int per_sm8 = 0, per_sm12 = 0;
+    int& per_sm = a.ps == 8 ? per_sm8 : per_sm12;
+    if (!per_sm) {
+      if (a.ps == 8)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_patch_gn<8>, 256, 0);
+      else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_patch_gn<12>, 256, 0);
+      if (per_sm < 1) per_sm = 1;
     }
+    size_t blocks = (size_t)per_sm * sm_count();
     const size_t need = (n + 255) / 256;
-    if ((size_t)blocks > need) blocks = (int)need;
-    if (blocks < 1) blocks = 1;
+    if (blocks > need) blocks = need;
     if (a.ps == 8)
-      k_patch_gn<8><<<blocks, 256, 0, st>>>(a, prep, counter);
-    else if (a.ps == 12)
-      k_patch_gn<12><<<blocks, 256, 0, st>>>(a, prep, counter);
+      k_patch_gn<8><<<(unsigned)blocks, 256, 0, st>>>(a, prep, counter, spill, spill_count);
     else
-      k_patch_gn<0><<<blocks, 256, 0, st>>>(a, prep, counter);
+      k_patch_gn<12><<<(unsigned)blocks, 256, 0, st>>>(a, prep, counter, spill, spill_count);
+    note_launch();
+    // parked (irregular-window) patches: a lane group per patch
+    if (a.ps == 8)
+      launch_gn_group<8, 8>(a, prep, counter, n, st, spill, spill_count, true);
+    else
+      launch_gn_group<12, 16>(a, prep, counter, n, st, spill, spill_count, true);
+    note_launch();
+  } else {
+    size_t blocks = (n + 127) / 128;
+    k_patch_gn_general<<<(unsigned)blocks, 128, 0, st>>>(a, prep, spill, spill_count, false);
+    note_launch();
   }
-  note_launch();
   prof_end(KC_SEARCH, st);
 }
 
