@@ -235,6 +235,11 @@ DIS_API void dis_profile_reset(void);
 /* Blocks on the recorded events; writes total ms and launch counts. */
 DIS_API int dis_profile_read(double* ms_out, int64_t* count_out, int32_t n_classes);
 
+/* Test hook: exact_div_pos (the SOR's division) and IEEE `/` on device
+ * arrays n, d -> fast, ieee (count elements). */
+DIS_API int dis_selftest_div(const double* n, const double* d, double* fast,
+                             double* ieee, size_t count, void* stream);
+
 /* Human-readable message of the last failing call on this host thread. */
 DIS_API const char* dis_last_error(void);
 /* DIS_B200_ABI_VERSION of the loaded library. */

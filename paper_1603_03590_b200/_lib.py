@@ -33,7 +33,7 @@ EXPORTED = (
     "dis_patch_search_workspace_bytes", "dis_densify",
     "dis_refine_workspace_bytes", "dis_refine", "dis_upsample_flow", "dis_grid_axis",
     "dis_last_error", "dis_abi_version", "dis_last_launch_count", "dis_profile_enable",
-    "dis_profile_reset", "dis_profile_read",
+    "dis_profile_reset", "dis_profile_read", "dis_selftest_div",
 )
 
 KERNEL_CLASSES = ("pyramid", "patch_search", "densify", "tensor_assemble", "sor", "upsample")
@@ -103,6 +103,8 @@ def lib() -> ctypes.CDLL:
     L.dis_profile_read.argtypes = [ctypes.POINTER(ctypes.c_double),
                                    ctypes.POINTER(ctypes.c_int64), _i32]
     L.dis_profile_read.restype = ctypes.c_int
+    L.dis_selftest_div.argtypes = [_vp, _vp, _vp, _vp, _sz, _vp]
+    L.dis_selftest_div.restype = ctypes.c_int
     L.dis_abi_version.argtypes = []
     L.dis_abi_version.restype = _i32
     if L.dis_abi_version() != 1:

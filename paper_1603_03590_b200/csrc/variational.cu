@@ -182,61 +182,111 @@ __device__ __forceinline__ void st_cluster(const double* local, unsigned rank, d
   asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(ra), "d"(v) : "memory");
 }
 
+// mbarrier helpers (band-boundary signalling between the CTAs of a cluster)
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(unsigned bar_local, unsigned rank) {
+  unsigned ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(bar_local), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(ra)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
 // The wavefront SOR kernel (see the file header).
 //
-// Thread (row y, sweep t) computes pixel x = k - y - 2t at step k.  A pair's
-// rows are split over a cluster of C CTAs (1..8); CTA c owns the band of rows
-// [c*Hc, c*Hc + Hc) and runs S x Hp threads (Hp = band rows rounded up to
-// 32).  Shared memory holds
-//   ring[R][Hp+2][kPitch] : the records of the live diagonals (+ one halo row
+// Thread (sweep t, row group g) owns RT consecutive rows of a band and, at
+// step k, computes pixel x = k - y - 2t of each of them (all on diagonal
+// j = k - 2t).  Its rows are independent within a step (every neighbour
+// value is from an earlier step), so a thread carries RT independent update
+// chains.  A pair's rows are split over a cluster of C CTAs (1..16); CTA c
+// owns the band [c*Hc, c*Hc + Hc).  Shared memory holds
+//   ring[R][Hp+2][kPitch] : records of the live diagonals (+ one halo row
 //                           above and below the band), filled by cp.async
 //                           kLookahead steps ahead; entries outside the
 //                           level are zero-filled
-//   xuv[2][S][Hp+2][2]    : U, V each thread produced at the last two steps
+//   xuv[2][S][Hp+2][2]    : U, V produced at the last two steps
 //   xd [3][S][Hp+2][2]    : du, dv of the last three steps (own previous)
-// The neighbours of (x, y, t): left = own registers (step k-1); up =
-// xuv[k-1][t][y-1]; right = xuv[k-1][t-1][y]; down = xuv[k-1][t-1][y+1];
-// own previous du/dv = xd[k-2][t-1][y]; for t = 0 the initial values come
-// from the ring (du = 0 or the carried du of a chained pass).  The band's
-// boundary rows write their U, V into the neighbouring CTA's halo rows of
-// xuv through distributed shared memory.  One (cluster) barrier per step.
-// A thread whose pixel is outside the level computes finite garbage from
-// zero-filled entries and never stores it, so no selects are needed.
-template <int S>
-__global__ void __launch_bounds__(S * kMaxBandRows, 1)
+// Neighbours of (x, y, t): left = own registers (step k-1); up = the
+// thread's own row above (registers, step k-1) or xuv[k-1][t][y-1] for its
+// first row; right = xuv[k-1][t-1][y]; down = xuv[k-1][t-1][y+1]; own
+// previous du/dv = xd[k-2][t-1][y]; for t = 0 the initial values come from
+// the ring (du = 0, or the carried du of a chained pass).  The band's
+// boundary rows write their U, V straight into the neighbouring CTA's halo
+// rows of xuv (distributed shared memory) and signal it with a remote
+// mbarrier arrive; the consumer waits on its local mbarrier — neighbour to
+// neighbour, no cluster-wide barrier per step.  A thread whose pixel is
+// outside the level computes finite garbage from zero-filled entries and
+// never stores it, so no selects are needed.
+// explicit shared-space accesses (32-bit addresses; keeps the compiler
+// from re-deriving generic->shared windows every step)
+__device__ __forceinline__ double lds(unsigned a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts2(unsigned a, double x, double y) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a), "d"(x), "d"(y) : "memory");
+}
+__device__ __forceinline__ void lds2(unsigned a, double& x, double& y) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(a) : "memory");
+}
+
+template <int S, int RT>
+__global__ void __launch_bounds__(S * kMaxBandRows / RT, 1)
     k_sor(const double* __restrict__ rec, int B, int W, int H, int Hc, size_t Ls, double omega,
           const double* du_in, const double* dv_in, double* du_out, double* dv_out,
           double* __restrict__ fu, double* __restrict__ fv, uint32_t* status) {
   extern __shared__ double smem[];
   constexpr int R = ring_slots<S>();
   constexpr int kFieldsPerThread = (8 + S - 1) / S;
+  constexpr unsigned kRowB = kPitch * 8;  // ring row bytes
   const int C = (int)(gridDim.x / (unsigned)B) > 0 ? (int)(gridDim.x / (unsigned)B) : 1;
   const int c = C > 1 ? (int)cluster_rank() : 0;
   const int b = blockIdx.x / C;
-  const int Hp = blockDim.x / S;
-  const int t = threadIdx.x / Hp;       // sweep
-  const int ty = threadIdx.x - t * Hp;  // row within the band
+  const int TS = blockDim.x / S;          // threads per sweep
+  const int Hp = TS * RT;                 // band rows (padded)
+  const int t = threadIdx.x / TS;         // sweep
+  const int tg = threadIdx.x - t * TS;    // row group
   const int y0 = c * Hc;
-  const int y = y0 + ty;
+  const int ty0 = tg * RT;                // first band row of this thread
   const int nrows = min(Hc, H - y0);
-  const bool row_ok = ty < nrows;
   const int ndiag = W + H - 1;
   const int rows = Hp + 2;  // + halo above and below
-  const int slot_elems = rows * kPitch;
-  double* ring = smem;                         // [R][rows][kPitch]
-  double* xuv = ring + R * slot_elems;         // [2][S][rows][2]
-  double* xd = xuv + 2 * S * rows * 2;         // [3][S][rows][2]
+  const unsigned slot_bytes = (unsigned)rows * kRowB;
+  double* ring = smem;                                // [R][rows][kPitch]
+  double* xuvp = ring + (size_t)R * rows * kPitch;   // [2][S][rows][2]
+  double* xdp = xuvp + (size_t)2 * S * rows * 2;     // [3][S][rows][2]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xdp + (size_t)3 * S * rows * 2);
+  const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
+  const unsigned ring_end = ring_s + (unsigned)R * slot_bytes;
+  const unsigned xuv_s = (unsigned)__cvta_generic_to_shared(xuvp);
+  const unsigned xd_s = (unsigned)__cvta_generic_to_shared(xdp);
+  const unsigned uv_par_b = (unsigned)(S * rows * 16);  // one parity of xuv, bytes
+  const unsigned d_ph_b = (unsigned)(S * rows * 16);    // one phase of xd, bytes
+  // mbarriers [above p0, above p1, below p0, below p1]: one per direction and
+  // step parity, so a barrier's phase n is step 2n + p and a neighbour (at
+  // most one step ahead) can never overrun a phase its consumer still waits on
+  const unsigned bar_above = (unsigned)__cvta_generic_to_shared(bars);
+  const unsigned bar_below = bar_above + 16;
   const double* __restrict__ base = rec + (size_t)b * Ls;
   const size_t fstride = (size_t)B * Ls;
   const double* Dui = du_in ? du_in + (size_t)b * Ls : nullptr;  // may alias du_out
   const double* Dvi = dv_in ? dv_in + (size_t)b * Ls : nullptr;
   const double om1 = 1.0 - omega;
-  const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
-  const unsigned slot_bytes = (unsigned)(slot_elems * 8);
-  const int me = ty + 1;  // my row index in ring / xuv / xd
 
-  // cp.async of this thread's record fields (t, t+S, ...) of one ring row;
-  // src = &record[field 0] of the pixel, ok = pixel inside the level
+  // cp.async of this thread's record fields (t, t+S, ...) of one ring row
   auto fetch = [&](unsigned dst, const double* src, bool ok) {
     const double* g = ok ? src : base;
 #pragma unroll
@@ -246,173 +296,248 @@ __global__ void __launch_bounds__(S * kMaxBandRows, 1)
     }
   };
 
-  {  // the ring and the exchange buffers start at zero: inactive threads read
-     // slots whose diagonal is not loaded yet, and their garbage must stay
-     // finite (it is multiplied by an exact zero weight at the row starts)
-    const int nx = R * slot_elems + (2 + 3) * S * rows * 2;
+  {  // ring + exchange buffers start at zero (idle threads read them)
+    const int nx = R * rows * kPitch + (2 + 3) * S * rows * 2;
     for (int i = threadIdx.x; i < nx; i += blockDim.x) ring[i] = 0.0;
   }
+  if (threadIdx.x == 0 && C > 1) {
+    mbar_init(bar_above, S);
+    mbar_init(bar_above + 8, S);
+    mbar_init(bar_below, S);
+    mbar_init(bar_below + 8, S);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   __syncthreads();
-  // prefetch state for diagonal jn = k + kLookahead (own row, and the halo
-  // rows for the first / last thread of the band)
   int jn = 0;
-  unsigned sin_s = ring_s;  // smem slot address of diagonal jn
-  const double* gsrc = base + y;  // &record[jn * H + y]
+  unsigned sin_s = ring_s;
+  const double* gsrc = base + y0 + ty0;  // &record[jn * H + y0 + ty0]
+  const unsigned my_ring_row = (unsigned)(ty0 + 1) * kRowB;
   auto issue_next = [&]() {
     if (jn < ndiag) {
-      const int x = jn - y;
-      fetch(sin_s + (unsigned)(me * kPitch * 8), gsrc, y < H && x >= 0 && x < W);
-      if (ty == 0)
-        fetch(sin_s, gsrc - 1, y0 > 0 && x + 1 >= 0 && x + 1 < W);
-      if (ty == Hp - 1)
-        fetch(sin_s + (unsigned)((Hp + 1) * kPitch * 8), gsrc + 1,
-              y + 1 < H && x - 1 >= 0 && x - 1 < W);
+#pragma unroll
+      for (int i = 0; i < RT; ++i) {
+        const int yy = y0 + ty0 + i;
+        const int x = jn - yy;
+        fetch(sin_s + my_ring_row + i * kRowB, gsrc + i, yy < H && x >= 0 && x < W);
+      }
+      if (tg == 0) fetch(sin_s, gsrc - 1, y0 > 0 && jn - (y0 - 1) >= 0 && jn - (y0 - 1) < W);
+      if (tg == TS - 1) {
+        const int yy = y0 + Hp;
+        fetch(sin_s + (unsigned)(Hp + 1) * kRowB, gsrc + RT, yy < H && jn - yy >= 0 &&
+                                                                 jn - yy < W);
+      }
     }
     cp_async_commit();
     ++jn;
     gsrc += H;
     sin_s += slot_bytes;
-    if (sin_s == ring_s + (unsigned)R * slot_bytes) sin_s = ring_s;
+    if (sin_s == ring_end) sin_s = ring_s;
   };
   for (int j = 0; j < kLookahead; ++j) issue_next();
   cp_async_wait<kLookahead - 2>();
-  if (C > 1) {
+  if (C > 1) {  // barriers initialised everywhere before any remote arrive
     cluster_arrive();
     cluster_wait();
   } else {
     __syncthreads();
   }
 
-  double lU = 0.0, lV = 0.0, lW = 0.0;  // this thread's previous pixel (left neighbour)
-  const bool hasU = y > 0, hasD = y < H - 1;
+  double lU[RT], lV[RT], lW[RT];  // each row's previous pixel (left neighbour / up of next row)
+#pragma unroll
+  for (int i = 0; i < RT; ++i) lU[i] = lV[i] = lW[i] = 0.0;
   bool bad = false;
   const int nsteps = ndiag + 2 * (S - 1);
-  // ring slot (element offset) of this sweep's diagonal j = k - 2t, and of j +- 1
-  int sj = ((-2 * t) % R + R) % R;
-  int offj = sj * slot_elems;
-  const int ring_elems = R * slot_elems;
-  // xuv / xd element offsets of (t, me) for each parity / phase
-  const int uv_me = (t * rows + me) * 2;
-  const int uv_par = S * rows * 2;
-  const int d_ph = S * rows * 2;
-  int m3 = 0;  // k mod 3
-  int x = -y - 2 * t;  // pixel of this thread at step k
+  // ring slot address of diagonal j = k - 2t (rotates by one slot per step)
+  unsigned a_j = ring_s + (unsigned)(((-2 * t) % R + R) % R) * slot_bytes;
+  // exchange-buffer offsets of (t, my first row) and (t-1, my first row)
+  const unsigned uv_me = (unsigned)((t * rows + ty0 + 1) * 16);
+  const unsigned uv_prev = (unsigned)(((t > 0 ? t - 1 : 0) * rows + ty0 + 1) * 16);
+  unsigned uv_r = xuv_s + uv_par_b, uv_w = xuv_s;  // parity of step k-1 / step k
+  unsigned d_w = xd_s, d_r = xd_s + d_ph_b;       // phase k mod 3 / (k-2) mod 3
+  const unsigned d_end = xd_s + 3 * d_ph_b;
   const size_t fplane = (size_t)W * H;
-  const bool top_cx = C > 1 && ty == 0 && c > 0;
-  const bool bot_cx = C > 1 && ty == nrows - 1 && c < C - 1;
-  for (int k = 0; k < nsteps; ++k) {
+  // band-boundary roles
+  const bool first_owner = C > 1 && c > 0 && tg == 0;                  // needs "up" of row 0
+  const int last_ty = nrows - 1;
+  const bool last_owner = C > 1 && c < C - 1 && ty0 <= last_ty && last_ty < ty0 + RT;
+  int xk = -y0 - ty0 - 2 * t;  // x of my first row at step k
+  for (int k = 0; k < nsteps; ++k, ++xk) {
+    if (k > 0 && C > 1) {  // halo values of step k-1 from the neighbouring bands
+      const unsigned sel = (unsigned)((k - 1) & 1) * 8u;
+      const unsigned par = (unsigned)(((k - 1) >> 1) & 1);
+      if (first_owner) mbar_wait_parity(bar_above + sel, par);
+      // every boundary-row thread waits (t = 0 does not read the halo, but
+      // its next write into the neighbour's halo must not overtake the
+      // neighbour's read of the previous one)
+      if (last_owner) mbar_wait_parity(bar_below + sel, par);
+    }
     issue_next();
     const int j = k - 2 * t;
-    const int offm = (offj == 0 ? ring_elems : offj) - slot_elems;
-    const int offp = offj + slot_elems == ring_elems ? 0 : offj + slot_elems;
-    const double* rp = ring + offj + me * kPitch;        // (x, y)
-    const double* rm = ring + offm + (me - 1) * kPitch;  // (x, y-1)
-    const double* rn = ring + offp + me * kPitch;        // (x+1, y); +kPitch: (x, y+1)
-    const int wpar = k & 1;
-    const double* uvp = xuv + (wpar ? 0 : uv_par) + uv_me;  // step k-1 values at (t, me)
-    const double uc = rp[F_U], vc = rp[F_V], wp = rp[F_WS];
-    const double m00 = rp[F_M00], m01 = rp[F_M01], m11 = rp[F_M11];
-    const double r0 = rp[F_R0], r1 = rp[F_R1];
-    const double upU = uvp[-2], upV = uvp[-1];
-    const double upW = rm[F_WS];
-    const double rW = rn[F_WS];
-    const double dnW = rn[F_WS + kPitch];
-    double rU, rV, dnU, dnV, du, dv;
-    if (t > 0) {
-      const double* q = uvp - rows * 2;  // (t-1, me), (t-1, me+1)
-      rU = q[0];
-      rV = q[1];
-      dnU = q[2];
-      dnV = q[3];
-      const int q2 = m3 == 2 ? 0 : m3 + 1;  // (k-2) mod 3
-      const double* d = xd + q2 * d_ph + uv_me - rows * 2;
-      du = d[0];
-      dv = d[1];
-    } else {
-      rU = rn[F_U];
-      rV = rn[F_V];
-      dnU = rn[F_U + kPitch];
-      dnV = rn[F_V + kPitch];
-      du = 0.0;
-      dv = 0.0;
-      if (Dui) {  // chained pass: the carried du/dv of the previous sweeps
+    const unsigned a_m = (a_j == ring_s ? ring_end : a_j) - slot_bytes;
+    const unsigned a_p = a_j + slot_bytes == ring_end ? ring_s : a_j + slot_bytes;
+    const unsigned rp0 = a_j + my_ring_row;          // (x, y) of my first row
+    const unsigned rm0 = a_m + my_ring_row - kRowB;  // (x, y-1)
+    const unsigned rn0 = a_p + my_ring_row;          // (x+1, y); + kRowB: (x, y+1)
+    double nU[RT], nV[RT], mU[RT], mV[RT], dU[RT], dV[RT], ucA[RT], vcA[RT], wpA[RT],
+        m01A[RT], den_uA[RT], den_vA[RT], r1svA[RT];
+    // Phase A (all rows, straight-line): neighbour values, weights, the four
+    // sums and the u numerator.  Decreasing i: the "up" value of row i is
+    // row i-1's step k-1 value (registers).
+#pragma unroll
+    for (int i = RT - 1; i >= 0; --i) {
+      const int y = y0 + ty0 + i;
+      const int x = xk - i;
+      const bool hasU = y > 0, hasD = y < H - 1;
+      const unsigned rp = rp0 + i * kRowB, rm = rm0 + i * kRowB, rn = rn0 + i * kRowB;
+      const double uc = lds(rp + 8 * F_U), vc = lds(rp + 8 * F_V), wp = lds(rp + 8 * F_WS);
+      const double m00 = lds(rp + 8 * F_M00), m01 = lds(rp + 8 * F_M01);
+      const double m11 = lds(rp + 8 * F_M11);
+      const double r0 = lds(rp + 8 * F_R0), r1 = lds(rp + 8 * F_R1);
+      double upU, upV;
+      if (i > 0) {  // row above is mine: its value from step k-1 (not yet updated)
+        upU = lU[i - 1];
+        upV = lV[i - 1];
+      } else {
+        lds2(uv_r + uv_me - 16, upU, upV);
+      }
+      const double upW = lds(rm + 8 * F_WS);
+      const double rW = lds(rn + 8 * F_WS);
+      const double dnW = lds(rn + kRowB + 8 * F_WS);
+      double rU, rV, dnU, dnV, du, dv;
+      if (t > 0) {
+        lds2(uv_r + uv_prev + 16 * i, rU, rV);
+        lds2(uv_r + uv_prev + 16 * (i + 1), dnU, dnV);
+        lds2(d_r + uv_prev + 16 * i, du, dv);
+      } else if (Dui) {  // chained pass: the carried du/dv of the previous sweeps
         const int jp = j + 1;
         const bool okp = jp >= 0 && jp < ndiag;
-        const bool ok = j >= 0 && j < ndiag;
-        rU = rU + Dui[okp ? (size_t)jp * H + y : 0];
-        rV = rV + Dvi[okp ? (size_t)jp * H + y : 0];
-        dnU = dnU + Dui[okp && hasD ? (size_t)jp * H + y + 1 : 0];
-        dnV = dnV + Dvi[okp && hasD ? (size_t)jp * H + y + 1 : 0];
+        const bool ok = j >= 0 && j < ndiag && y < H;
+        const int yc = y < H ? y : H - 1;
+        rU = lds(rn + 8 * F_U) + Dui[okp ? (size_t)jp * H + yc : 0];
+        rV = lds(rn + 8 * F_V) + Dvi[okp ? (size_t)jp * H + yc : 0];
+        dnU = lds(rn + kRowB + 8 * F_U) + Dui[okp && hasD ? (size_t)jp * H + yc + 1 : 0];
+        dnV = lds(rn + kRowB + 8 * F_V) + Dvi[okp && hasD ? (size_t)jp * H + yc + 1 : 0];
         du = Dui[ok ? (size_t)j * H + y : 0];
         dv = Dvi[ok ? (size_t)j * H + y : 0];
       } else {
-        rU = rU + 0.0;  // u + du with du = 0 (reference: u[q] + du[q])
-        rV = rV + 0.0;
-        dnU = dnU + 0.0;
-        dnV = dnV + 0.0;
+        rU = lds(rn + 8 * F_U) + 0.0;  // u + du with du = 0 (reference: u[q] + du[q])
+        rV = lds(rn + 8 * F_V) + 0.0;
+        dnU = lds(rn + kRowB + 8 * F_U) + 0.0;
+        dnV = lds(rn + kRowB + 8 * F_V) + 0.0;
+        du = 0.0;
+        dv = 0.0;
       }
+      // absent neighbours (borders) contribute wq = +0 times a finite value:
+      // adding an exact zero leaves the reference's partial sums unchanged
+      const double wqL = x > 0 ? 0.5 * (wp + lW[i]) : 0.0;
+      const double wqR = x < W - 1 ? 0.5 * (wp + rW) : 0.0;
+      const double wqU = hasU ? 0.5 * (wp + upW) : 0.0;
+      const double wqD = hasD ? 0.5 * (wp + dnW) : 0.0;
+      const double sw = (((0.0 + wqL) + wqR) + wqU) + wqD;
+      const double su = (((0.0 + wqL * (lU[i] - uc)) + wqR * (rU - uc)) + wqU * (upU - uc)) +
+                        wqD * (dnU - uc);
+      const double sv = (((0.0 + wqL * (lV[i] - vc)) + wqR * (rV - vc)) + wqU * (upV - vc)) +
+                        wqD * (dnV - vc);
+      ucA[i] = uc;
+      vcA[i] = vc;
+      wpA[i] = wp;
+      m01A[i] = m01;
+      den_uA[i] = m00 + sw;
+      den_vA[i] = m11 + sw;
+      r1svA[i] = r1 + sv;
+      dU[i] = du;
+      dV[i] = dv;
+      nU[i] = r0 + su - m01 * dv;
     }
-    // absent neighbours (borders) contribute wq = +0 times a finite value:
-    // adding an exact zero leaves the reference's partial sums unchanged
-    const double wqL = x > 0 ? 0.5 * (wp + lW) : 0.0;
-    const double wqR = x < W - 1 ? 0.5 * (wp + rW) : 0.0;
-    const double wqU = hasU ? 0.5 * (wp + upW) : 0.0;
-    const double wqD = hasD ? 0.5 * (wp + dnW) : 0.0;
-    const double sw = (((0.0 + wqL) + wqR) + wqU) + wqD;
-    const double su =
-        (((0.0 + wqL * (lU - uc)) + wqR * (rU - uc)) + wqU * (upU - uc)) + wqD * (dnU - uc);
-    const double sv =
-        (((0.0 + wqL * (lV - vc)) + wqR * (rV - vc)) + wqU * (upV - vc)) + wqD * (dnV - vc);
-    const double den_u = m00 + sw;
-    const double nu = om1 * du + omega * exact_div_pos(r0 + su - m01 * dv, den_u);
-    du = den_u > 1e-12 ? nu : du;
-    const double den_v = m11 + sw;
-    const double nv = om1 * dv + omega * exact_div_pos(r1 + sv - m01 * du, den_v);
-    dv = den_v > 1e-12 ? nv : dv;
-    const double U = uc + du, V = vc + dv;
-    lU = U;
-    lV = V;
-    lW = wp;
-    {
-      double* o = xuv + (wpar ? uv_par : 0) + uv_me;
-      o[0] = U;
-      o[1] = V;
-      double* od = xd + m3 * d_ph + uv_me;
-      od[0] = du;
-      od[1] = dv;
-      if (top_cx) {  // my band's first row -> CTA c-1's row below its band
-        double* h = o + (Hc + 1 - me) * 2;
-        st_cluster(h, c - 1, U);
-        st_cluster(h + 1, c - 1, V);
-      }
-      if (bot_cx) {  // my band's last row -> CTA c+1's row above its band
-        double* h = o - me * 2;
-        st_cluster(h, c + 1, U);
-        st_cluster(h + 1, c + 1, V);
-      }
+    // Phase B: u quotients (straight-line fast division; rare IEEE fallback;
+    // quotients of rows with den <= 1e-12 are discarded, whatever they are)
+    bool slow = false;
+#pragma unroll
+    for (int i = 0; i < RT; ++i) {
+      slow = slow | ((den_uA[i] > 1e-12) & !div_fast_ok(nU[i], den_uA[i]));
+      mU[i] = div_fast_rn(nU[i], den_uA[i]);
     }
-    if (t == S - 1 && row_ok && x >= 0 && x < W) {
-      if (du_out) {
-        du_out[(size_t)b * Ls + (size_t)j * H + y] = du;
-        dv_out[(size_t)b * Ls + (size_t)j * H + y] = dv;
+    if (slow) {
+#pragma unroll
+      for (int i = 0; i < RT; ++i) mU[i] = exact_div_pos(nU[i], den_uA[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < RT; ++i) {
+      const double q = nU[i] == 0.0 ? nU[i] : mU[i];
+      const double nu = om1 * dU[i] + omega * q;
+      dU[i] = den_uA[i] > 1e-12 ? nu : dU[i];
+      nV[i] = r1svA[i] - m01A[i] * dU[i];
+    }
+    // Phase C: v quotients
+    slow = false;
+#pragma unroll
+    for (int i = 0; i < RT; ++i) {
+      slow = slow | ((den_vA[i] > 1e-12) & !div_fast_ok(nV[i], den_vA[i]));
+      mV[i] = div_fast_rn(nV[i], den_vA[i]);
+    }
+    if (slow) {
+#pragma unroll
+      for (int i = 0; i < RT; ++i) mV[i] = exact_div_pos(nV[i], den_vA[i]);
+    }
+    // Phase D: updates, exchange stores, halo, output
+#pragma unroll
+    for (int i = 0; i < RT; ++i) {
+      const int ty = ty0 + i;
+      const int y = y0 + ty;
+      const int x = xk - i;
+      const double q = nV[i] == 0.0 ? nV[i] : mV[i];
+      const double nv = om1 * dV[i] + omega * q;
+      const double du = dU[i];
+      const double dv = den_vA[i] > 1e-12 ? nv : dV[i];
+      const double U = ucA[i] + du, V = vcA[i] + dv;
+      lU[i] = U;
+      lV[i] = V;
+      lW[i] = wpA[i];
+      if (ty < nrows) {  // padding rows never store: row nrows+1 is the halo
+        sts2(uv_w + uv_me + 16 * i, U, V);
+        sts2(d_w + uv_me + 16 * i, du, dv);
       }
-      if (fu) {
-        const size_t o = (size_t)b * fplane + (size_t)y * W + x;
-        fu[o] = U;
-        fv[o] = V;
-        bad |= !(isfinite(U) && isfinite(V));
+      if (C > 1) {
+        if (ty == 0 && c > 0) {  // band's first row -> CTA c-1's row below its band
+          double* h = xuvp + ((k & 1) * S * rows + t * rows + (Hc + 1)) * 2;
+          st_cluster(h, c - 1, U);
+          st_cluster(h + 1, c - 1, V);
+          mbar_arrive_remote(bar_below + (unsigned)(k & 1) * 8u, c - 1);
+        }
+        if (ty == last_ty && c < C - 1) {  // band's last row -> CTA c+1's row above its band
+          double* h = xuvp + ((k & 1) * S * rows + t * rows) * 2;
+          st_cluster(h, c + 1, U);
+          st_cluster(h + 1, c + 1, V);
+          mbar_arrive_remote(bar_above + (unsigned)(k & 1) * 8u, c + 1);
+        }
+      }
+      if (t == S - 1 && ty < nrows && x >= 0 && x < W) {
+        if (du_out) {
+          du_out[(size_t)b * Ls + (size_t)j * H + y] = du;
+          dv_out[(size_t)b * Ls + (size_t)j * H + y] = dv;
+        }
+        if (fu) {
+          const size_t oo = (size_t)b * fplane + (size_t)y * W + x;
+          fu[oo] = U;
+          fv[oo] = V;
+          bad |= !(isfinite(U) && isfinite(V));
+        }
       }
     }
     cp_async_wait<kLookahead - 2>();
-    if (C > 1) {
-      cluster_arrive();
-      cluster_wait();
-    } else {
-      __syncthreads();
-    }
-    offj = offp;
-    m3 = m3 == 2 ? 0 : m3 + 1;
-    ++x;
+    __syncthreads();
+    a_j = a_p;
+    const unsigned tu = uv_r;
+    uv_r = uv_w;
+    uv_w = tu;
+    d_w += d_ph_b;  // phases k mod 3 and (k-2) mod 3 both advance by one
+    if (d_w == d_end) d_w = xd_s;
+    d_r += d_ph_b;
+    if (d_r == d_end) d_r = xd_s;
+  }
+  if (C > 1) {  // no CTA may exit while a neighbour can still write into it
+    cluster_arrive();
+    cluster_wait();
   }
   if (bad) set_status(status, DIS_STATUS_NONFINITE_FLOW);
 }
@@ -421,7 +546,19 @@ template <int S>
 static size_t sor_smem_bytes(int hp) {
   const size_t rows = (size_t)hp + 2;
   return ((size_t)ring_slots<S>() * rows * kPitch + (size_t)(2 + 3) * S * rows * 2) *
-         sizeof(double);
+             sizeof(double) +
+         4 * sizeof(uint64_t);
+}
+
+// rows per thread (RT): a thread carries RT independent row updates per
+// step; fewer rows per thread = more warps to hide latency.
+static int sor_rows_per_thread() {
+  static const int rt = [] {
+    const char* e = getenv("DIS_SOR_RT");  // experiments only
+    const int v = e ? atoi(e) : 1;
+    return (v == 1 || v == 2 || v == 4) ? v : 1;
+  }();
+  return rt;
 }
 
 constexpr size_t kMaxSmem = 227 * 1024;
@@ -430,31 +567,36 @@ constexpr size_t kMaxSmem = 227 * 1024;
 // its ring in shared memory, and, for small batches, to spread a pair over
 // several SMs (the step rate of one band is bound by its SM's FP64 pipe).
 template <int S>
-static int choose_cluster(int B, int H) {
+static int choose_cluster(int B, int H, int RT) {
   static const int forced = [] {
     const char* e = getenv("DIS_SOR_CLUSTER");  // experiments only
     return e ? atoi(e) : 0;
   }();
   if (forced > 0) return forced;
-  auto hp = [&](int C) { return ((H + C - 1) / C + 31) / 32 * 32; };
+  const int q = 32 * RT;
+  auto hp = [&](int C) { return ((H + C - 1) / C + q - 1) / q * q; };
   int C = 1;
-  while (C < 16 && (hp(C) > kMaxBandRows || sor_smem_bytes<S>(hp(C)) > kMaxSmem)) ++C;
+  while (C < 16 && (hp(C) > kMaxBandRows || hp(C) / RT * S > S * kMaxBandRows / RT ||
+                    sor_smem_bytes<S>(hp(C)) > kMaxSmem))
+    ++C;
   return C;
 }
 
-template <int S>
-static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const double* dvi,
-                        double* duo, double* dvo, bool final_pass, cudaStream_t st) {
-  const int C = choose_cluster<S>(a.B, a.H);
+template <int S, int RT>
+static int launch_sor_rt(const RefineArgs& a, size_t Ls, const double* dui, const double* dvi,
+                         double* duo, double* dvo, bool final_pass, cudaStream_t st) {
+  const int C = choose_cluster<S>(a.B, a.H, RT);
   const int Hc = (a.H + C - 1) / C;
-  const int hp = (Hc + 31) / 32 * 32;
-  const int threads = hp * S;
+  const int q = 32 * RT;
+  const int hp = (Hc + q - 1) / q * q;
+  const int threads = hp / RT * S;
   const size_t smem = sor_smem_bytes<S>(hp);
   if (hp > kMaxBandRows || smem > kMaxSmem) return DIS_ERR_VALUE;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_sor<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
-    cudaFuncSetAttribute(k_sor<S>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_sor<S, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kMaxSmem);
+    cudaFuncSetAttribute(k_sor<S, RT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -471,9 +613,19 @@ static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const
   cfg.numAttrs = 1;
   double* fu = final_pass ? a.fu : nullptr;
   double* fv = final_pass ? a.fv : nullptr;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_sor<S>, (const double*)a.rec, a.B, a.W, a.H, Hc,
-                                     Ls, a.omega, dui, dvi, duo, dvo, fu, fv, a.status);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_sor<S, RT>, (const double*)a.rec, a.B, a.W, a.H,
+                                     Hc, Ls, a.omega, dui, dvi, duo, dvo, fu, fv, a.status);
   return e == cudaSuccess ? DIS_OK : DIS_ERR_CUDA;
+}
+
+template <int S>
+static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const double* dvi,
+                        double* duo, double* dvo, bool final_pass, cudaStream_t st) {
+  // more than 5 sweeps: the per-row shared memory grows, keep one row per thread
+  const int rt = S > 5 ? 1 : sor_rows_per_thread();
+  if (rt == 4) return launch_sor_rt<S, 4>(a, Ls, dui, dvi, duo, dvo, final_pass, st);
+  if (rt == 2) return launch_sor_rt<S, 2>(a, Ls, dui, dvi, duo, dvo, final_pass, st);
+  return launch_sor_rt<S, 1>(a, Ls, dui, dvi, duo, dvo, final_pass, st);
 }
 
 static int launch_sor(const RefineArgs& a, size_t Ls, int S, const double* dui,

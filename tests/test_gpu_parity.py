@@ -34,6 +34,38 @@ def _np(t):
     return t.detach().cpu().numpy()
 
 
+def test_exact_div_matches_ieee(torch):
+    """The SOR/densify/patch-search division helper is bit-identical to IEEE
+    division over ~50M operand pairs: SOR-like magnitudes, random exponents
+    over the whole fast-path range, tiny/huge/zero numerators (fallback)."""
+    from paper_1603_03590_b200 import _lib
+
+    rng = np.random.default_rng(123)
+    parts = []
+    for _ in range(6):
+        n = 8_000_000
+        num = rng.standard_normal(n) * 10.0 ** rng.uniform(-12, 8, n)
+        den = 10.0 ** rng.uniform(-11.9, 10, n) * rng.uniform(1, 2, n)
+        parts.append((num, den))
+    e1 = np.ldexp(rng.uniform(1, 2, 2_000_000), rng.integers(-1000, 1000, 2_000_000))
+    e2 = np.ldexp(rng.uniform(1, 2, 2_000_000), rng.integers(-1000, 1000, 2_000_000))
+    parts.append((e1 * np.sign(rng.standard_normal(2_000_000)), e2))
+    special = np.array([0.0, -0.0, 1e-300, -1e-300, 5e-324, 1e300, 1.0, -1.0, 3.0, np.nextafter(1, 2)])
+    parts.append((np.repeat(special, len(special)), np.tile(np.abs(special[special != 0][:8]).tolist() + [2.0, 7.0], len(special))))
+    L = _lib.lib()
+    for num, den in parts:
+        n_t = torch.tensor(num, device="cuda")
+        d_t = torch.tensor(den, device="cuda")
+        fast = torch.empty_like(n_t)
+        ieee = torch.empty_like(n_t)
+        _lib.check(L.dis_selftest_div(n_t.data_ptr(), d_t.data_ptr(), fast.data_ptr(),
+                                      ieee.data_ptr(), n_t.numel(), None))
+        f = fast.cpu().numpy().view(np.uint64)
+        i = ieee.cpu().numpy().view(np.uint64)
+        bad = np.flatnonzero(f != i)
+        assert bad.size == 0, (num[bad[:5]], den[bad[:5]])
+
+
 def test_pyramid_bit_exact(torch, st):
     g = golden("pyramid.npz")
     levels = st.build_pyramid(g["img"][None], 4, finest=0)

@@ -1,5 +1,4 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -2
-PROF="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --config c1"
-$PROF > gpurun_out/prof_plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c1.csv $PROF > gpurun_out/ncu_launch.log 2>&1
+export DIS_SOR_RT=1
+python tools/sor_bench.py 16 54 128 2 > gpurun_out/sorprof_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k_sor -s 1 -c 1 -o gpurun_out/sorprof6 -f python tools/sor_bench.py 16 54 128 2 > gpurun_out/sorprof_ncu.log 2>&1
