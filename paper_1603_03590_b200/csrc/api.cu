@@ -439,16 +439,43 @@ size_t dis_workspace_bytes(int32_t B, int32_t H, int32_t W, const dis_params_t* 
   return pl.total;
 }
 
-size_t dis_host_workspace_bytes(int32_t B, int32_t H, int32_t W, int32_t dtype,
-                                const dis_params_t* p) {
-  size_t base = dis_workspace_bytes(B, H, W, p);
+// ---- host-buffer path: chunked, multi-stream pipeline -----------------------
+// The batch is cut into nchunks chunks, each with its own slice of the
+// workspace and its own internal stream: chunk i's host->device copy, its
+// kernels and its device->host copy are stream-ordered, different chunks
+// overlap (the two copy directions run on separate copy engines, concurrently
+// with the kernels of other chunks).
+namespace {
+constexpr int kHostChunksMax = 4;
+
+int host_chunks(int B) { return B >= kHostChunksMax ? kHostChunksMax : (B < 1 ? 1 : B); }
+
+size_t host_chunk_bytes(int Bc, int H, int W, int dtype, const dis_params_t* p) {
+  size_t base = dis_workspace_bytes(Bc, H, W, p);
   if (!base) return 0;
   size_t cur = base;
-  const size_t frames = (size_t)B * H * W * dtype_size(dtype);
+  const size_t frames = (size_t)Bc * H * W * dtype_size(dtype);
   take(cur, frames);
   take(cur, frames);
-  take(cur, (size_t)B * H * W * 2 * sizeof(double));
+  take(cur, (size_t)Bc * H * W * 2 * sizeof(double));
   return (cur + 255) & ~size_t(255);
+}
+
+struct HostStreams {
+  int dev = -1;
+  cudaStream_t s[kHostChunksMax] = {};
+  cudaEvent_t start = nullptr, done[kHostChunksMax] = {};
+};
+std::mutex g_host_mu;
+HostStreams g_host[16];
+}  // namespace
+
+size_t dis_host_workspace_bytes(int32_t B, int32_t H, int32_t W, int32_t dtype,
+                                const dis_params_t* p) {
+  const int n = host_chunks(B);
+  const int Bc = (B + n - 1) / n;
+  const size_t per = host_chunk_bytes(Bc, H, W, dtype, p);
+  return per ? per * n : 0;
 }
 
 int dis_flow_batch(const void* frame1, const void* frame2, int32_t dtype, int32_t B, int32_t H,
@@ -504,25 +531,67 @@ int dis_flow_batch_host(const void* host_frame1, const void* host_frame2, int32_
   const size_t need = dis_host_workspace_bytes(B, H, W, dtype, p);
   if (workspace_bytes < need)
     return fail(DIS_ERR_WORKSPACE, "workspace holds %zu bytes, need %zu", workspace_bytes, need);
-  Plan pl;
-  make_plan(p, B, H, W, &pl);
-  size_t cur = pl.total;
-  const size_t fbytes = (size_t)B * H * W * dtype_size(dtype);
-  const size_t obytes = (size_t)B * H * W * 2 * sizeof(double);
-  char* base = static_cast<char*>(workspace);
-  void* d1 = base + take(cur, fbytes);
-  void* d2 = base + take(cur, fbytes);
-  double* dout = reinterpret_cast<double*>(base + take(cur, obytes));
+  const int n = host_chunks(B);
+  const int Bc = (B + n - 1) / n;
+  const size_t per = host_chunk_bytes(Bc, H, W, dtype, p);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> guard(g_host_mu);
+  HostStreams& hs = g_host[dev & 15];
+  if (hs.dev != dev) {
+    for (int i = 0; i < kHostChunksMax; ++i) {
+      cudaStreamCreateWithFlags(&hs.s[i], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&hs.done[i], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&hs.start, cudaEventDisableTiming);
+    hs.dev = dev;
+  }
   cudaStream_t st = as_stream(stream);
-  cudaMemcpyAsync(d1, host_frame1, fbytes, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(d2, host_frame2, fbytes, cudaMemcpyHostToDevice, st);
-  rc = dis_flow_batch(d1, d2, dtype, B, H, W, p, dout, workspace, pl.total, stream);
-  if (rc) return rc;
-  cudaMemcpyAsync(host_flow_out, dout, obytes, cudaMemcpyDeviceToHost, st);
-  uint32_t status = 0;
-  rc = dis_read_status(workspace, &status, stream);
-  if (rc) return rc;
-  return dis_status_to_error(status);
+  cudaEventRecord(hs.start, st);  // chunks start after the caller's prior work
+  const size_t esz = dtype_size(dtype);
+  const size_t px = (size_t)H * W;
+  long long launches = 0;
+  int used = 0;
+  for (int c = 0; c < n; ++c) {
+    const int b0 = c * Bc;
+    const int bn = B - b0 < Bc ? B - b0 : Bc;
+    if (bn <= 0) break;
+    ++used;
+    cudaStream_t cs = hs.s[c];
+    cudaStreamWaitEvent(cs, hs.start, 0);
+    char* wsc = static_cast<char*>(workspace) + (size_t)c * per;
+    Plan pl;
+    make_plan(p, bn, H, W, &pl);
+    size_t cur = dis_workspace_bytes(Bc, H, W, p);
+    const size_t fbytes = (size_t)bn * px * esz;
+    const size_t obytes = (size_t)bn * px * 2 * sizeof(double);
+    void* d1 = wsc + take(cur, (size_t)Bc * px * esz);
+    void* d2 = wsc + take(cur, (size_t)Bc * px * esz);
+    double* dout = reinterpret_cast<double*>(wsc + take(cur, (size_t)Bc * px * 2 * sizeof(double)));
+    cudaMemcpyAsync(d1, static_cast<const char*>(host_frame1) + (size_t)b0 * px * esz, fbytes,
+                    cudaMemcpyHostToDevice, cs);
+    cudaMemcpyAsync(d2, static_cast<const char*>(host_frame2) + (size_t)b0 * px * esz, fbytes,
+                    cudaMemcpyHostToDevice, cs);
+    rc = dis_flow_batch(d1, d2, dtype, bn, H, W, p, dout, wsc, pl.total, cs);
+    if (rc) return rc;
+    launches += g_launches.load();
+    cudaMemcpyAsync(host_flow_out + (size_t)b0 * px * 2, dout, obytes, cudaMemcpyDeviceToHost,
+                    cs);
+    cudaEventRecord(hs.done[c], cs);
+  }
+  for (int c = 0; c < used; ++c) cudaStreamWaitEvent(st, hs.done[c], 0);
+  g_launches = launches;
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return fail(DIS_ERR_CUDA, "dis_flow_batch_host: %s", cudaGetErrorString(e));
+  uint32_t any = 0;
+  for (int c = 0; c < used; ++c) {
+    uint32_t status = 0;
+    e = cudaMemcpy(&status, static_cast<char*>(workspace) + (size_t)c * per, sizeof(uint32_t),
+                   cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return fail(DIS_ERR_CUDA, "dis_flow_batch_host: %s", cudaGetErrorString(e));
+    any |= status;
+  }
+  return dis_status_to_error(any);
 }
 
 // ---- stage entry points -----------------------------------------------------
