@@ -192,6 +192,23 @@ __device__ __forceinline__ void mbar_arrive_remote(unsigned bar_local, unsigned 
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(ra)
                : "memory");
 }
+// st.async of (x, y) into CTA `rank`'s shared memory at local-equivalent
+// address a; completion is counted (16 bytes) on that CTA's mbarrier bar
+__device__ __forceinline__ void st_async2(unsigned a, unsigned bar, unsigned rank, double x,
+                                          double y) {
+  unsigned ra, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rb) : "r"(bar), "r"(rank));
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(
+          ra),
+      "d"(x), "d"(y), "r"(rb)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_wait_parity(unsigned bar, unsigned parity) {
   asm volatile(
       "{\n"
@@ -301,10 +318,12 @@ __global__ void __launch_bounds__(S * kMaxBandRows / RT, 1)
     for (int i = threadIdx.x; i < nx; i += blockDim.x) ring[i] = 0.0;
   }
   if (threadIdx.x == 0 && C > 1) {
-    mbar_init(bar_above, S);
-    mbar_init(bar_above + 8, S);
-    mbar_init(bar_below, S);
-    mbar_init(bar_below + 8, S);
+    // one local arrive (the consumer's expect_tx) per phase; the neighbour's
+    // S st.async (16 bytes each) complete the phase's transaction count
+    mbar_init(bar_above, 1);
+    mbar_init(bar_above + 8, 1);
+    mbar_init(bar_below, 1);
+    mbar_init(bar_below + 8, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -362,14 +381,20 @@ __global__ void __launch_bounds__(S * kMaxBandRows / RT, 1)
   const bool last_owner = C > 1 && c < C - 1 && ty0 <= last_ty && last_ty < ty0 + RT;
   int xk = -y0 - ty0 - 2 * t;  // x of my first row at step k
   for (int k = 0; k < nsteps; ++k, ++xk) {
-    if (k > 0 && C > 1) {  // halo values of step k-1 from the neighbouring bands
-      const unsigned sel = (unsigned)((k - 1) & 1) * 8u;
-      const unsigned par = (unsigned)(((k - 1) >> 1) & 1);
-      if (first_owner) mbar_wait_parity(bar_above + sel, par);
-      // every boundary-row thread waits (t = 0 does not read the halo, but
-      // its next write into the neighbour's halo must not overtake the
-      // neighbour's read of the previous one)
-      if (last_owner) mbar_wait_parity(bar_below + sel, par);
+    if (C > 1) {
+      // post this step's expected halo bytes (phase k>>1 of barrier k&1; the
+      // barrier's previous phase, step k-2, completed before step k-1 began)
+      if (first_owner && t == 0) mbar_expect_tx(bar_above + (unsigned)(k & 1) * 8u, 16u * S);
+      if (last_owner && t == 0) mbar_expect_tx(bar_below + (unsigned)(k & 1) * 8u, 16u * S);
+      if (k > 0) {  // halo values of step k-1 from the neighbouring bands
+        const unsigned sel = (unsigned)((k - 1) & 1) * 8u;
+        const unsigned par = (unsigned)(((k - 1) >> 1) & 1);
+        if (first_owner) mbar_wait_parity(bar_above + sel, par);
+        // every boundary-row thread waits (t = 0 does not read the halo, but
+        // its next write into the neighbour's halo must not overtake the
+        // neighbour's read of the previous one)
+        if (last_owner) mbar_wait_parity(bar_below + sel, par);
+      }
     }
     issue_next();
     const int j = k - 2 * t;
@@ -498,18 +523,12 @@ __global__ void __launch_bounds__(S * kMaxBandRows / RT, 1)
         sts2(d_w + uv_me + 16 * i, du, dv);
       }
       if (C > 1) {
-        if (ty == 0 && c > 0) {  // band's first row -> CTA c-1's row below its band
-          double* h = xuvp + ((k & 1) * S * rows + t * rows + (Hc + 1)) * 2;
-          st_cluster(h, c - 1, U);
-          st_cluster(h + 1, c - 1, V);
-          mbar_arrive_remote(bar_below + (unsigned)(k & 1) * 8u, c - 1);
-        }
-        if (ty == last_ty && c < C - 1) {  // band's last row -> CTA c+1's row above its band
-          double* h = xuvp + ((k & 1) * S * rows + t * rows) * 2;
-          st_cluster(h, c + 1, U);
-          st_cluster(h + 1, c + 1, V);
-          mbar_arrive_remote(bar_above + (unsigned)(k & 1) * 8u, c + 1);
-        }
+        if (ty == 0 && c > 0)  // band's first row -> CTA c-1's row below its band
+          st_async2(uv_w + (unsigned)((t * rows + Hc + 1) * 16), bar_below + (unsigned)(k & 1) * 8u,
+                    c - 1, U, V);
+        if (ty == last_ty && c < C - 1)  // band's last row -> CTA c+1's row above its band
+          st_async2(uv_w + (unsigned)(t * rows * 16), bar_above + (unsigned)(k & 1) * 8u, c + 1,
+                    U, V);
       }
       if (t == S - 1 && ty < nrows && x >= 0 && x < W) {
         if (du_out) {
@@ -579,6 +598,16 @@ static int choose_cluster(int B, int H, int RT) {
   while (C < 16 && (hp(C) > kMaxBandRows || hp(C) / RT * S > S * kMaxBandRows / RT ||
                     sor_smem_bytes<S>(hp(C)) > kMaxSmem))
     ++C;
+  // a band's step time scales with its rows: while the batch leaves SMs idle,
+  // split the rows further (bands of >= 32 rows; the st.async halo exchange
+  // costs ~0.15 us per step)
+  static const int sms = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
+  while (C < 16 && B * (C + 1) <= sms && (H + C) / (C + 1) >= 32) ++C;
   return C;
 }
 

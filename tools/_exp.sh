@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT
-export DIS_SOR_RT=1
-python tools/sor_bench.py 16 54 128 2 > gpurun_out/sorprof_plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_sor -s 1 -c 1 -o gpurun_out/sorprof6 -f python tools/sor_bench.py 16 54 128 2 > gpurun_out/sorprof_ncu.log 2>&1
+timeout 400 python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -2
+for i in 1 2; do timeout 60 python tools/sor_bench.py 16 436 1024 3; done
+timeout 60 python tools/sor_bench.py 64 218 512 5
+timeout 60 python tools/sor_bench.py 64 109 256 5
