@@ -22,11 +22,17 @@ struct Cover {
   bool extra;   // the clamped last origin covers too
 };
 
-__device__ __forceinline__ Cover cover_range(const GridAxis& ax, int ps, int y) {
+// floor(v / spacing) for 0 <= v < 2^20 / spacing: (v * magic) >> 20 with
+// magic = ceil(2^20 / spacing) (exact in that range)
+__device__ __forceinline__ int div_sp(int v, unsigned magic) {
+  return (int)(((unsigned long long)(unsigned)v * magic) >> 20);
+}
+
+__device__ __forceinline__ Cover cover_range(const GridAxis& ax, int ps, int y, unsigned magic) {
   Cover c;
-  int lo = y - ps + 1;
-  int j0 = lo <= 0 ? 0 : (lo + ax.spacing - 1) / ax.spacing;
-  int j1 = y / ax.spacing;
+  const int lo = y - ps + 1;
+  const int j0 = lo <= 0 ? 0 : div_sp(lo + ax.spacing - 1, magic);
+  int j1 = div_sp(y, magic);
   if (j1 > ax.nreg - 1) j1 = ax.nreg - 1;
   if (j1 < j0) j1 = j0 - 1;  // no regular origin covers y
   c.j0 = j0;
@@ -35,33 +41,33 @@ __device__ __forceinline__ Cover cover_range(const GridAxis& ax, int ps, int y) 
   return c;
 }
 
+// one thread per pixel (2D tiles of 32 x 8): covering patches in ascending
+// (grid row, grid column) order = the reference's ascending patch index
 __global__ void __launch_bounds__(256) k_densify(const double* __restrict__ ref_all,
-                                                 const double* __restrict__ qry_all, int B,
-                                                 int W, int H, GridAxis ax, GridAxis ay, int ps,
-                                                 const double* __restrict__ pu,
+                                                 const double* __restrict__ qry_all, int W,
+                                                 int H, GridAxis ax, GridAxis ay, int ps,
+                                                 unsigned magic, const double* __restrict__ pu,
                                                  const double* __restrict__ pv,
                                                  const double* __restrict__ poff,
                                                  double* __restrict__ fu, double* __restrict__ fv,
                                                  uint32_t* status) {
-  const size_t plane = (size_t)W * H;
-  const size_t n = (size_t)B * plane;
-  const int nx = ax.n;
-  const int P = nx * ay.n;
+  const int b = blockIdx.z;
+  const int x = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
   bool bad = false;
-  for (size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
-       g += (size_t)gridDim.x * blockDim.x) {
-    const int b = (int)(g / plane);
-    const size_t p = g - (size_t)b * plane;
-    const int y = (int)(p / W);
-    const int x = (int)(p - (size_t)y * W);
+  if (x < W && y < H) {
+    const size_t plane = (size_t)W * H;
+    const int nx = ax.n;
+    const int P = nx * ay.n;
+    const size_t p = (size_t)y * W + x;
     const double* __restrict__ ref = ref_all + b * plane;
     const double* __restrict__ qry = qry_all + b * plane;
     const double* __restrict__ u_ = pu + (size_t)b * P;
     const double* __restrict__ v_ = pv + (size_t)b * P;
     const double* __restrict__ o_ = poff + (size_t)b * P;
     const double r = __ldg(ref + p);
-    const Cover cy = cover_range(ay, ps, y);
-    const Cover cx = cover_range(ax, ps, x);
+    const Cover cy = cover_range(ay, ps, y, magic);
+    const Cover cx = cover_range(ax, ps, x, magic);
     double acc_u = 0.0, acc_v = 0.0, acc_w = 0.0;
     const int ny_cov = (cy.j1 - cy.j0 + 1) + (cy.extra ? 1 : 0);
     const int nx_cov = (cx.j1 - cx.j0 + 1) + (cx.extra ? 1 : 0);
@@ -81,9 +87,9 @@ __global__ void __launch_bounds__(256) k_densify(const double* __restrict__ ref_
         acc_w += wgt;
       }
     }
-    bad |= !(acc_w > 0.0);
-    fu[g] = exact_div_pos(acc_u, acc_w);  // acc_w > 0 (else flagged above)
-    fv[g] = exact_div_pos(acc_v, acc_w);
+    bad = !(acc_w > 0.0);
+    fu[b * plane + p] = exact_div_pos(acc_u, acc_w);  // acc_w > 0 (else flagged)
+    fv[b * plane + p] = exact_div_pos(acc_v, acc_w);
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) set_status(status, DIS_STATUS_COVERAGE);
 }
@@ -92,13 +98,10 @@ void launch_densify(const double* ref, const double* qry, int B, int W, int H, G
                     GridAxis ay, int ps, const double* pu, const double* pv,
                     const double* poff, double* fu, double* fv, uint32_t* status,
                     cudaStream_t st) {
-  const size_t n = (size_t)B * W * H;
-  const int TH = 256;
-  size_t blocks = (n + TH - 1) / TH;
-  if (blocks > 148 * 32) blocks = 148 * 32;
+  const unsigned magic = (unsigned)(((1u << 20) + ax.spacing - 1) / ax.spacing);
+  dim3 g((unsigned)((W + 31) / 32), (unsigned)((H + 7) / 8), (unsigned)B);
   prof_begin(KC_DENSIFY, st);
-  k_densify<<<(unsigned)blocks, TH, 0, st>>>(ref, qry, B, W, H, ax, ay, ps, pu, pv, poff, fu,
-                                             fv, status);
+  k_densify<<<g, 256, 0, st>>>(ref, qry, W, H, ax, ay, ps, magic, pu, pv, poff, fu, fv, status);
   prof_end(KC_DENSIFY, st);
   note_launch();
 }

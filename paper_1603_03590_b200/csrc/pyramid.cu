@@ -142,6 +142,125 @@ __global__ void k_gradients(const double* __restrict__ img, int B, int H, int W,
   }
 }
 
+// Tiled gradients: a 32 x 16 output tile per block.  The level image is
+// read once (tile + 2-pixel halo) into shared memory, gx / gy are evaluated
+// once for the tile + 1-pixel halo, the second derivatives come from those;
+// all outputs are written coalesced.  Identical arithmetic to RowGrad (the
+// border rules use global coordinates; halo cells outside the level are
+// never read for an in-level output).
+constexpr int kGTX = 32, kGTY = 16;
+__global__ void __launch_bounds__(256) k_gradients_tile(const double* __restrict__ img_all, int H,
+                                                        int W, double* __restrict__ gx_all,
+                                                        double* __restrict__ gy_all,
+                                                        double* __restrict__ dd_all) {
+  __shared__ double I[kGTY + 4][kGTX + 4];
+  __shared__ double GX[kGTY + 2][kGTX + 2];
+  __shared__ double GY[kGTY + 2][kGTX + 2];
+  const int b = blockIdx.z;
+  const int X0 = blockIdx.x * kGTX, Y0 = blockIdx.y * kGTY;
+  const size_t plane = (size_t)W * H;
+  const double* img = img_all + b * plane;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < (kGTY + 4) * (kGTX + 4); i += 256) {
+    const int ly = i / (kGTX + 4), lx = i - ly * (kGTX + 4);
+    int gy = Y0 - 2 + ly, gx = X0 - 2 + lx;
+    gy = gy < 0 ? 0 : (gy > H - 1 ? H - 1 : gy);
+    gx = gx < 0 ? 0 : (gx > W - 1 ? W - 1 : gx);
+    I[ly][lx] = __ldg(img + (size_t)gy * W + gx);
+  }
+  __syncthreads();
+  // gx, gy on the tile + 1 halo (local (ly, lx) <-> image (Y0-1+ly, X0-1+lx))
+  for (int i = tid; i < (kGTY + 2) * (kGTX + 2); i += 256) {
+    const int ly = i / (kGTX + 2), lx = i - ly * (kGTX + 2);
+    const int y = Y0 - 1 + ly, x = X0 - 1 + lx;
+    const int cy = ly + 1, cx = lx + 1;  // in I
+    double g;
+    if (x <= 0)
+      g = 0.5 * (I[cy][cx + 1] - I[cy][cx]);
+    else if (x >= W - 1)
+      g = 0.5 * (I[cy][cx] - I[cy][cx - 1]);
+    else
+      g = 0.5 * (I[cy][cx + 1] - I[cy][cx - 1]);
+    GX[ly][lx] = g;
+    if (y <= 0)
+      g = 0.5 * (I[cy + 1][cx] - I[cy][cx]);
+    else if (y >= H - 1)
+      g = 0.5 * (I[cy][cx] - I[cy - 1][cx]);
+    else
+      g = 0.5 * (I[cy + 1][cx] - I[cy - 1][cx]);
+    GY[ly][lx] = g;
+  }
+  __syncthreads();
+  for (int i = tid; i < kGTY * kGTX; i += 256) {
+    const int ly = i / kGTX, lx = i - ly * kGTX;
+    const int y = Y0 + ly, x = X0 + lx;
+    if (y >= H || x >= W) continue;
+    const int cy = ly + 1, cx = lx + 1;  // in GX / GY
+    const size_t o = b * plane + (size_t)y * W + x;
+    if (gx_all) gx_all[o] = GX[cy][cx];
+    if (gy_all) gy_all[o] = GY[cy][cx];
+    if (dd_all) {
+      double gxx, gxy, gyx, gyy;
+      if (x == 0) {
+        gxx = 0.5 * (GX[cy][cx + 1] - GX[cy][cx]);
+        gyx = 0.5 * (GY[cy][cx + 1] - GY[cy][cx]);
+      } else if (x == W - 1) {
+        gxx = 0.5 * (GX[cy][cx] - GX[cy][cx - 1]);
+        gyx = 0.5 * (GY[cy][cx] - GY[cy][cx - 1]);
+      } else {
+        gxx = 0.5 * (GX[cy][cx + 1] - GX[cy][cx - 1]);
+        gyx = 0.5 * (GY[cy][cx + 1] - GY[cy][cx - 1]);
+      }
+      if (y == 0) {
+        gxy = 0.5 * (GX[cy + 1][cx] - GX[cy][cx]);
+        gyy = 0.5 * (GY[cy + 1][cx] - GY[cy][cx]);
+      } else if (y == H - 1) {
+        gxy = 0.5 * (GX[cy][cx] - GX[cy - 1][cx]);
+        gyy = 0.5 * (GY[cy][cx] - GY[cy - 1][cx]);
+      } else {
+        gxy = 0.5 * (GX[cy + 1][cx] - GX[cy - 1][cx]);
+        gyy = 0.5 * (GY[cy + 1][cx] - GY[cy - 1][cx]);
+      }
+      double* d = dd_all + b * 4 * plane + (size_t)y * W + x;
+      d[0] = gxx;
+      d[plane] = gxy;
+      d[2 * plane] = gyx;
+      d[3 * plane] = gyy;
+    }
+  }
+}
+
+// level 1 straight from the frames + the finiteness check of every input
+// pixel (as_image, core.py:65-72), one pass over the frames
+template <typename T>
+__global__ void __launch_bounds__(256) k_level1_checked(const T* __restrict__ frames, int H,
+                                                        int W, double* __restrict__ out,
+                                                        uint32_t* status) {
+  const int Ho = H / 2, Wo = W / 2;
+  const int b = blockIdx.z;
+  const int X = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int Y = blockIdx.y * 8 + (threadIdx.x >> 5);
+  bool bad = false;
+  if (X < Wo && Y < Ho) {
+    const T* r0 = frames + ((size_t)b * H + 2 * Y) * W + 2 * X;
+    const T* r1 = r0 + W;
+    const double a = to_f64(r0[0]), bb = to_f64(r0[1]), c = to_f64(r1[0]), d = to_f64(r1[1]);
+    bad = !(isfinite(a) && isfinite(bb) && isfinite(c) && isfinite(d));
+    out[((size_t)b * Ho + Y) * Wo + X] = ((a + bb) + (c + d)) / 4.0;
+  }
+  // the pixels no 2x2 block covers (odd last column / row)
+  if ((W & 1) && X == Wo - 1 && Y < H / 2) {
+    bad |= !isfinite(to_f64(frames[((size_t)b * H + 2 * Y) * W + W - 1]));
+    bad |= !isfinite(to_f64(frames[((size_t)b * H + 2 * Y + 1) * W + W - 1]));
+  }
+  if ((H & 1) && Y == Ho - 1 && X < W / 2) {
+    bad |= !isfinite(to_f64(frames[((size_t)b * H + H - 1) * W + 2 * X]));
+    bad |= !isfinite(to_f64(frames[((size_t)b * H + H - 1) * W + 2 * X + 1]));
+    if ((W & 1) && X == Wo - 1) bad |= !isfinite(to_f64(frames[((size_t)b * H + H - 1) * W + W - 1]));
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) set_status(status, DIS_STATUS_NONFINITE_INPUT);
+}
+
 static inline int grid_for(size_t n, int threads) {
   size_t blocks = (n + threads - 1) / threads;
   size_t cap = 148 * 16;
@@ -156,16 +275,19 @@ static void launch_pyramid_t(const T* frames, int B, int H, int W, int coarsest,
                              double* const* dd, uint32_t* status, cudaStream_t st) {
   const int TH = 256;
   prof_begin(KC_PYRAMID, st);
-  // level 0 (and the finiteness check over every input pixel)
-  size_t n0 = (size_t)B * H * W;
-  k_level0<T><<<grid_for(n0, TH), TH, 0, st>>>(frames, B, H, W, img[0], status);
-  note_launch();
   int h = H, w = W;
+  if (img[0] != nullptr || coarsest == 0) {
+    // level 0 stored (finest scale 0): convert + check, then box-mean chain
+    const size_t n0 = (size_t)B * H * W;
+    k_level0<T><<<grid_for(n0, TH), TH, 0, st>>>(frames, B, H, W, img[0], status);
+    note_launch();
+  }
   for (int s = 1; s <= coarsest; ++s) {
-    int ho = h / 2, wo = w / 2;
-    size_t n = (size_t)B * ho * wo;
+    const int ho = h / 2, wo = w / 2;
+    const size_t n = (size_t)B * ho * wo;
     if (s == 1 && img[0] == nullptr) {
-      k_level1_from_frames<T><<<grid_for(n, TH), TH, 0, st>>>(frames, B, H, W, img[1]);
+      dim3 g((unsigned)((wo + 31) / 32), (unsigned)((ho + 7) / 8), (unsigned)B);
+      k_level1_checked<T><<<g, TH, 0, st>>>(frames, H, W, img[1], status);
     } else {
       k_downsample<<<grid_for(n, TH), TH, 0, st>>>(img[s - 1], B, h, w, img[s]);
     }
@@ -177,9 +299,8 @@ static void launch_pyramid_t(const T* frames, int B, int H, int W, int coarsest,
   w = W;
   for (int s = 0; s <= coarsest; ++s) {
     if (gx[s] || gy[s] || (dd && dd[s])) {
-      size_t n = (size_t)B * h * w;
-      k_gradients<<<grid_for(n, TH), TH, 0, st>>>(img[s], B, h, w, gx[s], gy[s],
-                                                    dd ? dd[s] : nullptr);
+      dim3 g((unsigned)((w + kGTX - 1) / kGTX), (unsigned)((h + kGTY - 1) / kGTY), (unsigned)B);
+      k_gradients_tile<<<g, 256, 0, st>>>(img[s], h, w, gx[s], gy[s], dd ? dd[s] : nullptr);
       note_launch();
     }
     h /= 2;

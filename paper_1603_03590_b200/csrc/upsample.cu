@@ -8,29 +8,41 @@
 namespace disb200 {
 
 __global__ void __launch_bounds__(256) k_upsample(const double* __restrict__ iu,
-                                                  const double* __restrict__ iv, int B, int W,
-                                                  int H, double* __restrict__ ou,
+                                                  const double* __restrict__ iv, int W, int H,
+                                                  double* __restrict__ ou,
                                                   double* __restrict__ ov,
                                                   double* __restrict__ oi, int Wn, int Hn) {
-  const size_t nplane = (size_t)Wn * Hn;
-  const size_t n = (size_t)B * nplane;
+  const int b = blockIdx.z;
+  const int x = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (x >= Wn || y >= Hn) return;
   const size_t plane = (size_t)W * H;
-  for (size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
-       g += (size_t)gridDim.x * blockDim.x) {
-    const int b = (int)(g / nplane);
-    const size_t p = g - (size_t)b * nplane;
-    const int y = (int)(p / Wn);
-    const int x = (int)(p - (size_t)y * Wn);
-    const double xs = (double)x / 2.0;
-    const double ys = (double)y / 2.0;
-    const double u = bilin_np(iu + b * plane, W, H, xs, ys) * 2.0;
-    const double v = bilin_np(iv + b * plane, W, H, xs, ys) * 2.0;
-    if (oi) {
-      reinterpret_cast<double2*>(oi)[g] = make_double2(u, v);
-    } else {
-      ou[g] = u;
-      ov[g] = v;
-    }
+  // bilinear_map (core.py:154-170) of u and v at the same coordinate: one
+  // clamp/floor/fraction setup, then the numpy formula for each component
+  double xs = (double)x / 2.0;
+  double ys = (double)y / 2.0;
+  xs = xs > W - 1.0 ? W - 1.0 : xs;
+  ys = ys > H - 1.0 ? H - 1.0 : ys;
+  const int x0 = (int)xs, y0 = (int)ys;  // xs, ys >= 0: floor
+  const int x1 = x0 + 1 < W - 1 ? x0 + 1 : W - 1;
+  const int y1 = y0 + 1 < H - 1 ? y0 + 1 : H - 1;
+  const double fx = xs - (double)x0, fy = ys - (double)y0;
+  const double gx = 1.0 - fx, gy = 1.0 - fy;
+  const double* U = iu + b * plane;
+  const double* V = iv + b * plane;
+  const size_t r0 = (size_t)y0 * W, r1 = (size_t)y1 * W;
+  const double ut = __ldg(U + r0 + x0) * gx + __ldg(U + r0 + x1) * fx;
+  const double ub = __ldg(U + r1 + x0) * gx + __ldg(U + r1 + x1) * fx;
+  const double vt = __ldg(V + r0 + x0) * gx + __ldg(V + r0 + x1) * fx;
+  const double vb = __ldg(V + r1 + x0) * gx + __ldg(V + r1 + x1) * fx;
+  const double u = (ut * gy + ub * fy) * 2.0;
+  const double v = (vt * gy + vb * fy) * 2.0;
+  const size_t g = ((size_t)b * Hn + y) * Wn + x;
+  if (oi) {
+    __stcs(reinterpret_cast<double2*>(oi) + g, make_double2(u, v));  // streamed: not re-read
+  } else {
+    ou[g] = u;
+    ov[g] = v;
   }
 }
 
@@ -50,9 +62,9 @@ static unsigned blocks_for(size_t n) {
 
 void launch_upsample(const double* iu, const double* iv, int B, int W, int H, double* ou,
                      double* ov, double* out_interleaved, int Wn, int Hn, cudaStream_t st) {
-  const size_t n = (size_t)B * Wn * Hn;
   prof_begin(KC_UPSAMPLE, st);
-  k_upsample<<<blocks_for(n), 256, 0, st>>>(iu, iv, B, W, H, ou, ov, out_interleaved, Wn, Hn);
+  dim3 g((unsigned)((Wn + 31) / 32), (unsigned)((Hn + 7) / 8), (unsigned)B);
+  k_upsample<<<g, 256, 0, st>>>(iu, iv, W, H, ou, ov, out_interleaved, Wn, Hn);
   prof_end(KC_UPSAMPLE, st);
   note_launch();
 }

@@ -46,13 +46,14 @@ size_t refine_scratch_doubles(int B, int W, int H) {
   return (size_t)(kRecords + 2) * B * Ls;  // + du/dv carry for > 8 sweeps
 }
 
-__global__ void __launch_bounds__(256) k_tensor_assemble(RefineArgs a, size_t Ls) {
+// Tile of kTTX x kTTY pixels per block: the record of each pixel is computed
+// with row-major (coalesced) reads, staged in shared memory, then written to
+// the skewed layout one diagonal run at a time (contiguous y on a diagonal).
+constexpr int kTTX = 32, kTTY = 16;
+
+__device__ __forceinline__ void pixel_record(const RefineArgs& a, int b, int x, int y,
+                                             double* r) {
   const int W = a.W, H = a.H;
-  const int y = blockIdx.x * 32 + threadIdx.x;
-  const int d = blockIdx.y * blockDim.y + threadIdx.y;
-  const int b = blockIdx.z;
-  const int x = d - y;
-  if (y >= H || x < 0 || x >= W) return;
   const size_t plane = (size_t)W * H;
   const size_t p = (size_t)y * W + x;
   const double* __restrict__ u = a.fu + b * plane;
@@ -109,11 +110,6 @@ __global__ void __launch_bounds__(256) k_tensor_assemble(RefineArgs a, size_t Ls
   const double psi_g = 0.5 / sqrt(tgzz + eps2);
   const double wi = a.delta * psi_i;
   const double wg = a.gamma * psi_g;
-  const double m00 = wi * t0xx + wg * tgxx;
-  const double m01 = wi * t0xy + wg * tgxy;
-  const double m11 = wi * t0yy + wg * tgyy;
-  const double r0 = -(wi * t0xz + wg * tgxz);
-  const double r1 = -(wi * t0yz + wg * tgyz);
   const int xm = x > 0 ? x - 1 : 0;
   const int xp = x < W - 1 ? x + 1 : W - 1;
   const int ym = y > 0 ? y - 1 : 0;
@@ -123,19 +119,47 @@ __global__ void __launch_bounds__(256) k_tensor_assemble(RefineArgs a, size_t Ls
   const double vx = 0.5 * (v[(size_t)y * W + xp] - v[(size_t)y * W + xm]);
   const double vy = 0.5 * (v[(size_t)yp * W + x] - v[(size_t)ym * W + x]);
   const double grad2 = ux * ux + uy * uy + vx * vx + vy * vy;
-  const double ws = a.alpha * 0.5 / sqrt(grad2 + eps2);
+  r[0] = up_;
+  r[1] = vp_;
+  r[2] = wi * t0xx + wg * tgxx;        // m00
+  r[3] = wi * t0xy + wg * tgxy;        // m01
+  r[4] = wi * t0yy + wg * tgyy;        // m11
+  r[5] = -(wi * t0xz + wg * tgxz);     // r0
+  r[6] = -(wi * t0yz + wg * tgyz);     // r1
+  r[7] = a.alpha * 0.5 / sqrt(grad2 + eps2);  // ws
+}
 
-  const size_t s = (size_t)d * H + y;
-  double* rec = a.rec;
+__global__ void __launch_bounds__(256, 3) k_tensor_assemble(RefineArgs a, size_t Ls) {
+  __shared__ double rs[kRecords][kTTY][kTTX + 1];
+  const int W = a.W, H = a.H;
+  const int b = blockIdx.z;
+  const int X0 = blockIdx.x * kTTX, Y0 = blockIdx.y * kTTY;
+  const int lx = threadIdx.x & 31;
+  for (int ly = threadIdx.x >> 5; ly < kTTY; ly += 8) {
+    const int x = X0 + lx, y = Y0 + ly;
+    if (x < W && y < H) {
+      double r[kRecords];
+      pixel_record(a, b, x, y, r);
+#pragma unroll
+      for (int f = 0; f < kRecords; ++f) rs[f][ly][lx] = r[f];
+    }
+  }
+  __syncthreads();
+  // write diagonal runs: diagonal d = X0 + Y0 + dd, rows y with x = d - y in
+  // the tile -> contiguous [d*H + y] in every record field
   const size_t B = (size_t)a.B;
-  rec[(0 * B + b) * Ls + s] = up_;
-  rec[(1 * B + b) * Ls + s] = vp_;
-  rec[(2 * B + b) * Ls + s] = m00;
-  rec[(3 * B + b) * Ls + s] = m01;
-  rec[(4 * B + b) * Ls + s] = m11;
-  rec[(5 * B + b) * Ls + s] = r0;
-  rec[(6 * B + b) * Ls + s] = r1;
-  rec[(7 * B + b) * Ls + s] = ws;
+  const int ndd = kTTX + kTTY - 1;
+  for (int i = threadIdx.x; i < kRecords * ndd * kTTY; i += 256) {
+    const int ly = i % kTTY;
+    const int rest = i / kTTY;
+    const int dd = rest % ndd;
+    const int f = rest / ndd;
+    const int lxx = dd - ly;
+    const int x = X0 + lxx, y = Y0 + ly;
+    if (lxx < 0 || lxx >= kTTX || x >= W || y >= H) continue;
+    const size_t d = (size_t)(x + y);
+    a.rec[(f * B + b) * Ls + d * H + y] = rs[f][ly][lxx];
+  }
 }
 
 constexpr int kLookahead = 8;  // diagonals prefetched ahead of the wavefront (covers HBM latency)
@@ -683,8 +707,8 @@ int launch_refine(const RefineArgs& a, cudaStream_t st) {
   const size_t Ls = (size_t)(a.W + a.H - 1) * a.H;
   double* carry_u = a.rec + (size_t)kRecords * a.B * Ls;
   double* carry_v = carry_u + (size_t)a.B * Ls;
-  dim3 tb(32, 8);
-  dim3 tg((a.H + 31) / 32, (a.W + a.H - 1 + 7) / 8, a.B);
+  dim3 tb(256);
+  dim3 tg((a.W + kTTX - 1) / kTTX, (a.H + kTTY - 1) / kTTY, a.B);
   for (int it = 0; it < a.outer; ++it) {
     prof_begin(KC_TENSOR, st);
     k_tensor_assemble<<<tg, tb, 0, st>>>(a, Ls);
