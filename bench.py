@@ -254,7 +254,7 @@ def run_ours(args, cfg, params):
     import torch
     import torch.distributed as dist
 
-    from paper_1603_03590_b200 import FlowEngine, _lib
+    from paper_1603_03590_b200 import FlowEngine, _lib, sharding
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -274,9 +274,7 @@ def run_ours(args, cfg, params):
     out = torch.empty((B, cfg.height, cfg.width, 2), dtype=torch.float64, device=dev)
     L = _lib.lib()
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
+    barrier = sharding.barrier
 
     # warm-up (first call checks the status word: errors surface here)
     for i in range(max(1, args.warmup)):
@@ -300,11 +298,7 @@ def run_ours(args, cfg, params):
     barrier()
     clk = clocks.stop()
     L.dis_profile_enable(0)
-    ms_total = ev0.elapsed_time(ev1)
-    ms = torch.tensor([ms_total], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms_total = float(ms.item())
+    ms_total = sharding.max_over_ranks(ev0.elapsed_time(ev1), device=dev)
     eng.check_status(stream)  # any non-finite / coverage failure raises here
     nk = len(_lib.KERNEL_CLASSES)
     kms = (ctypes.c_double * nk)()
@@ -351,10 +345,7 @@ def run_ours(args, cfg, params):
         for _ in range(e_steps):
             eng.run_host(h1, h2, out=ho, stream=stream)
         t1 = time.perf_counter()
-        et = torch.tensor([t1 - t0], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        e_s = float(et.item()) / e_steps
+        e_s = sharding.max_over_ranks(t1 - t0, device=dev) / e_steps
         assert np.array_equal(ho[0], out[0].cpu().numpy()), "host path != device path"
         e2e = {"value": world * B / e_s, "unit": UNIT,
                "h2d_bytes_per_step": int(h1.nbytes + h2.nbytes),
