@@ -82,6 +82,33 @@ def algorithmic_bytes(cfg, params, e=8):
     return b
 
 
+# Algorithmic FP64 flops, counted on the reference's formulation (one flop
+# per + - * / of inverse_search.py / variational.py; abs, compares, clamps
+# and floors not counted):
+#   patch search: precompute 7 per template sample (tsum, h00, h01, h11;
+#     inverse_search.py:89-96) per patch; one window evaluation 23 per sample
+#     (_bilin 11 incl. the two fractions + bx+ox, by+oy + the wsum add = 14;
+#     the residual pass e, mar, ssd, b0, b1 = 9; inverse_search.py:130-150);
+#   SOR: 62 per pixel update at an interior pixel (4 neighbours x 11 +
+#     den_u, val_u (4), du (4), den_v, val_v (4), dv (4);
+#     variational.py:133-165).
+SEARCH_PRE_FLOPS = 7
+SEARCH_EVAL_FLOPS = 23
+SOR_UPDATE_FLOPS = 62
+
+
+def algorithmic_flops(cfg, params, B, evals_total):
+    ss, sf, ps = params.coarsest_scale, params.finest_scale, params.patch_size
+    P = sum(grid_n(level_dims(cfg, s)[1], ps, params.overlap)
+            * grid_n(level_dims(cfg, s)[0], ps, params.overlap) for s in range(sf, ss + 1))
+    vi = params.variational.inner_sor_iters
+    sor = sum(level_dims(cfg, s)[0] * level_dims(cfg, s)[1] * vi * params.variational.outer_iters(s)
+              for s in range(sf, ss + 1))
+    return {"patch_search": B * P * SEARCH_PRE_FLOPS * ps * ps
+            + evals_total * SEARCH_EVAL_FLOPS * ps * ps,
+            "sor": B * sor * SOR_UPDATE_FLOPS}
+
+
 def measured_peak_gbs():
     path = os.path.join(REPO, "MEASURED_PEAKS.json")
     try:
@@ -164,16 +191,51 @@ def cpu_oracle_rate(cfg, params, f1, f2, cores, pairs):
 # --------------------------------------------------------------------------
 
 class ClockSampler:
+    """SM clocks and throttle reasons sampled DURING the timed region: NVML
+    (nvidia-ml-py) polled every 5 ms from a thread; nvidia-smi -lms 100 as
+    the fallback."""
+
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason* bits
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, device_index):
         self.dev = device_index
         self.rows = []
         self.proc = None
+        self.nvml = None
+        self.stop_ev = threading.Event()
 
     def start(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            bus = None
+            try:
+                import torch
+
+                bus = torch.cuda.get_device_properties(self.dev).pci_bus_id
+            except Exception:
+                pass
+            h = None
+            if bus:
+                try:
+                    h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+                except Exception:
+                    h = None
+            if h is None:
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.dev)
+            self.nvml = (pynvml, h)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.QUERY}",
@@ -185,11 +247,37 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _poll(self):
+        nv, h = self.nvml
+        while not self.stop_ev.is_set():
+            try:
+                mhz = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                try:
+                    bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except Exception:
+                    bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.rows.append((mhz, int(bits)))
+            except Exception:
+                pass
+            self.stop_ev.wait(0.005)
+
     def _read(self):
         for line in self.proc.stdout:
             self.rows.append([c.strip() for c in line.split(",")])
 
     def stop(self):
+        if self.nvml is not None:
+            self.stop_ev.set()
+            self.thread.join(timeout=2)
+            sm = [r[0] for r in self.rows]
+            reasons = sorted({name for _, bits in self.rows
+                              for bit, name in self.REASONS.items() if bits & bit})
+            if not sm:
+                return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                        "samples": 0, "source": "nvml"}
+            return {"sm_mhz": float(np.median(sm)), "sm_min_mhz": min(sm),
+                    "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(sm),
+                    "source": "nvml 5 ms"}
         if self.proc is None:
             return None
         self.proc.terminate()
@@ -211,7 +299,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi 100 ms"}
 
 
 # --------------------------------------------------------------------------
@@ -282,6 +370,20 @@ def run_ours(args, cfg, params):
     torch.cuda.synchronize(dev)
     launches_per_step = int(L.dis_last_launch_count())
 
+    # untimed census step: window evaluations of the patch search (FP64
+    # roofline numerator), and the FP64 peak of this device
+    _lib.check(L.dis_census_enable(1))
+    eng.run(f1, f2, out=out, stream=stream, check=False)
+    torch.cuda.synchronize(dev)
+    ev_n, ev_p = ctypes.c_longlong(0), ctypes.c_longlong(0)
+    _lib.check(L.dis_census_read(ctypes.byref(ev_n), ctypes.byref(ev_p)))
+    _lib.check(L.dis_census_enable(0))
+    evals_step = int(ev_n.value)
+    dadd, dmul = ctypes.c_double(0), ctypes.c_double(0)
+    _lib.check(L.dis_selftest_fp64_peak(ctypes.byref(dadd), ctypes.byref(dmul),
+                                        _lib.stream_handle(stream)))
+    fp64_peak_tflops = min(dadd.value, dmul.value) / 1e3
+
     # ---- timed region: device-resident inputs (> L2: 2 x B x H x W x 4 B) ----
     L.dis_profile_reset()
     L.dis_profile_enable(1)
@@ -310,25 +412,47 @@ def run_ours(args, cfg, params):
     ms_step = ms_total / args.steps
     value = world * B / (ms_step / 1e3)
 
-    # ---- roofline of the dominant kernel class ----
+    # ---- rooflines (each kernel class against what bounds it) ----
     per_pair = algorithmic_bytes(cfg, params)
-    dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
     peak, peak_kind = measured_peak_gbs()
+    flops = algorithmic_flops(cfg, params, B, evals_step)
+    total_ms = sum(x["ms_per_step"] for x in kernels.values())
+    for name, k in kernels.items():
+        if k["ms_per_step"] <= 0:
+            continue
+        sec = k["ms_per_step"] / 1e3
+        k["share"] = k["ms_per_step"] / max(1e-12, total_ms)
+        k["algorithmic_GBps"] = per_pair[name] * B / sec / 1e9
+        k["hbm_frac"] = k["algorithmic_GBps"] / peak
+        if name in flops:
+            k["algorithmic_TFLOPs"] = flops[name] / sec / 1e12
+            k["fp64_frac"] = k["algorithmic_TFLOPs"] / fp64_peak_tflops
+    dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
     d = kernels[dom]
     launches = max(1.0, d["launches_per_step"])
-    bytes_per_launch = per_pair[dom] * B / launches
     ms_per_launch = d["ms_per_step"] / launches
-    achieved = bytes_per_launch / (ms_per_launch / 1e3) / 1e9
-    for name in kernels:
-        k = kernels[name]
-        if k["ms_per_step"] > 0:
-            k["algorithmic_GBps"] = per_pair[name] * B / (k["ms_per_step"] / 1e3) / 1e9
-            k["share"] = k["ms_per_step"] / max(1e-12, sum(x["ms_per_step"]
-                                                           for x in kernels.values()))
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(cfg.name, dom), "peak_source": peak_kind,
-                "algorithmic_bytes_per_launch": bytes_per_launch}
+    if dom == "patch_search":
+        # FP64-bound: no stage of the patch search streams HBM (windows hit L1)
+        per_launch = flops[dom] / launches
+        achieved = per_launch / (ms_per_launch / 1e3) / 1e12
+        roofline = {"bound": "fp64", "kernel": dom, "achieved": achieved,
+                    "peak": fp64_peak_tflops, "unit": "TFLOP/s",
+                    "frac": achieved / fp64_peak_tflops,
+                    "traffic": ncu_traffic(cfg.name, dom),
+                    "peak_source": "measured live: DADD independent chains, no FMA "
+                                   "(dis_selftest_fp64_peak)",
+                    "algorithmic_flops_per_launch": per_launch,
+                    "evaluations_per_step": evals_step,
+                    "hbm_frac": d["hbm_frac"]}
+    else:
+        bytes_per_launch = per_pair[dom] * B / launches
+        achieved = bytes_per_launch / (ms_per_launch / 1e3) / 1e9
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                    "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": ncu_traffic(cfg.name, dom), "peak_source": peak_kind,
+                    "algorithmic_bytes_per_launch": bytes_per_launch}
+        if "fp64_frac" in d:
+            roofline["fp64_frac"] = d["fp64_frac"]
 
     # ---- e2e: host buffers through the C ABI (copies in the timed region) ----
     e2e = None
@@ -381,6 +505,7 @@ def run_ours(args, cfg, params):
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk, "kernels": kernels,
+            "fp64_peak": {"dadd_TFLOPs": dadd.value / 1e3, "dmul_TFLOPs": dmul.value / 1e3},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -217,6 +217,13 @@ DIS_API int dis_upsample_flow(const double* in_u, const double* in_v, int32_t B,
                       int32_t W, int32_t H, double* out_u, double* out_v,
                       int32_t Wn, int32_t Hn, void* stream);
 
+/* compose_flows (pipeline.py:186-199): out(x) = ab(x) + bc(x + ab(x)) with
+ * bc sampled by bilinear_map (core.py:154-170).  B fields, each H x W x 2
+ * float64 interleaved (u, v), device memory; `out` must not alias the
+ * inputs.  Frame chaining (cli.py chain) composes consecutive fields. */
+DIS_API int dis_compose_flows(const double* flow_ab, const double* flow_bc, int32_t B,
+                              int32_t H, int32_t W, double* flow_out, void* stream);
+
 /* Patch grid (create_grid densification.py:58-79): number of window
  * origins per axis and the origins themselves (host memory).  Returns the
  * count, or a negative status. */
@@ -234,6 +241,17 @@ DIS_API void dis_profile_enable(int32_t on);
 DIS_API void dis_profile_reset(void);
 /* Blocks on the recorded events; writes total ms and launch counts. */
 DIS_API int dis_profile_read(double* ms_out, int64_t* count_out, int32_t n_classes);
+
+/* Evaluation census (bench roofline): while on, the patch-search kernels
+ * count window evaluations and finished patches on the device; read with
+ * dis_census_read (blocking).  Turning it on resets the counters. */
+DIS_API int dis_census_enable(int32_t on);
+DIS_API int dis_census_read(long long* evals_out, long long* patches_out);
+
+/* Measured FP64 peak of this device for the roofline denominator:
+ * independent DADD and DMUL chains (no FMA, as in the exact-parity
+ * kernels) over all SMs; writes Gop/s of each. */
+DIS_API int dis_selftest_fp64_peak(double* dadd_gops, double* dmul_gops, void* stream);
 
 /* Test hook: exact_div_pos (the SOR's division) and IEEE `/` on device
  * arrays n, d -> fast, ieee (count elements). */

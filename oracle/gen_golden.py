@@ -245,9 +245,135 @@ def gen_full_hashes():
          flow_absmean=np.array([r[5] for r in rows]), flow_absmax=np.array([r[6] for r in rows]))
 
 
+def smooth_field(rng, h, w, mag, sigma=6.0):
+    from scipy.ndimage import gaussian_filter
+
+    f = np.stack([gaussian_filter(rng.standard_normal((h, w)), sigma) for _ in range(2)], -1)
+    return f * (mag / max(1e-12, np.abs(f).max()))
+
+
+def gen_compose():
+    """compose_flows (pipeline.py:186-199) on smooth fields, fields that
+    push samples outside the raster (clamping), and a 1-row field."""
+    rng = np.random.default_rng(300)
+    d = {}
+    for k, (h, w, mag) in enumerate([(37, 53, 3.0), (29, 41, 40.0), (1, 17, 5.0)]):
+        ab = smooth_field(rng, h, w, mag) if h > 1 else rng.uniform(-mag, mag, (h, w, 2))
+        bc = smooth_field(rng, h, w, mag) if h > 1 else rng.uniform(-mag, mag, (h, w, 2))
+        d[f"ab{k}"] = ab
+        d[f"bc{k}"] = bc
+        d[f"out{k}"] = pipeline.compose_flows(ab, bc)
+    save("next_compose.npz", **d)
+
+
+def _params_dict(p):
+    vp = p.variational
+    return dict(patch_size=p.patch_size, overlap=p.overlap, iterations=p.iterations,
+                finest=p.finest_scale, coarsest=p.coarsest_scale,
+                mean_norm=int(p.use_mean_normalization), norm=p.residual_norm,
+                variational=int(vp is not None),
+                outer=-1 if vp is None or not isinstance(vp, VarParamsFixed) else vp.fixed_outer,
+                bidirectional=int(p.bidirectional), mode=p.mode)
+
+
+def gen_stereo():
+    """dis_stereo (pipeline.py:166-183) end to end, and the horizontal-only
+    stages: conditioning (inverse_search.py:259-264) and SOR
+    (variational.py:161)."""
+    cases = [
+        # (seed, h, w, maxdisp, params)
+        (20, 96, 160, 6.0, dataclasses.replace(core.DisParams.preset(2, stereo=True),
+                                               coarsest_scale=3)),
+        (21, 109, 256, 10.0, core.DisParams(patch_size=12, overlap=0.75, iterations=32,
+                                            finest_scale=0, coarsest_scale=3,
+                                            variational=VarParamsFixed(fixed_outer=1),
+                                            mode="stereo")),
+        (22, 80, 128, 5.0, core.DisParams(patch_size=8, overlap=0.5, iterations=16,
+                                          finest_scale=1, coarsest_scale=3, variational=None,
+                                          mode="stereo")),
+        # flow-mode params through dis_stereo (the reference does not check mode)
+        (23, 96, 160, 6.0, core.DisParams(patch_size=8, overlap=0.5, iterations=16,
+                                          finest_scale=1, coarsest_scale=3,
+                                          variational=VarParamsFixed(fixed_outer=1))),
+    ]
+    for k, (seed, h, w, md, params) in enumerate(cases):
+        f1, f2, _ = synth.make_stereo_pair(seed, h, w, md)
+        flow = pipeline.dis_stereo(f1, f2, params)
+        save(f"next_stereo_{k}.npz", f1=f1, f2=f2, flow=flow, **_params_dict(params))
+    # horizontal SOR on the refine.npz system
+    g = np.load(os.path.join(OUT, "refine.npz"))
+    init = g["init"]
+    u = np.ascontiguousarray(init[:, :, 0])
+    v = np.ascontiguousarray(init[:, :, 1])
+    sysm = [np.ascontiguousarray(x) for x in g["sys"]]
+    du = np.zeros_like(u)
+    dv = np.zeros_like(u)
+    variational._sor_sweeps(u, v, du, dv, *sysm, 1.6, 5, True)
+    f1, f2 = g["f1"], g["f2"]
+    pyr1 = core.build_pyramid(f1, 0)
+    pyr2 = core.build_pyramid(f2, 0)
+    ref_h = variational.refine(init, pyr1[0], pyr2[0], VarParamsFixed(fixed_outer=2), 0,
+                               horizontal_only=True)
+    # horizontal conditioning on a textured level
+    pset = inverse_search.precompute_patch_set(pyr1[0], np.arange(0, 70, 5.0),
+                                               np.arange(0, 70, 5.0) * 0.5, 8,
+                                               horizontal_only=True)
+    save("next_stereo_stages.npz", sor_du=du, sor_dv=dv, refined_h=ref_h,
+         cond_valid=pset.valid, cond_hinv=pset.hessian_inv, cond_hess=pset.hessian)
+
+
+def gen_bidir():
+    """bidirectional densification: densify_bidirectional
+    (densification.py:194-234) on explicit patch sets, and dis_flow with
+    bidirectional=True end to end."""
+    rng = np.random.default_rng(400)
+    f1, f2, gt = synth.make_pair(24, 54, 128, 6.0, True, 6.0)
+    pyr1 = core.build_pyramid(f1, 0)
+    pyr2 = core.build_pyramid(f2, 0)
+    d = dict(f1=f1, f2=f2)
+    for k, (ps, ov, mag) in enumerate([(8, 0.5, 3.0), (12, 0.75, 9.0), (8, 0.3, 40.0)]):
+        fg = densification.create_grid(128, 54, ps, ov)
+        n = fg.starts.shape[0]
+        fdisp = rng.normal(0, mag, (n, 2))
+        fdisp[::7] = np.round(fdisp[::7])  # integer displacements: closed windows
+        bdisp = rng.normal(0, mag, (n, 2))
+        bdisp[::5] = np.round(bdisp[::5])
+        foff = rng.normal(0, 2, n)
+        boff = rng.normal(0, 2, n)
+        d[f"ps{k}"] = ps
+        d[f"ov{k}"] = ov
+        d[f"fdisp{k}"] = fdisp
+        d[f"bdisp{k}"] = bdisp
+        d[f"foff{k}"] = foff
+        d[f"boff{k}"] = boff
+        d[f"flow{k}"] = densification.densify_bidirectional(
+            fg, fdisp, foff, fg, bdisp, boff, pyr1[0].image, pyr2[0].image)
+    save("next_bidir_stage.npz", **d)
+    cases = [
+        (25, 109, 256, 8.0, core.DisParams(patch_size=8, overlap=0.5, iterations=32,
+                                           finest_scale=1, coarsest_scale=3,
+                                           variational=VarParamsFixed(fixed_outer=1),
+                                           bidirectional=True)),
+        (26, 96, 160, 6.0, core.DisParams(patch_size=12, overlap=0.75, iterations=64,
+                                          finest_scale=0, coarsest_scale=3,
+                                          variational=VarParamsFixed(fixed_outer=1),
+                                          bidirectional=True)),
+        (27, 80, 128, 5.0, core.DisParams(patch_size=8, overlap=0.3, iterations=16,
+                                          finest_scale=2, coarsest_scale=3, variational=None,
+                                          bidirectional=True)),
+        (28, 96, 160, 6.0, dataclasses.replace(core.DisParams.preset(2), coarsest_scale=3,
+                                               bidirectional=True)),
+    ]
+    for k, (seed, h, w, mag, params) in enumerate(cases):
+        f1, f2, _ = synth.make_pair(seed, h, w, mag, True, mag)
+        flow = pipeline.dis_flow(f1, f2, params)
+        save(f"next_bidir_{k}.npz", f1=f1, f2=f2, flow=flow, **_params_dict(params))
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    which = sys.argv[1:] or ["pyramid", "samplers", "search", "refine", "e2e", "full"]
+    which = sys.argv[1:] or ["pyramid", "samplers", "search", "refine", "e2e", "full",
+                             "compose", "stereo", "bidir"]
     pipeline.warmup()
     if "pyramid" in which:
         gen_pyramid()
@@ -261,3 +387,9 @@ if __name__ == "__main__":
         gen_e2e_small()
     if "full" in which:
         gen_full_hashes()
+    if "compose" in which:
+        gen_compose()
+    if "stereo" in which:
+        gen_stereo()
+    if "bidir" in which:
+        gen_bidir()

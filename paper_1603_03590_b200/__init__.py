@@ -15,7 +15,7 @@ from .params import (
     VarParams,
     coarsest_scale_for,
 )
-from .pipeline import FlowEngine, dis_flow, dis_flow_batch
+from .pipeline import FlowEngine, compose_flows, dis_flow, dis_flow_batch
 
 __version__ = "0.1.0"
 
@@ -27,4 +27,5 @@ __all__ = [
     "FlowEngine",
     "dis_flow",
     "dis_flow_batch",
+    "compose_flows",
 ]

@@ -33,7 +33,8 @@ EXPORTED = (
     "dis_patch_search_workspace_bytes", "dis_densify",
     "dis_refine_workspace_bytes", "dis_refine", "dis_upsample_flow", "dis_grid_axis",
     "dis_last_error", "dis_abi_version", "dis_last_launch_count", "dis_profile_enable",
-    "dis_profile_reset", "dis_profile_read", "dis_selftest_div",
+    "dis_profile_reset", "dis_profile_read", "dis_selftest_div", "dis_census_enable",
+    "dis_census_read", "dis_selftest_fp64_peak", "dis_compose_flows",
 )
 
 KERNEL_CLASSES = ("pyramid", "patch_search", "densify", "tensor_assemble", "sor", "upsample")
@@ -90,6 +91,8 @@ def lib() -> ctypes.CDLL:
     L.dis_refine.restype = ctypes.c_int
     L.dis_upsample_flow.argtypes = [_vp, _vp, _i32, _i32, _i32, _vp, _vp, _i32, _i32, _vp]
     L.dis_upsample_flow.restype = ctypes.c_int
+    L.dis_compose_flows.argtypes = [_vp, _vp, _i32, _i32, _i32, _vp, _vp]
+    L.dis_compose_flows.restype = ctypes.c_int
     L.dis_grid_axis.argtypes = [_i32, _i32, ctypes.c_double, ctypes.POINTER(_i32), _i32]
     L.dis_grid_axis.restype = _i32
     L.dis_last_error.argtypes = []
@@ -105,6 +108,14 @@ def lib() -> ctypes.CDLL:
     L.dis_profile_read.restype = ctypes.c_int
     L.dis_selftest_div.argtypes = [_vp, _vp, _vp, _vp, _sz, _vp]
     L.dis_selftest_div.restype = ctypes.c_int
+    L.dis_census_enable.argtypes = [_i32]
+    L.dis_census_enable.restype = ctypes.c_int
+    L.dis_census_read.argtypes = [ctypes.POINTER(ctypes.c_longlong),
+                                  ctypes.POINTER(ctypes.c_longlong)]
+    L.dis_census_read.restype = ctypes.c_int
+    L.dis_selftest_fp64_peak.argtypes = [ctypes.POINTER(ctypes.c_double),
+                                         ctypes.POINTER(ctypes.c_double), _vp]
+    L.dis_selftest_fp64_peak.restype = ctypes.c_int
     L.dis_abi_version.argtypes = []
     L.dis_abi_version.restype = _i32
     if L.dis_abi_version() != 1:

@@ -1,7 +1,8 @@
 // api.cu — the C ABI (include/dis_b200.h): parameter validation, workspace
 // planning and the coarse-to-fine host loop (dis_flow / _dense_scales /
 // _upscale_to_full, pipeline.py:85-163) enqueueing the sm_100a kernels on one
-// stream.  Nothing here allocates device memory; nothing synchronizes except
+// stream.  Nothing on the flow path allocates device memory (only the
+// bench-only evaluation census owns two counters); nothing synchronizes except
 // the explicitly synchronous *_host / dis_read_status entry points.
 #include <atomic>
 #include <cmath>
@@ -52,6 +53,13 @@ cudaEvent_t prof_event() {
 
 namespace disb200 {
 void note_launch(int n) { g_launches += n; }
+
+// evaluation census: while enabled, the Gauss-Newton kernels add each
+// finished patch's window-evaluation count to census[0] and 1 to census[1]
+// (bench.py's FP64 roofline of the patch search; not used when timing)
+unsigned long long* g_census = nullptr;
+bool g_census_on = false;
+unsigned long long* census_counters() { return g_census_on ? g_census : nullptr; }
 void prof_begin(int cls, cudaStream_t st) {
   std::lock_guard<std::mutex> g(g_prof_mu);
   if (!g_prof_on) return;
@@ -246,6 +254,7 @@ int run_pipeline(const Plan& pl, const dis_params_t* p, double* out, void* ws,
     a.out_u = at<double>(ws, pl.off_pu[s]);
     a.out_v = at<double>(ws, pl.off_pv[s]);
     a.out_off = at<double>(ws, pl.off_poff[s]);
+    a.census = census_counters();
     launch_patch_search(a, at<char>(ws, pl.off_search), st);
     double* fu = at<double>(ws, pl.off_fu[s]);
     double* fv = at<double>(ws, pl.off_fv[s]);
@@ -353,6 +362,26 @@ void dis_profile_reset(void) {
     g_prof_n[c] = 0;
     g_prof_open[c] = nullptr;
   }
+}
+
+int dis_census_enable(int32_t on) {
+  if (on && !g_census) {
+    if (cudaMalloc(&g_census, 2 * sizeof(unsigned long long)) != cudaSuccess)
+      return fail(DIS_ERR_CUDA, "census: cudaMalloc failed");
+  }
+  if (on && cudaMemset(g_census, 0, 2 * sizeof(unsigned long long)) != cudaSuccess)
+    return fail(DIS_ERR_CUDA, "census: cudaMemset failed");
+  g_census_on = on != 0;
+  return DIS_OK;
+}
+
+int dis_census_read(long long* evals_out, long long* patches_out) {
+  unsigned long long h[2] = {0, 0};
+  if (g_census && cudaMemcpy(h, g_census, sizeof h, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(DIS_ERR_CUDA, "census: cudaMemcpy failed");
+  *evals_out = (long long)h[0];
+  *patches_out = (long long)h[1];
+  return DIS_OK;
 }
 
 int dis_profile_read(double* ms_out, int64_t* count_out, int32_t n_classes) {
@@ -745,6 +774,24 @@ int dis_upsample_flow(const double* in_u, const double* in_v, int32_t B, int32_t
                       double* out_u, double* out_v, int32_t Wn, int32_t Hn, void* stream) {
   launch_upsample(in_u, in_v, B, W, H, out_u, out_v, nullptr, Wn, Hn, as_stream(stream));
   return check_cuda("dis_upsample_flow");
+}
+
+int dis_compose_flows(const double* flow_ab, const double* flow_bc, int32_t B, int32_t H,
+                      int32_t W, double* flow_out, void* stream) {
+  if (B < 1 || H < 1 || W < 1)
+    return fail(DIS_ERR_VALUE, "flow fields must be non-empty, got (%d, %d, %d)", B, H, W);
+  if (!flow_ab || !flow_bc || !flow_out)
+    return fail(DIS_ERR_VALUE, "compose_flows: null field pointer");
+  const size_t bytes = (size_t)B * H * W * 2 * sizeof(double);
+  auto overlap = [&](const double* a) {
+    return (const char*)a < (const char*)flow_out + bytes &&
+           (const char*)flow_out < (const char*)a + bytes;
+  };
+  if (overlap(flow_ab) || overlap(flow_bc))
+    return fail(DIS_ERR_VALUE, "compose_flows: the output must not alias an input field");
+  g_launches = 0;
+  launch_compose(flow_ab, flow_bc, B, H, W, flow_out, as_stream(stream));
+  return check_cuda("dis_compose_flows");
 }
 
 }  // extern "C"

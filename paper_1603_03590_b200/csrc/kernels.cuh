@@ -24,6 +24,8 @@ enum KernelClass {
 void prof_begin(int cls, cudaStream_t st);
 void prof_end(int cls, cudaStream_t st);
 void note_launch(int n = 1);
+// evaluation census (bench roofline): device counters or null when off
+unsigned long long* census_counters();
 
 // pyramid.cu
 void launch_pyramid(const void* frames, int dtype, int B, int H, int W, int coarsest,
@@ -51,6 +53,7 @@ struct SearchArgs {
   double* out_iv;     // optional
   uint8_t* out_valid; // optional
   int32_t* out_evals; // optional
+  unsigned long long* census;  // optional: [0] += evaluations, [1] += patches
 };
 size_t patch_search_scratch_bytes(int B, int P);
 void launch_patch_search(const SearchArgs& a, void* scratch, cudaStream_t st);
@@ -87,5 +90,9 @@ void launch_upsample(const double* iu, const double* iv, int B, int W, int H, do
                      double* ov, double* out_interleaved, int Wn, int Hn, cudaStream_t st);
 void launch_interleave(const double* u, const double* v, int B, int W, int H, double* out,
                        cudaStream_t st);
+
+// compose.cu — compose_flows (interleaved (B, H, W, 2) fields)
+void launch_compose(const double* ab, const double* bc, int B, int H, int W, double* out,
+                    cudaStream_t st);
 
 }  // namespace disb200

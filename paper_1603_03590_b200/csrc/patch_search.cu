@@ -314,6 +314,10 @@ __device__ __forceinline__ bool gn_update(Lane& L, const SearchArgs& a, int ps, 
       a.out_off[o] = off;
       if (a.out_mar) a.out_mar[o] = mar;
       if (a.out_evals) a.out_evals[o] = L.evals;
+      if (a.census) {
+        atomicAdd(a.census, (unsigned long long)L.evals);
+        atomicAdd(a.census + 1, 1ull);
+      }
     }
     L.pid = -1;
   }

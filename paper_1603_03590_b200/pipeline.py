@@ -214,3 +214,36 @@ def dis_flow(frame1, frame2, params: DisParams | None = None, threads: int = 1):
     if isinstance(frame1, torch.Tensor):
         return out
     return out.cpu().numpy()
+
+
+def compose_flows(flow_ab, flow_bc):
+    """Chain two fields (pipeline.py:186-199): out(x) = ab(x) + bc(x + ab(x)),
+    ``bc`` sampled with bilinear_map (clamped).  (H, W, 2) or a batch
+    (B, H, W, 2); numpy in -> numpy out, torch in -> torch (CUDA) out.  One
+    sm_100a kernel (compose.cu) per call."""
+    torch = _require_cuda()
+    as_torch = isinstance(flow_ab, torch.Tensor)
+    s1, s2 = tuple(flow_ab.shape), tuple(flow_bc.shape)
+    if s1 != s2:
+        raise ValueError("flow fields must share dimensions to compose")
+    if len(s1) not in (3, 4) or s1[-1] != 2:
+        raise ValueError(f"flow fields must be (H, W, 2) or (B, H, W, 2), got {s1}")
+    dev = flow_ab.device if as_torch and flow_ab.is_cuda else torch.device("cuda")
+
+    def dev64(x):
+        t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.asarray(x))
+        return t.to(device=dev, dtype=torch.float64).contiguous()
+
+    ab, bc = dev64(flow_ab), dev64(flow_bc)
+    batched = ab.dim() == 4
+    if not batched:
+        ab, bc = ab.unsqueeze(0), bc.unsqueeze(0)
+    B, H, W = ab.shape[:3]
+    out = torch.empty_like(ab)
+    if B * H * W:
+        _lib.check(_lib.lib().dis_compose_flows(
+            ab.data_ptr(), bc.data_ptr(), B, H, W, out.data_ptr(),
+            _lib.stream_handle(torch.cuda.current_stream(dev))))
+    if not batched:
+        out = out[0]
+    return out if as_torch else out.cpu().numpy()

@@ -1,5 +1,6 @@
 #!/bin/bash
-# One GPU session: parity tests, bench, ncu launch list + full captures.
+# One GPU session: smoke, parity tests, bench, ncu launch list + full capture
+# of every kernel of one pipeline step.
 # usage: tools/gpu_round.sh <tag> [config]
 set -u
 TAG=${1:-r}
@@ -8,12 +9,16 @@ OUT=gpurun_out
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > $OUT/smi_$TAG.txt 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG.log 2>&1
-timeout 1500 python -m pytest tests -m gpu -q -rfE > $OUT/pytest_gpu_$TAG.log 2>&1
+if [ "${TESTS:-1}" = "1" ]; then
+  timeout 1500 python -m pytest tests -m gpu -q -rfE > $OUT/pytest_gpu_$TAG.log 2>&1
+fi
 timeout 900 python bench.py --steps 20 --warmup 3 --config $CFG > $OUT/bench_$TAG.log 2>&1
 PROF="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --config $CFG"
 if [ "${NCU:-1}" = "1" ]; then
   $PROF > $OUT/prof_plain_$TAG.log 2>&1 && \
-  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv $PROF > $OUT/ncu_launch_$TAG.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"k_sor|k_patch_search" -s 8 -c 2 -o $OUT/prof_$TAG -f $PROF > $OUT/ncu_full_$TAG.log 2>&1
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv $PROF > $OUT/ncu_launch_$TAG.log 2>&1
+  # one full pipeline step (the second warm-up step) — every kernel once
+  NL=$(python -c "import json,sys; d=json.loads(open('$OUT/prof_plain_$TAG.log').read().strip().splitlines()[-1]); print(int(d['gpu_launches']))")
+  ncu --set full --clock-control none --import-source on -k regex:"^k_" -s $NL -c $NL -o $OUT/full_$TAG -f $PROF > $OUT/ncu_full_$TAG.log 2>&1
 fi
 echo finished

@@ -130,6 +130,25 @@ def make_pair(seed: int, h: int, w: int, maxmag: float, rects: bool, rmax: float
     return f1, f2.astype(np.float32), np.stack([u, v], axis=-1)
 
 
+def make_stereo_pair(seed: int, h: int, w: int, maxdisp: float, rects: bool = True):
+    """A rectified pair for dis_stereo: frame2 = frame1 warped by a smooth
+    horizontal displacement (plus fronto-parallel rectangles), v = 0, + N(0, 2).
+    Returns (left, right, gt_u) with right(x + u(x)) ~ left(x)."""
+    rng = np.random.default_rng(seed)
+    f1 = texture(rng, h, w)
+    u = gaussian_filter(rng.standard_normal((h, w)), 20.0)
+    u *= maxdisp / max(1e-12, np.abs(u).max())
+    if rects:
+        for _ in range(int(rng.integers(2, 5))):
+            bw = int(rng.integers(max(2, w // 8), max(3, w // 3)))
+            bh = int(rng.integers(max(2, h // 8), max(3, h // 3)))
+            x0 = int(rng.integers(0, w - bw))
+            y0 = int(rng.integers(0, h - bh))
+            u[y0:y0 + bh, x0:x0 + bw] = rng.uniform(-maxdisp, maxdisp)
+    f2 = warp(f1, u, np.zeros_like(u)) + rng.normal(0.0, 2.0, (h, w))
+    return f1, f2.astype(np.float32), u
+
+
 def make_stream(seed: int, h: int, w: int, n_frames: int, maxmag: float, rmax: float):
     """c4: frames k+1 = warp(clean_k, flow_k) + N(0,2); flow_k blends two
     smooth fields (t = k/(n-1)) plus rectangles.  Returns (n, h, w) f32."""
