@@ -80,8 +80,12 @@ extern "C" {
  *  - outer_iters_fixed: > 0 overrides VarParams.outer_iters(s) = s + 1
  *    (core.py:212-213) with a constant (BASELINE configs use 1);
  *    <= 0 keeps the reference rule.
- *  - mode/bidirectional are carried for validation only: this path
- *    implements mode "flow" with bidirectional = 0 (pipeline.py:136-163).
+ *  - mode: 0 "flow", 1 "stereo".  dis_flow_batch rejects stereo-mode
+ *    parameters like dis_flow_on_pyramids (pipeline.py:141-142);
+ *    dis_stereo_batch runs horizontal-only search and refinement with either
+ *    mode (pipeline.py:166-183).
+ *  - bidirectional: forward and backward searches merged by
+ *    densify_bidirectional at every scale (pipeline.py:97-124).
  */
 typedef struct dis_params_t {
   int32_t patch_size;            /* theta_ps                          */
@@ -102,8 +106,8 @@ typedef struct dis_params_t {
   double var_penalizer_eps;
   double var_sor_omega;
   int32_t outer_iters_fixed;     /* extension, see above              */
-  int32_t mode;                  /* 0 flow, 1 stereo (rejected here)  */
-  int32_t bidirectional;         /* must be 0 on this path            */
+  int32_t mode;                  /* 0 flow, 1 stereo                  */
+  int32_t bidirectional;         /* densify_bidirectional per scale   */
   int32_t reserved;
 } dis_params_t;
 
@@ -111,8 +115,7 @@ typedef struct dis_params_t {
 DIS_API void dis_params_default(dis_params_t* p);
 
 /* DisParams.validate + VarParams.validate (core.py:296-316, 215-223) plus
- * this path's own restrictions (downscale == 2, mode flow, no
- * bidirectional). */
+ * this path's own restriction downscale == 2. */
 DIS_API int dis_params_validate(const dis_params_t* p);
 
 /* Workspace bytes for dis_flow_batch on B pairs of H x W frames. */
@@ -134,6 +137,15 @@ DIS_API int dis_flow_batch(const void* frame1, const void* frame2, int32_t dtype
                    double* flow_out, void* workspace, size_t workspace_bytes,
                    void* stream);
 
+/* dis_stereo (pipeline.py:166-183) for a batch of rectified pairs: the
+ * same pipeline with horizontal-only conditioning (inverse_search.py:
+ * 259-264) and SOR (variational.py:161); v comes out identically 0.  Same
+ * arguments and workspace as dis_flow_batch. */
+DIS_API int dis_stereo_batch(const void* left, const void* right, int32_t dtype,
+                             int32_t B, int32_t H, int32_t W, const dis_params_t* p,
+                             double* flow_out, void* workspace, size_t workspace_bytes,
+                             void* stream);
+
 /* Workspace bytes for dis_flow_batch_host (adds device staging for the
  * frames and the flow). */
 DIS_API size_t dis_host_workspace_bytes(int32_t B, int32_t H, int32_t W, int32_t dtype,
@@ -147,6 +159,28 @@ DIS_API int dis_flow_batch_host(const void* host_frame1, const void* host_frame2
                         int32_t dtype, int32_t B, int32_t H, int32_t W,
                         const dis_params_t* p, double* host_flow_out,
                         void* workspace, size_t workspace_bytes, void* stream);
+
+/* Host-buffer dis_stereo_batch (same contract as dis_flow_batch_host). */
+DIS_API int dis_stereo_batch_host(const void* host_left, const void* host_right,
+                                  int32_t dtype, int32_t B, int32_t H, int32_t W,
+                                  const dis_params_t* p, double* host_flow_out,
+                                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* sparse_correspondences (pipeline.py:230-287) for one pair: displacements
+ * at `n_seeds` seed locations (host (n, 2) x, y in full-resolution pixels)
+ * -> host (n, 2) displacements and (n) validity flags.  Seeds outside the
+ * image are invalid with (0, 0).  use_densification: the unrefined dense
+ * field of the finest scale sampled at the seeds; otherwise one patch chain
+ * per seed down the scales (_sparse_chain 202-227).  Frames on the device;
+ * synchronous (returns after the results reached the host). */
+DIS_API size_t dis_sparse_workspace_bytes(int32_t H, int32_t W, int32_t n_seeds,
+                                          const dis_params_t* p);
+DIS_API int dis_sparse_correspondences(const void* frame1, const void* frame2,
+                                       int32_t dtype, int32_t H, int32_t W,
+                                       const dis_params_t* p, const double* host_seeds,
+                                       int32_t n_seeds, double* host_disp_out,
+                                       uint8_t* host_valid_out, void* workspace,
+                                       size_t workspace_bytes, void* stream);
 
 /* Copy the status word out of the workspace (blocking on `stream`). */
 DIS_API int dis_read_status(const void* workspace, uint32_t* status_out, void* stream);
@@ -173,7 +207,8 @@ DIS_API int dis_build_pyramid(const void* frames, int32_t dtype, int32_t B, int3
                       double* const* levels_dd, uint32_t* status, void* stream);
 
 /* init_patches + precompute_patch_set + optimize_patch_set + reset_outliers
- * + refresh_patch_stats for one scale (pipeline.py:54-82).
+ * + refresh_patch_stats for one scale (pipeline.py:54-82).  p->mode == 1
+ * selects the horizontal_only conditioning (stereo).
  *   ref_img/ref_gx/ref_gy/qry_img : level s, B x H x W
  *   coarse_flow_u/v : level s+1 flow (B x Hc x Wc) or NULL (zeros)
  *   out_u/out_v/out_off/out_mar : B x P_s, P_s in grid row-major order
@@ -198,10 +233,28 @@ DIS_API int dis_densify(const double* ref_img, const double* qry_img, int32_t B,
                 const double* patch_off, double* flow_u, double* flow_v,
                 uint32_t* status, void* stream);
 
+/* densify_bidirectional (densification.py:194-234): forward patches (on
+ * ref_img, grid of the level) merged with the negated backward patches (on
+ * qry_img, same grid) whose displaced windows cover each pixel
+ * (_accumulate_backward 131-153); per-pixel sums in ascending patch index.
+ * The workspace holds the backward windows' tile bins. */
+DIS_API size_t dis_densify_bidirectional_workspace_bytes(int32_t B, int32_t W, int32_t H,
+                                                         const dis_params_t* p);
+DIS_API int dis_densify_bidirectional(const double* ref_img, const double* qry_img,
+                                      int32_t B, int32_t W, int32_t H,
+                                      const dis_params_t* p, const double* fwd_u,
+                                      const double* fwd_v, const double* fwd_off,
+                                      const double* bwd_u, const double* bwd_v,
+                                      const double* bwd_off, double* flow_u,
+                                      double* flow_v, void* workspace,
+                                      size_t workspace_bytes, uint32_t* status,
+                                      void* stream);
+
 /* Workspace for dis_refine on one level. */
 DIS_API size_t dis_refine_workspace_bytes(int32_t B, int32_t W, int32_t H);
 
-/* refine (variational.py:220-275) in place on flow_u/flow_v, running
+/* refine (variational.py:220-275) in place on flow_u/flow_v (p->mode == 1:
+ * horizontal_only), running
  * `outer_iters` fixed-point iterations (pass params->outer_iters_fixed or
  * scale_index + 1).  ref_dd/qry_dd: 4 rasters each (gxx, gxy, gyx, gyy). */
 DIS_API int dis_refine(const double* ref_img, const double* ref_gx, const double* ref_gy,

@@ -370,10 +370,87 @@ def gen_bidir():
         save(f"next_bidir_{k}.npz", f1=f1, f2=f2, flow=flow, **_params_dict(params))
 
 
+def gen_sparse():
+    """sparse_correspondences (pipeline.py:230-287): densified and per-seed
+    chain modes; seeds inside, on the border, fractional and outside."""
+    f1, f2, _ = synth.make_pair(29, 109, 256, 8.0, True, 8.0)
+    rng = np.random.default_rng(500)
+    seeds = np.concatenate([
+        rng.uniform([0, 0], [255, 108], (40, 2)),
+        np.array([[0.0, 0.0], [255.0, 108.0], [255.0, 0.0], [0.0, 108.0], [3.5, 100.25],
+                  [-0.5, 10.0], [256.0, 5.0], [10.0, -1e-9], [10.0, 108.5]]),
+    ])
+    cases = {
+        "dense": core.DisParams(patch_size=8, overlap=0.5, iterations=32, finest_scale=1,
+                                coarsest_scale=3, variational=VarParamsFixed(fixed_outer=1)),
+        "chain": core.DisParams(patch_size=8, overlap=0.5, iterations=32, finest_scale=1,
+                                coarsest_scale=3, use_densification=False),
+        "chain_s0": core.DisParams(patch_size=12, overlap=0.75, iterations=64, finest_scale=0,
+                                   coarsest_scale=3, use_densification=False),
+        "dense_bidir": core.DisParams(patch_size=8, overlap=0.3, iterations=16,
+                                      finest_scale=2, coarsest_scale=3, variational=None,
+                                      bidirectional=True),
+    }
+    d = dict(f1=f1, f2=f2, seeds=seeds)
+    for name, p in cases.items():
+        m = pipeline.sparse_correspondences(f1, f2, seeds, p)
+        d[f"{name}_disp"] = np.array([mm.displacement for mm in m])
+        d[f"{name}_valid"] = np.array([mm.valid for mm in m])
+        d[f"{name}_seed"] = np.array([mm.seed for mm in m])
+        for k, v in _params_dict(p).items():
+            d[f"{name}_{k}"] = v
+        d[f"{name}_dens"] = int(p.use_densification)
+    save("next_sparse.npz", **d)
+
+
+def gen_flowio():
+    """flowio.py: .flo bytes written by the reference, images decoded by it
+    (P5 8/16-bit with header comments, P6 luminance), written PGM/PPM bytes."""
+    import tempfile
+
+    from disflow import flowio
+
+    rng = np.random.default_rng(600)
+    d = {}
+    flow = rng.normal(0, 5, (7, 11, 2))
+    flow[2, 3] = [1e10, 1e10]  # sentinel passes through
+    with tempfile.TemporaryDirectory() as td:
+        fp = os.path.join(td, "a.flo")
+        flowio.write_flo(flow, fp)
+        d["flo_in"] = flow
+        d["flo_bytes"] = np.frombuffer(open(fp, "rb").read(), dtype=np.uint8)
+        d["flo_read"] = flowio.read_flo(fp)
+        pgm8 = rng.integers(0, 256, (9, 13), dtype=np.uint8)
+        raw = b"P5\n# a comment\n13 9\n# another\n255\n" + pgm8.tobytes()
+        d["pgm8_bytes"] = np.frombuffer(raw, dtype=np.uint8)
+        open(os.path.join(td, "a.pgm"), "wb").write(raw)
+        d["pgm8_img"] = flowio.read_image(os.path.join(td, "a.pgm"))
+        pgm16 = rng.integers(0, 1000, (5, 6)).astype(">u2")
+        raw = b"P5 6 5 999\n" + pgm16.tobytes()
+        d["pgm16_bytes"] = np.frombuffer(raw, dtype=np.uint8)
+        open(os.path.join(td, "b.pgm"), "wb").write(raw)
+        d["pgm16_img"] = flowio.read_image(os.path.join(td, "b.pgm"))
+        ppm = rng.integers(0, 256, (4, 5, 3), dtype=np.uint8)
+        raw = b"P6\n5 4\n255\n" + ppm.tobytes()
+        d["ppm_bytes"] = np.frombuffer(raw, dtype=np.uint8)
+        open(os.path.join(td, "c.ppm"), "wb").write(raw)
+        d["ppm_img"] = flowio.read_image(os.path.join(td, "c.ppm"))
+        img = rng.uniform(-20, 280, (6, 8))
+        flowio.write_image(img, os.path.join(td, "d.pgm"))
+        d["wimg_in"] = img
+        d["wimg_bytes"] = np.frombuffer(open(os.path.join(td, "d.pgm"), "rb").read(), np.uint8)
+        rgb = rng.uniform(0, 255, (3, 4, 3))
+        flowio.write_image(rgb, os.path.join(td, "e.ppm"))
+        d["wrgb_in"] = rgb
+        d["wrgb_bytes"] = np.frombuffer(open(os.path.join(td, "e.ppm"), "rb").read(), np.uint8)
+        d["mask"] = flowio.flow_valid_mask(flow)
+    save("next_flowio.npz", **d)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     which = sys.argv[1:] or ["pyramid", "samplers", "search", "refine", "e2e", "full",
-                             "compose", "stereo", "bidir"]
+                             "compose", "stereo", "bidir", "sparse", "flowio"]
     pipeline.warmup()
     if "pyramid" in which:
         gen_pyramid()
@@ -393,3 +470,7 @@ if __name__ == "__main__":
         gen_stereo()
     if "bidir" in which:
         gen_bidir()
+    if "sparse" in which:
+        gen_sparse()
+    if "flowio" in which:
+        gen_flowio()

@@ -15,7 +15,16 @@ from .params import (
     VarParams,
     coarsest_scale_for,
 )
-from .pipeline import FlowEngine, compose_flows, dis_flow, dis_flow_batch
+from .pipeline import (
+    FlowEngine,
+    SparseMatch,
+    compose_flows,
+    dis_flow,
+    dis_flow_batch,
+    dis_stereo,
+    dis_stereo_batch,
+    sparse_correspondences,
+)
 
 __version__ = "0.1.0"
 
@@ -28,4 +37,8 @@ __all__ = [
     "dis_flow",
     "dis_flow_batch",
     "compose_flows",
+    "dis_stereo",
+    "dis_stereo_batch",
+    "sparse_correspondences",
+    "SparseMatch",
 ]

@@ -34,7 +34,10 @@ EXPORTED = (
     "dis_refine_workspace_bytes", "dis_refine", "dis_upsample_flow", "dis_grid_axis",
     "dis_last_error", "dis_abi_version", "dis_last_launch_count", "dis_profile_enable",
     "dis_profile_reset", "dis_profile_read", "dis_selftest_div", "dis_census_enable",
-    "dis_census_read", "dis_selftest_fp64_peak", "dis_compose_flows",
+    "dis_census_read", "dis_selftest_fp64_peak", "dis_compose_flows", "dis_stereo_batch",
+    "dis_stereo_batch_host", "dis_densify_bidirectional",
+    "dis_densify_bidirectional_workspace_bytes", "dis_sparse_workspace_bytes",
+    "dis_sparse_correspondences",
 )
 
 KERNEL_CLASSES = ("pyramid", "patch_search", "densify", "tensor_assemble", "sor", "upsample")
@@ -91,6 +94,20 @@ def lib() -> ctypes.CDLL:
     L.dis_refine.restype = ctypes.c_int
     L.dis_upsample_flow.argtypes = [_vp, _vp, _i32, _i32, _i32, _vp, _vp, _i32, _i32, _vp]
     L.dis_upsample_flow.restype = ctypes.c_int
+    L.dis_stereo_batch.argtypes = L.dis_flow_batch.argtypes
+    L.dis_stereo_batch.restype = ctypes.c_int
+    L.dis_stereo_batch_host.argtypes = L.dis_flow_batch_host.argtypes
+    L.dis_stereo_batch_host.restype = ctypes.c_int
+    L.dis_densify_bidirectional_workspace_bytes.argtypes = [_i32, _i32, _i32, _pp]
+    L.dis_densify_bidirectional_workspace_bytes.restype = _sz
+    L.dis_densify_bidirectional.argtypes = [_vp, _vp, _i32, _i32, _i32, _pp] + [_vp] * 8 + [
+        _sz, _vp, _vp]
+    L.dis_densify_bidirectional.restype = ctypes.c_int
+    L.dis_sparse_workspace_bytes.argtypes = [_i32, _i32, _i32, _pp]
+    L.dis_sparse_workspace_bytes.restype = _sz
+    L.dis_sparse_correspondences.argtypes = [_vp, _vp, _i32, _i32, _i32, _pp, _vp, _i32, _vp,
+                                             _vp, _vp, _sz, _vp]
+    L.dis_sparse_correspondences.restype = ctypes.c_int
     L.dis_compose_flows.argtypes = [_vp, _vp, _i32, _i32, _i32, _vp, _vp]
     L.dis_compose_flows.restype = ctypes.c_int
     L.dis_grid_axis.argtypes = [_i32, _i32, ctypes.c_double, ctypes.POINTER(_i32), _i32]

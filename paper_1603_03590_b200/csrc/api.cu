@@ -110,6 +110,10 @@ struct Plan {
   size_t off_img[2][32], off_gx[2][32], off_gy[2][32], off_dd[2][32];
   size_t off_pu[32], off_pv[32], off_poff[32];
   size_t off_fu[32], off_fv[32];
+  bool bidir;
+  size_t off_bpu[32], off_bpv[32], off_bpoff[32];  // backward patches (bidirectional)
+  size_t off_bfu[32], off_bfv[32];                 // backward dense flows
+  size_t off_bin;                                  // backward-window bins
   size_t off_rec;
   size_t off_search;
   size_t total;
@@ -131,6 +135,7 @@ void make_plan(const dis_params_t* p, int B, int H, int W, Plan* pl) {
   pl->sf = p->finest_scale;
   pl->ps = p->patch_size;
   pl->var = p->variational != 0;
+  pl->bidir = p->bidirectional != 0;
   const int sp = grid_spacing(p->patch_size, p->overlap);
   for (int s = 0; s <= pl->ss; ++s) {
     pl->hs[s] = H >> s;
@@ -169,6 +174,25 @@ void make_plan(const dis_params_t* p, int B, int H, int W, Plan* pl) {
     const size_t n = (size_t)B * H * W;
     pl->off_fu[0] = take(cur, n * d);
     pl->off_fv[0] = take(cur, n * d);
+  }
+  pl->off_bin = kNone;
+  for (int s = 0; s < 32; ++s)
+    pl->off_bpu[s] = pl->off_bpv[s] = pl->off_bpoff[s] = pl->off_bfu[s] = pl->off_bfv[s] = kNone;
+  if (pl->bidir) {
+    size_t mx = 0;
+    for (int s = pl->sf; s <= pl->ss; ++s) {
+      const int P = pl->ax[s].n * pl->ay[s].n;
+      const size_t Pb = (size_t)B * P;
+      pl->off_bpu[s] = take(cur, Pb * d);
+      pl->off_bpv[s] = take(cur, Pb * d);
+      pl->off_bpoff[s] = take(cur, Pb * d);
+      const size_t n = (size_t)B * pl->hs[s] * pl->ws[s];
+      pl->off_bfu[s] = take(cur, n * d);
+      pl->off_bfv[s] = take(cur, n * d);
+      size_t r = bidir_scratch_bytes(B, pl->ws[s], pl->hs[s], P, pl->ps);
+      if (r > mx) mx = r;
+    }
+    pl->off_bin = take(cur, mx);
   }
   {
     size_t mx = 0;
@@ -222,76 +246,124 @@ int check_dims(const dis_params_t* p, int B, int H, int W) {
   return DIS_OK;
 }
 
-int run_pipeline(const Plan& pl, const dis_params_t* p, double* out, void* ws,
-                 cudaStream_t st) {
+// one direction's _ScaleState.search (pipeline.py:54-82) on level s
+void search_scale(const Plan& pl, const dis_params_t* p, void* ws, int s, int dir, bool stereo,
+                  const double* coarse_u, const double* coarse_v, int wc, int hc,
+                  double* pu, double* pv, double* poff, cudaStream_t st) {
+  SearchArgs a{};
+  a.ref = at<double>(ws, pl.off_img[dir][s]);
+  a.rgx = at<double>(ws, pl.off_gx[dir][s]);
+  a.rgy = at<double>(ws, pl.off_gy[dir][s]);
+  a.qry = at<double>(ws, pl.off_img[1 - dir][s]);
+  a.B = pl.B;
+  a.W = pl.ws[s];
+  a.H = pl.hs[s];
+  a.cu = coarse_u;
+  a.cv = coarse_v;
+  a.Wc = wc;
+  a.Hc = hc;
+  a.ax = pl.ax[s];
+  a.ay = pl.ay[s];
+  a.ps = pl.ps;
+  a.iters = p->iterations;
+  a.mean_norm = p->use_mean_normalization;
+  a.code = p->residual_norm;
+  a.hb = p->huber_b;
+  a.out_u = pu;
+  a.out_v = pv;
+  a.out_off = poff;
+  a.census = census_counters();
+  a.horizontal = stereo ? 1 : 0;
+  launch_patch_search(a, at<char>(ws, pl.off_search), st);
+}
+
+// refine (variational.py:220-275) of one direction's field on level s
+int refine_scale(const Plan& pl, const dis_params_t* p, void* ws, int s, int dir, bool stereo,
+                 double* fu, double* fv, cudaStream_t st) {
+  RefineArgs r{};
+  r.ref = at<double>(ws, pl.off_img[dir][s]);
+  r.rgx = at<double>(ws, pl.off_gx[dir][s]);
+  r.rgy = at<double>(ws, pl.off_gy[dir][s]);
+  r.rdd = at<double>(ws, pl.off_dd[dir][s]);
+  r.qry = at<double>(ws, pl.off_img[1 - dir][s]);
+  r.qgx = at<double>(ws, pl.off_gx[1 - dir][s]);
+  r.qgy = at<double>(ws, pl.off_gy[1 - dir][s]);
+  r.qdd = at<double>(ws, pl.off_dd[1 - dir][s]);
+  r.B = pl.B;
+  r.W = pl.ws[s];
+  r.H = pl.hs[s];
+  r.delta = p->var_intensity_weight;
+  r.gamma = p->var_gradient_weight;
+  r.alpha = p->var_smoothness_weight;
+  r.eps = p->var_penalizer_eps;
+  r.omega = p->var_sor_omega;
+  r.sweeps = p->var_inner_sor_iters;
+  r.outer = p->outer_iters_fixed > 0 ? p->outer_iters_fixed : s + 1;
+  r.horizontal = stereo ? 1 : 0;
+  r.fu = fu;
+  r.fv = fv;
+  r.rec = at<double>(ws, pl.off_rec);
+  r.status = at<uint32_t>(ws, pl.off_status);
+  int rc = launch_refine(r, st);
+  if (rc) return fail(rc, "refine: level %d (%dx%d) unsupported", s, pl.ws[s], pl.hs[s]);
+  return DIS_OK;
+}
+
+// _dense_scales (pipeline.py:85-126) + _upscale_to_full (129-133)
+int run_pipeline(const Plan& pl, const dis_params_t* p, double* out, void* ws, cudaStream_t st,
+                 bool stereo, bool upscale = true) {
   uint32_t* status = at<uint32_t>(ws, pl.off_status);
   double* prev_u = nullptr;
   double* prev_v = nullptr;
+  double* bprev_u = nullptr;  // backward state's flow (bidirectional)
+  double* bprev_v = nullptr;
   int prev_w = 0, prev_h = 0;
   for (int s = pl.ss; s >= pl.sf; --s) {
     const int h = pl.hs[s], w = pl.ws[s];
     double* ref = at<double>(ws, pl.off_img[0][s]);
     double* qry = at<double>(ws, pl.off_img[1][s]);
-    SearchArgs a{};
-    a.ref = ref;
-    a.rgx = at<double>(ws, pl.off_gx[0][s]);
-    a.rgy = at<double>(ws, pl.off_gy[0][s]);
-    a.qry = qry;
-    a.B = pl.B;
-    a.W = w;
-    a.H = h;
-    a.cu = prev_u;
-    a.cv = prev_v;
-    a.Wc = prev_w;
-    a.Hc = prev_h;
-    a.ax = pl.ax[s];
-    a.ay = pl.ay[s];
-    a.ps = pl.ps;
-    a.iters = p->iterations;
-    a.mean_norm = p->use_mean_normalization;
-    a.code = p->residual_norm;
-    a.hb = p->huber_b;
-    a.out_u = at<double>(ws, pl.off_pu[s]);
-    a.out_v = at<double>(ws, pl.off_pv[s]);
-    a.out_off = at<double>(ws, pl.off_poff[s]);
-    a.census = census_counters();
-    launch_patch_search(a, at<char>(ws, pl.off_search), st);
+    double* pu = at<double>(ws, pl.off_pu[s]);
+    double* pv = at<double>(ws, pl.off_pv[s]);
+    double* poff = at<double>(ws, pl.off_poff[s]);
+    search_scale(pl, p, ws, s, 0, stereo, prev_u, prev_v, prev_w, prev_h, pu, pv, poff, st);
     double* fu = at<double>(ws, pl.off_fu[s]);
     double* fv = at<double>(ws, pl.off_fv[s]);
-    launch_densify(ref, qry, pl.B, w, h, pl.ax[s], pl.ay[s], pl.ps, a.out_u, a.out_v,
-                   a.out_off, fu, fv, status, st);
+    double* bfu = nullptr;
+    double* bfv = nullptr;
+    if (!pl.bidir) {
+      launch_densify(ref, qry, pl.B, w, h, pl.ax[s], pl.ay[s], pl.ps, pu, pv, poff, fu, fv,
+                     status, st);
+    } else {
+      double* bpu = at<double>(ws, pl.off_bpu[s]);
+      double* bpv = at<double>(ws, pl.off_bpv[s]);
+      double* bpoff = at<double>(ws, pl.off_bpoff[s]);
+      search_scale(pl, p, ws, s, 1, stereo, bprev_u, bprev_v, prev_w, prev_h, bpu, bpv, bpoff,
+                   st);
+      bfu = at<double>(ws, pl.off_bfu[s]);
+      bfv = at<double>(ws, pl.off_bfv[s]);
+      void* bins = at<char>(ws, pl.off_bin);
+      // densification.py:194-234, both directions (pipeline.py:102-113)
+      launch_densify_bidir(ref, qry, pl.B, w, h, pl.ax[s], pl.ay[s], pl.ps, pu, pv, poff, bpu,
+                           bpv, bpoff, fu, fv, bins, status, st);
+      launch_densify_bidir(qry, ref, pl.B, w, h, pl.ax[s], pl.ay[s], pl.ps, bpu, bpv, bpoff, pu,
+                           pv, poff, bfu, bfv, bins, status, st);
+    }
     if (pl.var) {
-      RefineArgs r{};
-      r.ref = ref;
-      r.rgx = a.rgx;
-      r.rgy = a.rgy;
-      r.rdd = at<double>(ws, pl.off_dd[0][s]);
-      r.qry = qry;
-      r.qgx = at<double>(ws, pl.off_gx[1][s]);
-      r.qgy = at<double>(ws, pl.off_gy[1][s]);
-      r.qdd = at<double>(ws, pl.off_dd[1][s]);
-      r.B = pl.B;
-      r.W = w;
-      r.H = h;
-      r.delta = p->var_intensity_weight;
-      r.gamma = p->var_gradient_weight;
-      r.alpha = p->var_smoothness_weight;
-      r.eps = p->var_penalizer_eps;
-      r.omega = p->var_sor_omega;
-      r.sweeps = p->var_inner_sor_iters;
-      r.outer = p->outer_iters_fixed > 0 ? p->outer_iters_fixed : s + 1;
-      r.fu = fu;
-      r.fv = fv;
-      r.rec = at<double>(ws, pl.off_rec);
-      r.status = status;
-      int rc = launch_refine(r, st);
-      if (rc) return fail(rc, "refine: level %d (%dx%d) unsupported", s, w, h);
+      int rc = refine_scale(pl, p, ws, s, 0, stereo, fu, fv, st);
+      if (rc) return rc;
+      if (pl.bidir) {
+        rc = refine_scale(pl, p, ws, s, 1, stereo, bfu, bfv, st);
+        if (rc) return rc;
+      }
     }
     prev_u = fu;
     prev_v = fv;
+    bprev_u = bfu;
+    bprev_v = bfv;
     prev_w = w;
     prev_h = h;
   }
+  if (!upscale) return check_cuda("dense_scales");  // the finest scale's field stays in ws
   // _upscale_to_full (pipeline.py:129-133)
   if (pl.sf == 0) {
     launch_interleave(prev_u, prev_v, pl.B, pl.W, pl.H, out, st);
@@ -455,9 +527,6 @@ int dis_params_validate(const dis_params_t* p) {
     if (!(p->var_sor_omega > 0.0 && p->var_sor_omega < 2.0))
       return fail(DIS_ERR_PARAMETER, "sor_omega must lie in (0, 2)");
   }
-  if (p->mode == 1) return fail(DIS_ERR_VALUE, "use dis_stereo for stereo-mode parameters");
-  if (p->bidirectional)
-    return fail(DIS_ERR_PARAMETER, "bidirectional densification is not implemented by this path");
   return DIS_OK;
 }
 
@@ -507,11 +576,20 @@ size_t dis_host_workspace_bytes(int32_t B, int32_t H, int32_t W, int32_t dtype,
   return per ? per * n : 0;
 }
 
-int dis_flow_batch(const void* frame1, const void* frame2, int32_t dtype, int32_t B, int32_t H,
-                   int32_t W, const dis_params_t* p, double* flow_out, void* workspace,
-                   size_t workspace_bytes, void* stream) {
+}  // extern "C"
+
+namespace {
+// dis_flow / dis_stereo on a batch (pipeline.py:150-183): validation, pyramids,
+// _dense_scales, _upscale_to_full — all enqueued on `stream`.
+int flow_batch_impl(const void* frame1, const void* frame2, int32_t dtype, int32_t B, int32_t H,
+                    int32_t W, const dis_params_t* p, double* flow_out, void* workspace,
+                    size_t workspace_bytes, void* stream, bool stereo) {
   int rc = dis_params_validate(p);
   if (rc) return rc;
+  // dis_flow_on_pyramids rejects stereo-mode parameters (pipeline.py:141-142);
+  // dis_stereo takes either mode (pipeline.py:172-180)
+  if (!stereo && p->mode == 1)
+    return fail(DIS_ERR_VALUE, "use dis_stereo for stereo-mode parameters");
   if (dtype < 0 || dtype > 2) return fail(DIS_ERR_VALUE, "unsupported frame dtype %d", dtype);
   rc = check_dims(p, B, H, W);
   if (rc) return rc;
@@ -526,7 +604,28 @@ int dis_flow_batch(const void* frame1, const void* frame2, int32_t dtype, int32_
   build_pyramids(pl, frame1, frame2, dtype, workspace, st);
   rc = check_cuda("pyramid");
   if (rc) return rc;
-  return run_pipeline(pl, p, flow_out, workspace, st);
+  return run_pipeline(pl, p, flow_out, workspace, st, stereo);
+}
+
+int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dtype, int32_t B,
+                    int32_t H, int32_t W, const dis_params_t* p, double* host_flow_out,
+                    void* workspace, size_t workspace_bytes, void* stream, bool stereo);
+}  // namespace
+
+extern "C" {
+
+int dis_flow_batch(const void* frame1, const void* frame2, int32_t dtype, int32_t B, int32_t H,
+                   int32_t W, const dis_params_t* p, double* flow_out, void* workspace,
+                   size_t workspace_bytes, void* stream) {
+  return flow_batch_impl(frame1, frame2, dtype, B, H, W, p, flow_out, workspace,
+                         workspace_bytes, stream, false);
+}
+
+int dis_stereo_batch(const void* left, const void* right, int32_t dtype, int32_t B, int32_t H,
+                     int32_t W, const dis_params_t* p, double* flow_out, void* workspace,
+                     size_t workspace_bytes, void* stream) {
+  return flow_batch_impl(left, right, dtype, B, H, W, p, flow_out, workspace, workspace_bytes,
+                         stream, true);
 }
 
 int dis_read_status(const void* workspace, uint32_t* status_out, void* stream) {
@@ -552,8 +651,28 @@ int dis_flow_batch_host(const void* host_frame1, const void* host_frame2, int32_
                         int32_t B, int32_t H, int32_t W, const dis_params_t* p,
                         double* host_flow_out, void* workspace, size_t workspace_bytes,
                         void* stream) {
+  return host_batch_impl(host_frame1, host_frame2, dtype, B, H, W, p, host_flow_out, workspace,
+                         workspace_bytes, stream, false);
+}
+
+int dis_stereo_batch_host(const void* host_left, const void* host_right, int32_t dtype,
+                          int32_t B, int32_t H, int32_t W, const dis_params_t* p,
+                          double* host_flow_out, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  return host_batch_impl(host_left, host_right, dtype, B, H, W, p, host_flow_out, workspace,
+                         workspace_bytes, stream, true);
+}
+
+}  // extern "C"
+
+namespace {
+int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dtype, int32_t B,
+                    int32_t H, int32_t W, const dis_params_t* p, double* host_flow_out,
+                    void* workspace, size_t workspace_bytes, void* stream, bool stereo) {
   int rc = dis_params_validate(p);
   if (rc) return rc;
+  if (!stereo && p->mode == 1)
+    return fail(DIS_ERR_VALUE, "use dis_stereo for stereo-mode parameters");
   if (dtype < 0 || dtype > 2) return fail(DIS_ERR_VALUE, "unsupported frame dtype %d", dtype);
   rc = check_dims(p, B, H, W);
   if (rc) return rc;
@@ -601,7 +720,7 @@ int dis_flow_batch_host(const void* host_frame1, const void* host_frame2, int32_
                     cudaMemcpyHostToDevice, cs);
     cudaMemcpyAsync(d2, static_cast<const char*>(host_frame2) + (size_t)b0 * px * esz, fbytes,
                     cudaMemcpyHostToDevice, cs);
-    rc = dis_flow_batch(d1, d2, dtype, bn, H, W, p, dout, wsc, pl.total, cs);
+    rc = flow_batch_impl(d1, d2, dtype, bn, H, W, p, dout, wsc, pl.total, cs, stereo);
     if (rc) return rc;
     launches += g_launches.load();
     cudaMemcpyAsync(host_flow_out + (size_t)b0 * px * 2, dout, obytes, cudaMemcpyDeviceToHost,
@@ -622,6 +741,9 @@ int dis_flow_batch_host(const void* host_frame1, const void* host_frame2, int32_
   }
   return dis_status_to_error(any);
 }
+}  // namespace
+
+extern "C" {
 
 // ---- stage entry points -----------------------------------------------------
 
@@ -708,6 +830,7 @@ int dis_patch_search(const double* ref_img, const double* ref_gx, const double* 
   a.out_iu = out_init_u;
   a.out_iv = out_init_v;
   a.out_valid = out_valid;
+  a.horizontal = p->mode == 1;  // horizontal_only (inverse_search.py:259-264)
   launch_patch_search(a, workspace, as_stream(stream));
   return check_cuda("dis_patch_search");
 }
@@ -725,6 +848,158 @@ int dis_densify(const double* ref_img, const double* qry_img, int32_t B, int32_t
                  make_axis(H, p->patch_size, sp), p->patch_size, patch_u, patch_v, patch_off,
                  flow_u, flow_v, status, as_stream(stream));
   return check_cuda("dis_densify");
+}
+
+// ---- sparse correspondences (pipeline.py:202-287) --------------------------
+}  // extern "C"
+namespace {
+struct SparsePlan {
+  dis_params_t q;  // params with refinement off (refine=False, pipeline.py:266-268)
+  Plan pl;
+  size_t off_seeds, off_valid, off_out, off_scratch, total;
+};
+void make_sparse_plan(const dis_params_t* p, int H, int W, int n, SparsePlan* sp) {
+  sp->q = *p;
+  sp->q.variational = 0;
+  make_plan(&sp->q, 1, H, W, &sp->pl);
+  size_t cur = sp->pl.total;
+  const size_t nn = (size_t)(n > 0 ? n : 1);
+  sp->off_seeds = take(cur, nn * 2 * sizeof(double));
+  sp->off_valid = take(cur, nn);
+  sp->off_out = take(cur, nn * 2 * sizeof(double));
+  sp->off_scratch =
+      take(cur, nn * 3 * (size_t)p->patch_size * p->patch_size * sizeof(double));
+  sp->total = (cur + 255) & ~size_t(255);
+}
+}  // namespace
+extern "C" {
+
+size_t dis_sparse_workspace_bytes(int32_t H, int32_t W, int32_t n_seeds, const dis_params_t* p) {
+  if (dis_params_validate(p) || n_seeds < 0) return 0;
+  dis_params_t q = *p;
+  q.variational = 0;
+  if (check_dims(&q, 1, H, W)) return 0;
+  SparsePlan sp;
+  make_sparse_plan(p, H, W, n_seeds, &sp);
+  return sp.total;
+}
+
+int dis_sparse_correspondences(const void* frame1, const void* frame2, int32_t dtype,
+                               int32_t H, int32_t W, const dis_params_t* p,
+                               const double* host_seeds, int32_t n_seeds,
+                               double* host_disp_out, uint8_t* host_valid_out, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  int rc = dis_params_validate(p);
+  if (rc) return rc;
+  if (dtype < 0 || dtype > 2) return fail(DIS_ERR_VALUE, "unsupported frame dtype %d", dtype);
+  if (n_seeds < 0) return fail(DIS_ERR_VALUE, "negative seed count");
+  dis_params_t q = *p;
+  q.variational = 0;
+  rc = check_dims(&q, 1, H, W);  // as_image / _check_pair / _check_levels
+  if (rc) return rc;
+  SparsePlan sp;
+  make_sparse_plan(p, H, W, n_seeds, &sp);
+  if (workspace_bytes < sp.total)
+    return fail(DIS_ERR_WORKSPACE, "workspace holds %zu bytes, need %zu", workspace_bytes,
+                sp.total);
+  // in-bounds test (pipeline.py:257-261); out-of-bounds seeds are (0, 0), invalid
+  std::vector<uint8_t> valid((size_t)n_seeds);
+  int ngood = 0;
+  for (int i = 0; i < n_seeds; ++i) {
+    const double x = host_seeds[2 * i], y = host_seeds[2 * i + 1];
+    valid[i] = (x >= 0) && (x <= W - 1) && (y >= 0) && (y <= H - 1);
+    ngood += valid[i];
+    host_disp_out[2 * i] = host_disp_out[2 * i + 1] = 0.0;
+    host_valid_out[i] = valid[i];
+  }
+  g_launches = 0;
+  if (!ngood) return DIS_OK;  // the reference skips the pyramid descent
+  cudaStream_t st = as_stream(stream);
+  const Plan& pl = sp.pl;
+  double* d_seeds = at<double>(workspace, sp.off_seeds);
+  uint8_t* d_valid = at<uint8_t>(workspace, sp.off_valid);
+  double* d_out = at<double>(workspace, sp.off_out);
+  cudaMemsetAsync(at<char>(workspace, pl.off_status), 0, 256, st);
+  cudaMemcpyAsync(d_seeds, host_seeds, (size_t)n_seeds * 2 * sizeof(double),
+                  cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d_valid, valid.data(), (size_t)n_seeds, cudaMemcpyHostToDevice, st);
+  cudaMemsetAsync(d_out, 0, (size_t)n_seeds * 2 * sizeof(double), st);
+  build_pyramids(pl, frame1, frame2, dtype, workspace, st);
+  rc = check_cuda("pyramid");
+  if (rc) return rc;
+  if (p->use_densification) {
+    rc = run_pipeline(pl, &sp.q, nullptr, workspace, st, false, false);
+    if (rc) return rc;
+    const int sf = pl.sf;
+    launch_sparse_sample(at<double>(workspace, pl.off_fu[sf]), at<double>(workspace, pl.off_fv[sf]),
+                         pl.ws[sf], pl.hs[sf], sf, d_seeds, d_valid, n_seeds, d_out, st);
+  } else {
+    SparseChainArgs a{};
+    for (int s = 0; s <= pl.ss; ++s) {
+      a.img[s] = at<double>(workspace, pl.off_img[0][s]);
+      a.gx[s] = at<double>(workspace, pl.off_gx[0][s]);
+      a.gy[s] = at<double>(workspace, pl.off_gy[0][s]);
+      a.qry[s] = at<double>(workspace, pl.off_img[1][s]);
+      a.W[s] = pl.ws[s];
+      a.H[s] = pl.hs[s];
+    }
+    a.coarsest = pl.ss;
+    a.finest = pl.sf;
+    a.ps = p->patch_size;
+    a.iters = p->iterations;
+    a.mean_norm = p->use_mean_normalization;
+    a.code = p->residual_norm;
+    a.hb = p->huber_b;
+    a.seeds = d_seeds;
+    a.valid = d_valid;
+    a.n = n_seeds;
+    a.scratch = at<double>(workspace, sp.off_scratch);
+    a.out = d_out;
+    launch_sparse_chain(a, st);
+  }
+  rc = check_cuda("dis_sparse_correspondences");
+  if (rc) return rc;
+  cudaMemcpyAsync(host_disp_out, d_out, (size_t)n_seeds * 2 * sizeof(double),
+                  cudaMemcpyDeviceToHost, st);
+  uint32_t status = 0;
+  cudaMemcpyAsync(&status, at<char>(workspace, pl.off_status), sizeof status,
+                  cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess)
+    return fail(DIS_ERR_CUDA, "dis_sparse_correspondences: %s", cudaGetErrorString(e));
+  rc = dis_status_to_error(status);
+  if (rc) {
+    for (int i = 0; i < 2 * n_seeds; ++i) host_disp_out[i] = 0.0;
+  }
+  return rc;
+}
+
+size_t dis_densify_bidirectional_workspace_bytes(int32_t B, int32_t W, int32_t H,
+                                                 const dis_params_t* p) {
+  if (dis_params_validate(p) || W < p->patch_size || H < p->patch_size) return 0;
+  const int sp = grid_spacing(p->patch_size, p->overlap);
+  const int P = make_axis(W, p->patch_size, sp).n * make_axis(H, p->patch_size, sp).n;
+  return bidir_scratch_bytes(B, W, H, P, p->patch_size);
+}
+
+int dis_densify_bidirectional(const double* ref_img, const double* qry_img, int32_t B,
+                              int32_t W, int32_t H, const dis_params_t* p,
+                              const double* fwd_u, const double* fwd_v, const double* fwd_off,
+                              const double* bwd_u, const double* bwd_v, const double* bwd_off,
+                              double* flow_u, double* flow_v, void* workspace,
+                              size_t workspace_bytes, uint32_t* status, void* stream) {
+  if (dis_params_validate(p)) return DIS_ERR_PARAMETER;
+  if (W < p->patch_size || H < p->patch_size)
+    return fail(DIS_ERR_VALUE, "level %dx%d is smaller than the patch size %d", W, H,
+                p->patch_size);
+  if (workspace_bytes < dis_densify_bidirectional_workspace_bytes(B, W, H, p))
+    return fail(DIS_ERR_WORKSPACE, "bidirectional densify workspace too small");
+  const int sp = grid_spacing(p->patch_size, p->overlap);
+  launch_densify_bidir(ref_img, qry_img, B, W, H, make_axis(W, p->patch_size, sp),
+                       make_axis(H, p->patch_size, sp), p->patch_size, fwd_u, fwd_v, fwd_off,
+                       bwd_u, bwd_v, bwd_off, flow_u, flow_v, workspace, status,
+                       as_stream(stream));
+  return check_cuda("dis_densify_bidirectional");
 }
 
 size_t dis_refine_workspace_bytes(int32_t B, int32_t W, int32_t H) {
@@ -761,6 +1036,7 @@ int dis_refine(const double* ref_img, const double* ref_gx, const double* ref_gy
   r.omega = p->var_sor_omega;
   r.sweeps = p->var_inner_sor_iters;
   r.outer = outer_iters;
+  r.horizontal = p->mode == 1;  // horizontal_only (variational.py:161)
   r.fu = flow_u;
   r.fv = flow_v;
   r.rec = static_cast<double*>(workspace);

@@ -54,6 +54,7 @@ struct SearchArgs {
   uint8_t* out_valid; // optional
   int32_t* out_evals; // optional
   unsigned long long* census;  // optional: [0] += evaluations, [1] += patches
+  int horizontal;     // stereo: _condition_hessians horizontal_only (259-264)
 };
 size_t patch_search_scratch_bytes(int B, int P);
 void launch_patch_search(const SearchArgs& a, void* scratch, cudaStream_t st);
@@ -63,6 +64,15 @@ void launch_densify(const double* ref, const double* qry, int B, int W, int H, G
                     GridAxis ay, int ps, const double* pu, const double* pv,
                     const double* poff, double* fu, double* fv, uint32_t* status,
                     cudaStream_t st);
+
+// densify.cu — bidirectional merge (densify_bidirectional): forward set
+// gathered per pixel, backward set binned by window tile
+size_t bidir_scratch_bytes(int B, int W, int H, int P, int ps);
+void launch_densify_bidir(const double* ref, const double* qry, int B, int W, int H,
+                          GridAxis ax, GridAxis ay, int ps, const double* fu_p,
+                          const double* fv_p, const double* foff_p, const double* bu_p,
+                          const double* bv_p, const double* boff_p, double* fu, double* fv,
+                          void* scratch, uint32_t* status, cudaStream_t st);
 
 // variational.cu
 struct RefineArgs {
@@ -77,6 +87,7 @@ struct RefineArgs {
   int B, W, H;
   double delta, gamma, alpha, eps, omega;
   int sweeps, outer;
+  int horizontal;  // stereo: _sor_sweeps horizontal_only (variational.py:161)
   double* fu;  // flow, row-major planar, refined in place
   double* fv;
   double* rec;  // 8 * B * (W + H - 1) * H doubles of scratch
@@ -90,6 +101,26 @@ void launch_upsample(const double* iu, const double* iv, int B, int W, int H, do
                      double* ov, double* out_interleaved, int Wn, int Hn, cudaStream_t st);
 void launch_interleave(const double* u, const double* v, int B, int W, int H, double* out,
                        cudaStream_t st);
+
+// sparse.cu — sparse_correspondences (pipeline.py:202-287)
+struct SparseChainArgs {
+  const double* img[32];
+  const double* gx[32];
+  const double* gy[32];
+  const double* qry[32];
+  int W[32], H[32];
+  int coarsest, finest, ps, iters, mean_norm, code;
+  double hb;
+  const double* seeds;   // (n, 2) device
+  const uint8_t* valid;  // (n) device
+  int n;
+  double* scratch;       // n * 3 * ps^2 doubles
+  double* out;           // (n, 2)
+};
+void launch_sparse_chain(const SparseChainArgs& a, cudaStream_t st);
+void launch_sparse_sample(const double* fu, const double* fv, int W, int H, int finest,
+                          const double* seeds, const uint8_t* valid, int n, double* out,
+                          cudaStream_t st);
 
 // compose.cu — compose_flows (interleaved (B, H, W, 2) fields)
 void launch_compose(const double* ab, const double* bc, int B, int H, int W, double* out,

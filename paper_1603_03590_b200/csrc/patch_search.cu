@@ -32,20 +32,6 @@
 
 namespace disb200 {
 
-// _transform_residual, inverse_search.py:61-72
-__device__ __forceinline__ double transform_residual(double e, int code, double b) {
-  if (code == DIS_NORM_L1) {
-    double r = sqrt(fabs(e));
-    return e >= 0.0 ? r : -r;
-  }
-  if (code == DIS_NORM_HUBER) {
-    if (fabs(e) < b) return e;
-    double r = sqrt(2.0 * b * fabs(e) - b * b);
-    return e >= 0.0 ? r : -r;
-  }
-  return e;
-}
-
 // reset_outliers' test np.hypot(du, dv) > ps (densification.py:104),
 // decided exactly for a correctly rounded hypot: sqrt(a^2 + b^2) compared
 // with the rounding midpoint ps + ulp(ps)/2 in double-double.  (glibc's
@@ -127,6 +113,20 @@ __global__ void __launch_bounds__(128) k_patch_prep(SearchArgs a, double* __rest
   const double mean_t = exact_div_pos(tsum, dn);
 
   // ---- _condition_hessians (inverse_search.py:255-276) ----
+  if (a.horizontal) {  // horizontal_only (259-264): valid = h00 > 1e-6, hinv = [1/h00, 0, 0]
+    const bool hv = h00 > 1e-6;
+    prep[PR_U0 * N + gid] = u0;
+    prep[PR_V0 * N + gid] = v0;
+    prep[PR_MEAN * N + gid] = mean_t;
+    prep[PR_I00 * N + gid] = hv ? 1.0 / h00 : 0.0;
+    prep[PR_I01 * N + gid] = 0.0;
+    prep[PR_I11 * N + gid] = 0.0;
+    prep[PR_VALID * N + gid] = hv ? 1.0 : 0.0;
+    if (a.out_iu) a.out_iu[gid] = u0;
+    if (a.out_iv) a.out_iv[gid] = v0;
+    if (a.out_valid) a.out_valid[gid] = hv ? 1 : 0;
+    return;
+  }
   const double tr = h00 + h11;
   const double det = h00 * h11 - h01 * h01;
   const double q = 0.25 * tr * tr;

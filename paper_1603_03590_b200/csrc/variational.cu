@@ -284,7 +284,7 @@ __device__ __forceinline__ void lds2(unsigned a, double& x, double& y) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(a) : "memory");
 }
 
-template <int S, int RT>
+template <int S, int RT, bool HZ>
 __global__ void __launch_bounds__(S * kMaxBandRows / RT, 1)
     k_sor(const double* __restrict__ rec, int B, int W, int H, int Hc, size_t Ls, double omega,
           const double* du_in, const double* dv_in, double* du_out, double* dv_out,
@@ -517,16 +517,19 @@ __global__ void __launch_bounds__(S * kMaxBandRows / RT, 1)
       dU[i] = den_uA[i] > 1e-12 ? nu : dU[i];
       nV[i] = r1svA[i] - m01A[i] * dU[i];
     }
-    // Phase C: v quotients
-    slow = false;
+    // Phase C: v quotients (none in stereo mode: horizontal_only skips the
+    // dv update, variational.py:161)
+    if (!HZ) {
+      slow = false;
 #pragma unroll
-    for (int i = 0; i < RT; ++i) {
-      slow = slow | ((den_vA[i] > 1e-12) & !div_fast_ok(nV[i], den_vA[i]));
-      mV[i] = div_fast_rn(nV[i], den_vA[i]);
-    }
-    if (slow) {
+      for (int i = 0; i < RT; ++i) {
+        slow = slow | ((den_vA[i] > 1e-12) & !div_fast_ok(nV[i], den_vA[i]));
+        mV[i] = div_fast_rn(nV[i], den_vA[i]);
+      }
+      if (slow) {
 #pragma unroll
-      for (int i = 0; i < RT; ++i) mV[i] = exact_div_pos(nV[i], den_vA[i]);
+        for (int i = 0; i < RT; ++i) mV[i] = exact_div_pos(nV[i], den_vA[i]);
+      }
     }
     // Phase D: updates, exchange stores, halo, output
 #pragma unroll
@@ -534,10 +537,13 @@ __global__ void __launch_bounds__(S * kMaxBandRows / RT, 1)
       const int ty = ty0 + i;
       const int y = y0 + ty;
       const int x = xk - i;
-      const double q = nV[i] == 0.0 ? nV[i] : mV[i];
-      const double nv = om1 * dV[i] + omega * q;
+      double dv = dV[i];
+      if (!HZ) {
+        const double q = nV[i] == 0.0 ? nV[i] : mV[i];
+        const double nv = om1 * dV[i] + omega * q;
+        dv = den_vA[i] > 1e-12 ? nv : dV[i];
+      }
       const double du = dU[i];
-      const double dv = den_vA[i] > 1e-12 ? nv : dV[i];
       const double U = ucA[i] + du, V = vcA[i] + dv;
       lU[i] = U;
       lV[i] = V;
@@ -635,7 +641,7 @@ static int choose_cluster(int B, int H, int RT) {
   return C;
 }
 
-template <int S, int RT>
+template <int S, int RT, bool HZ>
 static int launch_sor_rt(const RefineArgs& a, size_t Ls, const double* dui, const double* dvi,
                          double* duo, double* dvo, bool final_pass, cudaStream_t st) {
   const int C = choose_cluster<S>(a.B, a.H, RT);
@@ -647,9 +653,9 @@ static int launch_sor_rt(const RefineArgs& a, size_t Ls, const double* dui, cons
   if (hp > kMaxBandRows || smem > kMaxSmem) return DIS_ERR_VALUE;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_sor<S, RT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_sor<S, RT, HZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kMaxSmem);
-    cudaFuncSetAttribute(k_sor<S, RT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_sor<S, RT, HZ>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -666,7 +672,7 @@ static int launch_sor_rt(const RefineArgs& a, size_t Ls, const double* dui, cons
   cfg.numAttrs = 1;
   double* fu = final_pass ? a.fu : nullptr;
   double* fv = final_pass ? a.fv : nullptr;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_sor<S, RT>, (const double*)a.rec, a.B, a.W, a.H,
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_sor<S, RT, HZ>, (const double*)a.rec, a.B, a.W, a.H,
                                      Hc, Ls, a.omega, dui, dvi, duo, dvo, fu, fv, a.status);
   return e == cudaSuccess ? DIS_OK : DIS_ERR_CUDA;
 }
@@ -674,11 +680,13 @@ static int launch_sor_rt(const RefineArgs& a, size_t Ls, const double* dui, cons
 template <int S>
 static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const double* dvi,
                         double* duo, double* dvo, bool final_pass, cudaStream_t st) {
+  // stereo (horizontal_only): one row per thread
+  if (a.horizontal) return launch_sor_rt<S, 1, true>(a, Ls, dui, dvi, duo, dvo, final_pass, st);
   // more than 5 sweeps: the per-row shared memory grows, keep one row per thread
   const int rt = S > 5 ? 1 : sor_rows_per_thread();
-  if (rt == 4) return launch_sor_rt<S, 4>(a, Ls, dui, dvi, duo, dvo, final_pass, st);
-  if (rt == 2) return launch_sor_rt<S, 2>(a, Ls, dui, dvi, duo, dvo, final_pass, st);
-  return launch_sor_rt<S, 1>(a, Ls, dui, dvi, duo, dvo, final_pass, st);
+  if (rt == 4) return launch_sor_rt<S, 4, false>(a, Ls, dui, dvi, duo, dvo, final_pass, st);
+  if (rt == 2) return launch_sor_rt<S, 2, false>(a, Ls, dui, dvi, duo, dvo, final_pass, st);
+  return launch_sor_rt<S, 1, false>(a, Ls, dui, dvi, duo, dvo, final_pass, st);
 }
 
 static int launch_sor(const RefineArgs& a, size_t Ls, int S, const double* dui,

@@ -12,6 +12,7 @@ library these functions raise.
 from __future__ import annotations
 
 import ctypes
+from typing import NamedTuple
 
 import numpy as np
 
@@ -70,11 +71,14 @@ class FlowEngine:
     ``dis_workspace_bytes``)."""
 
     def __init__(self, batch: int, height: int, width: int, params: DisParams | None = None,
-                 device=None):
+                 device=None, stereo: bool = False):
         torch = _require_cuda()
-        self.params = params if params is not None else DisParams.preset(2)
+        self.stereo = bool(stereo)
+        if params is None:
+            params = DisParams.preset(2, stereo=self.stereo)
+        self.params = params
         self.params.validate()
-        if self.params.mode == "stereo":
+        if self.params.mode == "stereo" and not self.stereo:
             raise ValueError("use dis_stereo for stereo-mode parameters")
         self.B, self.H, self.W = int(batch), int(height), int(width)
         self.device = torch.device(device) if device is not None else torch.device("cuda")
@@ -112,7 +116,9 @@ class FlowEngine:
         if out is None:
             out = torch.empty((self.B, self.H, self.W, 2), dtype=torch.float64,
                               device=self.device)
-        rc = _lib.lib().dis_flow_batch(
+        L = _lib.lib()
+        fn = L.dis_stereo_batch if self.stereo else L.dis_flow_batch
+        rc = fn(
             f1.data_ptr(), f2.data_ptr(), _dtype_code(f1), self.B, self.H, self.W,
             ctypes.byref(self.cparams), out.data_ptr(), self.workspace.data_ptr(),
             self.workspace_bytes, _lib.stream_handle(stream))
@@ -147,10 +153,10 @@ class FlowEngine:
             self._host_ws = torch.empty(int(n), dtype=torch.uint8, device=self.device)
         if out is None:
             out = np.empty((self.B, self.H, self.W, 2), dtype=np.float64)
-        rc = L.dis_flow_batch_host(a.ctypes.data, b.ctypes.data, code, self.B, self.H, self.W,
-                                   ctypes.byref(self.cparams), out.ctypes.data,
-                                   self._host_ws.data_ptr(), int(n),
-                                   _lib.stream_handle(stream))
+        fn = L.dis_stereo_batch_host if self.stereo else L.dis_flow_batch_host
+        rc = fn(a.ctypes.data, b.ctypes.data, code, self.B, self.H, self.W,
+                ctypes.byref(self.cparams), out.ctypes.data, self._host_ws.data_ptr(), int(n),
+                _lib.stream_handle(stream))
         _lib.check(rc)
         return out
 
@@ -158,13 +164,13 @@ class FlowEngine:
 _ENGINES: dict = {}
 
 
-def _engine(B, H, W, params):
-    key = (B, H, W, params)
+def _engine(B, H, W, params, stereo=False):
+    key = (B, H, W, params, stereo)
     eng = _ENGINES.get(key)
     if eng is None:
         if len(_ENGINES) > 8:
             _ENGINES.clear()
-        eng = FlowEngine(B, H, W, params)
+        eng = FlowEngine(B, H, W, params, stereo=stereo)
         _ENGINES[key] = eng
     return eng
 
@@ -214,6 +220,94 @@ def dis_flow(frame1, frame2, params: DisParams | None = None, threads: int = 1):
     if isinstance(frame1, torch.Tensor):
         return out
     return out.cpu().numpy()
+
+
+def dis_stereo(left, right, params: DisParams | None = None, threads: int = 1):
+    """Horizontal-only displacement between a rectified pair
+    (pipeline.py:166-183): flow-style field, sampling ``right`` at x + u(x)
+    matches ``left`` at x; the v channel is identically zero.  numpy in ->
+    numpy out, torch in -> torch (CUDA) out."""
+    torch = _require_cuda()
+    params = params if params is not None else DisParams.preset(2, stereo=True)
+    params.validate()
+    _check_frame(left)
+    _check_frame(right)
+    if tuple(left.shape) != tuple(right.shape):
+        raise ValueError(
+            f"frame dimensions differ: {tuple(left.shape)[::-1]} vs "
+            f"{tuple(right.shape)[::-1]}")
+    h, w = left.shape
+    out = _engine(1, int(h), int(w), params, stereo=True).run(left, right)[0]
+    if isinstance(left, torch.Tensor):
+        return out
+    return out.cpu().numpy()
+
+
+def dis_stereo_batch(left, right, params: DisParams | None = None):
+    """dis_stereo for a batch of independent rectified pairs: (B, H, W) ->
+    (B, H, W, 2) float64 CUDA tensor."""
+    _require_cuda()
+    params = params if params is not None else DisParams.preset(2, stereo=True)
+    s1, s2 = tuple(left.shape), tuple(right.shape)
+    if len(s1) != 3:
+        raise ValueError(f"frame batch must be (B, H, W), got {s1}")
+    if s1 != s2:
+        raise ValueError(f"frame dimensions differ: {s1[:0:-1]} vs {s2[:0:-1]}")
+    return _engine(s1[0], s1[1], s1[2], params, stereo=True).run(left, right)
+
+
+class SparseMatch(NamedTuple):
+    """One seed's result (pipeline.py:24-27)."""
+
+    seed: tuple[float, float]
+    displacement: tuple[float, float]
+    valid: bool
+
+
+def sparse_correspondences(frame1, frame2, seeds, params: DisParams | None = None,
+                           threads: int = 1) -> list[SparseMatch]:
+    """Displacements at seed locations only, in full-resolution pixels
+    (pipeline.py:230-287).  With densification the seeds read the unrefined
+    dense field of the finest computed scale; without it every seed runs its
+    own patch chain down the scales.  Seeds outside the image come back
+    flagged invalid.  One C-ABI call (dis_sparse_correspondences)."""
+    torch = _require_cuda()
+    params = params if params is not None else DisParams.preset(2)
+    params.validate()
+    _check_frame(frame1)
+    _check_frame(frame2)
+    if tuple(frame1.shape) != tuple(frame2.shape):
+        raise ValueError(
+            f"frame dimensions differ: {tuple(frame1.shape)[::-1]} vs "
+            f"{tuple(frame2.shape)[::-1]}")
+    seed_arr = np.ascontiguousarray(np.atleast_2d(np.asarray(seeds, dtype=np.float64)))
+    if seed_arr.ndim != 2 or seed_arr.shape[1] != 2:
+        raise ValueError(f"seeds must be (n, 2) x, y pairs, got shape {seed_arr.shape}")
+    n = seed_arr.shape[0]
+    h, w = (int(d) for d in frame1.shape)
+    dev = torch.device("cuda")
+    f1 = _to_device_frames(frame1, dev)
+    f2 = _to_device_frames(frame2, dev)
+    if f2.dtype != f1.dtype:
+        f2 = f2.to(f1.dtype)
+    cp = to_c(params)
+    L = _lib.lib()
+    nbytes = int(L.dis_sparse_workspace_bytes(h, w, n, ctypes.byref(cp)))
+    if nbytes == 0:  # re-run the checks through the entry point to raise the precise error
+        _lib.check(L.dis_sparse_correspondences(None, None, _dtype_code(f1), h, w,
+                                                ctypes.byref(cp), None, 0, None, None, None,
+                                                0, None))
+        raise ValueError("invalid problem size")
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    disp = np.zeros((n, 2), dtype=np.float64)
+    valid = np.zeros(n, dtype=np.uint8)
+    _lib.check(L.dis_sparse_correspondences(
+        f1.data_ptr(), f2.data_ptr(), _dtype_code(f1), h, w, ctypes.byref(cp),
+        seed_arr.ctypes.data, n, disp.ctypes.data, valid.ctypes.data, ws.data_ptr(), nbytes,
+        _lib.stream_handle(torch.cuda.current_stream(dev))))
+    return [SparseMatch((float(seed_arr[i, 0]), float(seed_arr[i, 1])),
+                        (float(disp[i, 0]), float(disp[i, 1])), bool(valid[i]))
+            for i in range(n)]
 
 
 def compose_flows(flow_ab, flow_bc):

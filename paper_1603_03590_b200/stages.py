@@ -139,3 +139,28 @@ def upsample_flow(fu, fv, new_width: int, new_height: int):
                                             ou.data_ptr(), ov.data_ptr(), new_width,
                                             new_height, None))
     return ou, ov
+
+
+def densify_bidirectional(ref_img, qry_img, params: DisParams, fu_p, fv_p, foff, bu_p, bv_p,
+                          boff):
+    """densify_bidirectional (densification.py:194-234) -> (u, v) (B, H, W):
+    forward patch set (fu_p, fv_p, foff: (B, P) on the reference frame)
+    merged with the negated backward set (on the query frame, same grid)."""
+    torch = _require_cuda()
+    B, H, W = ref_img.shape
+    fu = torch.empty_like(ref_img)
+    fv = torch.empty_like(ref_img)
+    status = torch.zeros(1, dtype=torch.int32, device=ref_img.device)
+    cp = to_c(params)
+    L = _lib.lib()
+    nbytes = int(L.dis_densify_bidirectional_workspace_bytes(B, W, H, ctypes.byref(cp)))
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=ref_img.device)
+    f64 = lambda t: t.to(device=ref_img.device, dtype=torch.float64).contiguous()  # noqa: E731
+    args = [f64(t) for t in (fu_p, fv_p, foff, bu_p, bv_p, boff)]
+    _lib.check(L.dis_densify_bidirectional(
+        ref_img.data_ptr(), qry_img.data_ptr(), B, W, H, ctypes.byref(cp),
+        *[t.data_ptr() for t in args], fu.data_ptr(), fv.data_ptr(), ws.data_ptr(), nbytes,
+        status.data_ptr(), None))
+    if int(status.item()) != 0:
+        raise AssertionError("pixel without a contributing patch; grid coverage broken")
+    return fu, fv

@@ -79,3 +79,26 @@ def test_bidirectional_end_to_end_oracle(orc, k):
     p = params_from(g)
     assert p.bidirectional
     assert np.array_equal(orc.dis_flow(g["f1"], g["f2"], p), g["flow"])
+
+
+# ---- sparse correspondences (pipeline.py:202-287) ---------------------------
+
+SPARSE_CASES = ["dense", "chain", "chain_s0", "dense_bidir"]
+
+
+def sparse_params(g, name):
+    sub = {k[len(name) + 1:]: g[k] for k in g.files if k.startswith(name + "_")
+           and not any(k.startswith(o + "_") for o in SPARSE_CASES if o != name and
+                       o.startswith(name))}
+    import dataclasses
+
+    return dataclasses.replace(params_from(sub), use_densification=bool(int(sub["dens"])))
+
+
+@pytest.mark.parametrize("name", SPARSE_CASES)
+def test_sparse_correspondences_oracle(orc, name):
+    g = golden("next_sparse.npz")
+    disp, valid = orc.sparse_correspondences(g["f1"], g["f2"], g["seeds"],
+                                             sparse_params(g, name))
+    assert np.array_equal(valid, g[f"{name}_valid"])
+    assert np.array_equal(disp, g[f"{name}_disp"])

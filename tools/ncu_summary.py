@@ -89,9 +89,15 @@ BYTE_UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "M
 
 
 def full_capture(rep):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
-    rows = list(csv.reader(io.StringIO(txt)))
+    if rep.endswith(".csv"):  # `ncu -i <rep> --page raw --csv` exported on the GPU box
+        with open(rep) as f:
+            txt = f.read()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
+    rows = [r for r in csv.reader(io.StringIO(txt)) if r]
+    while rows and "Kernel Name" not in rows[0]:
+        rows.pop(0)
     hdr, units = rows[0], rows[1]
     idx = {h: i for i, h in enumerate(hdr)}
     stall_cols = [h for h in hdr if h.startswith("smsp__average_warps_issue_stalled_")
