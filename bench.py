@@ -118,13 +118,16 @@ def measured_peak_gbs():
         return 6650.0, "fallback"
 
 
-def ncu_traffic(config_name, kernel_class):
-    """DRAM bytes per launch of a kernel class from the committed ncu
-    summary (profiles/ncu_traffic.json), or None."""
+def ncu_traffic(config_name, kernel_class, launches_per_step):
+    """DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per launch of
+    a kernel class, from the committed `ncu --set full` capture of one
+    pipeline step (profiles/ncu_traffic.json holds the class's per-step
+    total), or None."""
     path = os.path.join(REPO, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(config_name, {}).get(kernel_class)
+            v = json.load(f).get(config_name, {}).get(kernel_class)
+        return None if v is None else v / max(1.0, launches_per_step)
     except Exception:
         return None
 
@@ -438,7 +441,7 @@ def run_ours(args, cfg, params):
         roofline = {"bound": "fp64", "kernel": dom, "achieved": achieved,
                     "peak": fp64_peak_tflops, "unit": "TFLOP/s",
                     "frac": achieved / fp64_peak_tflops,
-                    "traffic": ncu_traffic(cfg.name, dom),
+                    "traffic": ncu_traffic(cfg.name, dom, launches),
                     "peak_source": "measured live: DADD independent chains, no FMA "
                                    "(dis_selftest_fp64_peak)",
                     "algorithmic_flops_per_launch": per_launch,
@@ -449,7 +452,7 @@ def run_ours(args, cfg, params):
         achieved = bytes_per_launch / (ms_per_launch / 1e3) / 1e9
         roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                     "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": ncu_traffic(cfg.name, dom), "peak_source": peak_kind,
+                    "traffic": ncu_traffic(cfg.name, dom, launches), "peak_source": peak_kind,
                     "algorithmic_bytes_per_launch": bytes_per_launch}
         if "fp64_frac" in d:
             roofline["fp64_frac"] = d["fp64_frac"]

@@ -11,8 +11,8 @@
   utilisation, issue-slot utilisation, achieved occupancy, top stall reasons.
 
 Writes profiles/<tag>_launches.csv (trimmed), profiles/<tag>_summary.md and
-merges the per-launch DRAM traffic of each kernel class into
-profiles/ncu_traffic.json (read by bench.py for roofline.traffic).
+merges each kernel class's DRAM traffic over the captured step into
+profiles/ncu_traffic.json (read by bench.py for roofline.traffic, per launch).
 """
 
 from __future__ import annotations
@@ -194,8 +194,9 @@ def main():
                 tj = json.load(f)
         except Exception:
             tj = {}
-        # per-launch DRAM bytes of a class: mean over its captured launches
-        tj[args.config] = {c: sum(v) / len(v) for c, v in traffic.items()}
+        # DRAM bytes of a class over the captured pipeline step (bench.py
+        # divides by its per-step launch count of the class)
+        tj[args.config] = {c: sum(v) for c, v in traffic.items()}
         tj.setdefault("_source", {})[args.config] = f"{args.tag}: {os.path.basename(args.rep)}"
         with open(path, "w") as f:
             json.dump(tj, f, indent=1, sort_keys=True)
