@@ -358,7 +358,11 @@ __device__ __forceinline__ bool window_regular(double bx, double by, int W, int 
 
 // One window evaluation (the reference's two passes, inverse_search.py:
 // 130-152) for a regular window: rows loaded once each as contiguous
-// segments with immediate-offset loads and carried to the next row pair.
+// segments with immediate-offset loads.  Sample (oy, c) is _bilin's
+// a + fy*(b - a) with a = row(oy)[c] + fx_c*(row(oy)[c+1] - row(oy)[c]) and b
+// the same expression on row oy+1; since fx_c depends on the column alone,
+// b of row oy IS a of row oy+1 (same operands, same operations), so each
+// row's horizontal interpolants are computed once and carried down.
 template <int PS>
 __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
                                              const double* __restrict__ ref,
@@ -373,19 +377,22 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
   double wsum = 0.0;
   {
     const double* g = qry + (size_t)ybase * W + xbase;
-    double s0[S1], s1[S1];
+    double A[PS], s1[S1];
 #pragma unroll
-    for (int c = 0; c < S1; ++c) s0[c] = __ldg(g + c);
+    for (int c = 0; c < S1; ++c) s1[c] = __ldg(g + c);
+#pragma unroll
+    for (int c = 0; c < PS; ++c) A[c] = s1[c] + FX[c] * (s1[c + 1] - s1[c]);
     for (int oy = 0; oy < PS; ++oy) {
       const double fy = axis_sample(by + oy, H).f;
       g += W;
 #pragma unroll
       for (int c = 0; c < S1; ++c) s1[c] = __ldg(g + c);
 #pragma unroll
-      for (int ox = 0; ox < PS; ++ox)
-        wsum += seg_sample(s0[ox], s0[ox + 1], s1[ox], s1[ox + 1], FX[ox], fy);
-#pragma unroll
-      for (int c = 0; c < S1; ++c) s0[c] = s1[c];
+      for (int ox = 0; ox < PS; ++ox) {
+        const double Bv = s1[ox] + FX[ox] * (s1[ox + 1] - s1[ox]);
+        wsum += A[ox] + fy * (Bv - A[ox]);
+        A[ox] = Bv;
+      }
     }
   }
   off = mean_norm ? exact_div_pos(wsum, dn) - mean_t : 0.0;
@@ -403,9 +410,11 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
   };
   {
     const double* g = qry + (size_t)ybase * W + xbase;
-    double s0[S1], s1[S1];
+    double A[PS], s1[S1];
 #pragma unroll
-    for (int c = 0; c < S1; ++c) s0[c] = __ldg(g + c);
+    for (int c = 0; c < S1; ++c) s1[c] = __ldg(g + c);
+#pragma unroll
+    for (int c = 0; c < PS; ++c) A[c] = s1[c] + FX[c] * (s1[c + 1] - s1[c]);
     const double* tr = ref + (size_t)y0i * W + x0i;
     const double* gxr = rgx + (size_t)y0i * W + x0i;
     const double* gyr = rgy + (size_t)y0i * W + x0i;
@@ -420,19 +429,22 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
           const double2 t = __ldg(reinterpret_cast<const double2*>(tr + ox));
           const double2 gx = __ldg(reinterpret_cast<const double2*>(gxr + ox));
           const double2 gy = __ldg(reinterpret_cast<const double2*>(gyr + ox));
-          accumulate(seg_sample(s0[ox], s0[ox + 1], s1[ox], s1[ox + 1], FX[ox], fy), t.x, gx.x,
-                     gy.x);
-          accumulate(seg_sample(s0[ox + 1], s0[ox + 2], s1[ox + 1], s1[ox + 2], FX[ox + 1], fy),
-                     t.y, gx.y, gy.y);
+          const double B0 = s1[ox] + FX[ox] * (s1[ox + 1] - s1[ox]);
+          accumulate(A[ox] + fy * (B0 - A[ox]), t.x, gx.x, gy.x);
+          A[ox] = B0;
+          const double B1 = s1[ox + 1] + FX[ox + 1] * (s1[ox + 2] - s1[ox + 1]);
+          accumulate(A[ox + 1] + fy * (B1 - A[ox + 1]), t.y, gx.y, gy.y);
+          A[ox + 1] = B1;
         }
       } else {
 #pragma unroll
-        for (int ox = 0; ox < PS; ++ox)
-          accumulate(seg_sample(s0[ox], s0[ox + 1], s1[ox], s1[ox + 1], FX[ox], fy),
-                     __ldg(tr + ox), __ldg(gxr + ox), __ldg(gyr + ox));
+        for (int ox = 0; ox < PS; ++ox) {
+          const double Bv = s1[ox] + FX[ox] * (s1[ox + 1] - s1[ox]);
+          accumulate(A[ox] + fy * (Bv - A[ox]), __ldg(tr + ox), __ldg(gxr + ox),
+                     __ldg(gyr + ox));
+          A[ox] = Bv;
+        }
       }
-#pragma unroll
-      for (int c = 0; c < S1; ++c) s0[c] = s1[c];
       tr += W;
       gxr += W;
       gyr += W;

@@ -4,9 +4,20 @@
 // Per outer (fixed-point) iteration:
 //   k_tensor_assemble : _tensor_fields (variational.py:36-88) fused with
 //                       _assemble_system (91-121); the 12 tensor entries never
-//                       reach HBM.  Writes the 8-value SOR record of every
-//                       pixel (u, v, m00, m01, m11, r0, r1, ws) in the skewed
-//                       layout [(x + y) * H + y].
+//                       reach HBM.  It also folds in everything of the SOR
+//                       update (124-165) that does not change during the
+//                       sweeps: the four neighbour weights wq = 0.5 (wp + ws_q)
+//                       (+0 for an absent neighbour), sw = (((0 + wqL) + wqR)
+//                       + wqU) + wqD and the denominators den_u = m00 + sw,
+//                       den_v = m11 + sw — the same operations in the same
+//                       order, so bit-identical, computed once instead of
+//                       once per sweep.  Writes one 96-byte SOR record per
+//                       pixel (u, v, m01, r0, r1, den_u, den_v, wqL, wqR, wqU,
+//                       wqD, dok) as six 16-byte chunks (dok = 1 when both
+//                       denominators are in the fast-division range) in the skewed,
+//                       chunk-major layout [x + y][chunk][y]: one chunk of a
+//                       whole anti-diagonal is one contiguous run, so a band
+//                       of a diagonal is six bulk copies.
 //   k_sor<S>          : theta_vi in-place lexicographic SOR sweeps
 //                       (_sor_sweeps, variational.py:124-165) + the update
 //                       u += du, v += dv (266-267) + the finiteness check.
@@ -16,18 +27,9 @@
 // left/up neighbours from sweep t and its right/down neighbours from sweep
 // t-1.  Processing pixel (x, y) of sweep t at step k = x + y + 2t respects
 // every one of those dependencies (bit-identical), and at
-// a fixed step row y holds exactly one pixel per sweep, x = k - y - 2t.  So
-// one THREAD OWNS ONE ROW and carries all sweeps at once:
-//   left  (x-1, y, t)   = this thread's own sweep-t value from step k-1
-//   right (x+1, y, t-1) = this thread's own sweep-(t-1) value from step k-1
-//   own   (x,   y, t-1) = this thread's sweep-(t-1) value from step k-2
-//   up    (x, y-1, t)   = lane y-1's sweep-t value from step k-1 (shuffle)
-//   down  (x, y+1, t-1) = lane y+1's sweep-(t-1) value from step k-1 (shuffle)
-// Sweeps are processed in decreasing t inside a step so every read sees the
-// previous step's value; warp boundaries exchange through shared memory with
-// one __syncthreads per step.  All values stay in registers; the static
-// per-pixel record is read from the skewed layout, where the pixels of one
-// step (an anti-diagonal) are contiguous: coalesced.
+// a fixed step row y holds exactly one pixel per sweep, x = k - y - 2t.  A
+// thread owns one (row, sweep) pair; all rows of a band step together with
+// one barrier per step (see k_sor below).
 //
 // Neighbour terms use U_q = fl(u_q + du_q) exactly as the reference's
 // `u[y, x-1] + du[y, x-1]`; the last sweep's U is the updated flow.
@@ -38,20 +40,27 @@
 
 namespace disb200 {
 
-constexpr int kRecords = 8;  // u v m00 m01 m11 r0 r1 ws
+// SOR record (doubles); 96 bytes = 6 chunks of 16 bytes
+enum RecField {
+  F_U = 0, F_V, F_M01, F_R0, F_R1, F_DENU, F_DENV, F_WL, F_WR, F_WU, F_WD, F_DOK, kRec
+};
+constexpr int kChunks = kRec / 2;  // 16-byte chunks per record
 constexpr int kMaxSweepsPerPass = 8;
+
+constexpr int kZeroDoubles = 2 * 128;  // a zeroed line the SOR ring fill copies from
 
 size_t refine_scratch_doubles(int B, int W, int H) {
   const size_t Ls = (size_t)(W + H - 1) * H;
-  return (size_t)(kRecords + 2) * B * Ls;  // + du/dv carry for > 8 sweeps
+  // records + du/dv carry for > 8 sweeps + the zero line
+  return (size_t)(kRec + 2) * B * Ls + kZeroDoubles;
 }
 
-// Tile of kTTX x kTTY pixels per block: the record of each pixel is computed
-// with row-major (coalesced) reads, staged in shared memory, then written to
-// the skewed layout one diagonal run at a time (contiguous y on a diagonal).
-constexpr int kTTX = 32, kTTY = 16;
+// Tile of kTTX x kTTY pixels per block (one pixel per thread).
+constexpr int kTTX = 32, kTTY = 8;
 
-__device__ __forceinline__ void pixel_record(const RefineArgs& a, int b, int x, int y,
+// _tensor_fields (variational.py:36-88) + the system part of _assemble_system
+// (91-118) at one pixel: u, v, m00, m01, m11, r0, r1.
+__device__ __forceinline__ void pixel_system(const RefineArgs& a, int b, int x, int y,
                                              double* r) {
   const int W = a.W, H = a.H;
   const size_t plane = (size_t)W * H;
@@ -68,7 +77,6 @@ __device__ __forceinline__ void pixel_record(const RefineArgs& a, int b, int x, 
   const double* __restrict__ qdd = a.qdd + b * 4 * plane;
 
   const double up_ = u[p], vp_ = v[p];
-  // ---- _tensor_fields (variational.py:36-88) ----
   double t0xx = 0.0, t0xy = 0.0, t0xz = 0.0, t0yy = 0.0, t0yz = 0.0, t0zz = 0.0;
   double tgxx = 0.0, tgxy = 0.0, tgxz = 0.0, tgyy = 0.0, tgyz = 0.0, tgzz = 0.0;
   const double wxp = x + up_;
@@ -104,12 +112,26 @@ __device__ __forceinline__ void pixel_record(const RefineArgs& a, int b, int x, 
     tgyz = bx * ixy * ixz + by * iyy * iyz;
     tgzz = bx * ixz * ixz + by * iyz * iyz;
   }
-  // ---- _assemble_system (variational.py:91-121) ----
   const double eps2 = a.eps * a.eps;
   const double psi_i = 0.5 / sqrt(t0zz + eps2);
   const double psi_g = 0.5 / sqrt(tgzz + eps2);
   const double wi = a.delta * psi_i;
   const double wg = a.gamma * psi_g;
+  r[0] = up_;
+  r[1] = vp_;
+  r[2] = wi * t0xx + wg * tgxx;     // m00
+  r[3] = wi * t0xy + wg * tgxy;     // m01
+  r[4] = wi * t0yy + wg * tgyy;     // m11
+  r[5] = -(wi * t0xz + wg * tgxz);  // r0
+  r[6] = -(wi * t0yz + wg * tgyz);  // r1
+}
+
+// the smoothness weight of _assemble_system (variational.py:113-121)
+__device__ __forceinline__ double pixel_ws(const RefineArgs& a, int b, int x, int y) {
+  const int W = a.W, H = a.H;
+  const size_t plane = (size_t)W * H;
+  const double* __restrict__ u = a.fu + b * plane;
+  const double* __restrict__ v = a.fv + b * plane;
   const int xm = x > 0 ? x - 1 : 0;
   const int xp = x < W - 1 ? x + 1 : W - 1;
   const int ym = y > 0 ? y - 1 : 0;
@@ -119,75 +141,86 @@ __device__ __forceinline__ void pixel_record(const RefineArgs& a, int b, int x, 
   const double vx = 0.5 * (v[(size_t)y * W + xp] - v[(size_t)y * W + xm]);
   const double vy = 0.5 * (v[(size_t)yp * W + x] - v[(size_t)ym * W + x]);
   const double grad2 = ux * ux + uy * uy + vx * vx + vy * vy;
-  r[0] = up_;
-  r[1] = vp_;
-  r[2] = wi * t0xx + wg * tgxx;        // m00
-  r[3] = wi * t0xy + wg * tgxy;        // m01
-  r[4] = wi * t0yy + wg * tgyy;        // m11
-  r[5] = -(wi * t0xz + wg * tgxz);     // r0
-  r[6] = -(wi * t0yz + wg * tgyz);     // r1
-  r[7] = a.alpha * 0.5 / sqrt(grad2 + eps2);  // ws
+  const double eps2 = a.eps * a.eps;
+  return a.alpha * 0.5 / sqrt(grad2 + eps2);
 }
 
+// One block per kTTX x kTTY tile: the smoothness weights of the tile plus a
+// one-pixel ring (the neighbours' ws), then each pixel's record (system +
+// static SOR terms) staged in shared memory and written out as contiguous
+// diagonal runs of 96-byte records (16-byte stores, coalesced).
 __global__ void __launch_bounds__(256, 3) k_tensor_assemble(RefineArgs a, size_t Ls) {
-  __shared__ double rs[kRecords][kTTY][kTTX + 1];
+  constexpr int HX = kTTX + 2, HY = kTTY + 2;
+  constexpr int kPad = kChunks + 1;  // 7 x 16 B per staged record: conflict-free writes
+  __shared__ double ws_t[HY][HX];
+  __shared__ double2 rs[kTTY * kTTX][kPad];
   const int W = a.W, H = a.H;
   const int b = blockIdx.z;
   const int X0 = blockIdx.x * kTTX, Y0 = blockIdx.y * kTTY;
-  const int lx = threadIdx.x & 31;
-  for (int ly = threadIdx.x >> 5; ly < kTTY; ly += 8) {
+  if (blockIdx.x == 0 && blockIdx.y == 0 && b == 0) {  // the SOR's zero line
+    double* z = a.rec + (size_t)(kRec + 2) * a.B * Ls;
+    for (int i = threadIdx.x; i < kZeroDoubles; i += 256) z[i] = 0.0;
+  }
+  for (int i = threadIdx.x; i < HX * HY; i += 256) {
+    const int hy = i / HX, hx = i - hy * HX;
+    const int x = X0 - 1 + hx, y = Y0 - 1 + hy;
+    ws_t[hy][hx] = (x >= 0 && x < W && y >= 0 && y < H) ? pixel_ws(a, b, x, y) : 0.0;
+  }
+  __syncthreads();
+  {
+    const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
     const int x = X0 + lx, y = Y0 + ly;
     if (x < W && y < H) {
-      double r[kRecords];
-      pixel_record(a, b, x, y, r);
-#pragma unroll
-      for (int f = 0; f < kRecords; ++f) rs[f][ly][lx] = r[f];
+      double r[7];
+      pixel_system(a, b, x, y, r);
+      // _sor_sweeps' static part (variational.py:133-158): absent neighbours
+      // give wq = +0, and adding +0 to the non-negative partial sum sw
+      // leaves it unchanged
+      const double wp = ws_t[ly + 1][lx + 1];
+      const double wqL = x > 0 ? 0.5 * (wp + ws_t[ly + 1][lx]) : 0.0;
+      const double wqR = x < W - 1 ? 0.5 * (wp + ws_t[ly + 1][lx + 2]) : 0.0;
+      const double wqU = y > 0 ? 0.5 * (wp + ws_t[ly][lx + 1]) : 0.0;
+      const double wqD = y < H - 1 ? 0.5 * (wp + ws_t[ly + 2][lx + 1]) : 0.0;
+      const double sw = (((0.0 + wqL) + wqR) + wqU) + wqD;
+      double2* o = rs[threadIdx.x];
+      o[0] = make_double2(r[0], r[1]);       // u, v
+      o[1] = make_double2(r[3], r[5]);       // m01, r0
+      o[2] = make_double2(r[6], r[2] + sw);  // r1, den_u = m00 + sw
+      o[3] = make_double2(r[4] + sw, wqL);   // den_v = m11 + sw, wqL
+      o[4] = make_double2(wqR, wqU);
+      const double den_u = r[2] + sw, den_v = r[4] + sw;
+      o[5] = make_double2(wqD, den_fast_ok(den_u) && den_fast_ok(den_v) ? 1.0 : 0.0);
     }
   }
   __syncthreads();
-  // write diagonal runs: diagonal d = X0 + Y0 + dd, rows y with x = d - y in
-  // the tile -> contiguous [d*H + y] in every record field
-  const size_t B = (size_t)a.B;
+  // diagonal runs: diagonal d = X0 + Y0 + dd holds tile rows ly with
+  // lx = dd - ly in the tile; chunk c of those records is the contiguous run
+  // [(d * kChunks + c) * H + y] of the layout
   const int ndd = kTTX + kTTY - 1;
-  for (int i = threadIdx.x; i < kRecords * ndd * kTTY; i += 256) {
+  double2* __restrict__ out = reinterpret_cast<double2*>(a.rec + (size_t)b * Ls * kRec);
+  for (int i = threadIdx.x; i < kChunks * ndd * kTTY; i += 256) {
     const int ly = i % kTTY;
     const int rest = i / kTTY;
-    const int dd = rest % ndd;
-    const int f = rest / ndd;
+    const int c = rest % kChunks;
+    const int dd = rest / kChunks;
     const int lxx = dd - ly;
     const int x = X0 + lxx, y = Y0 + ly;
     if (lxx < 0 || lxx >= kTTX || x >= W || y >= H) continue;
     const size_t d = (size_t)(x + y);
-    a.rec[(f * B + b) * Ls + d * H + y] = rs[f][ly][lxx];
+    out[(d * kChunks + c) * H + y] = rs[ly * kTTX + lxx][c];
   }
 }
 
-constexpr int kLookahead = 8;  // diagonals prefetched ahead of the wavefront (covers HBM latency)
-constexpr int kPitch = 9;      // doubles per ring row: 8 fields + 1 pad (72 B, conflict-free LDS.64)
+constexpr int kLookahead = 5;      // diagonals fetched ahead of sweep 0 (~4 steps of latency cover)
 constexpr int kMaxBandRows = 128;  // rows (threads per sweep) of one CTA's band
-
-enum RecField { F_U = 0, F_V, F_M00, F_M01, F_M11, F_R0, F_R1, F_WS };
 
 template <int S>
 __host__ __device__ constexpr int ring_slots() {
-  // live at step k: diagonals k - 2(S-1) - 1 (last sweep's up-neighbour) .. k + 1,
-  // plus the ones in flight up to k + kLookahead
-  return kLookahead + 2 * S;
+  // live at step k: diagonals k - 2(S-1) (last sweep) .. k + 1 (sweep 0's right
+  // and down neighbours), plus the fills in flight up to k + kLookahead
+  return 2 * (S - 1) + 1 + kLookahead;
 }
 
-__device__ __forceinline__ void cp_async8(unsigned smem_dst, const double* gsrc, unsigned src_bytes) {
-  // src_bytes = 0 zero-fills the 8 destination bytes
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_dst), "l"(gsrc),
-               "r"(src_bytes)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
 __device__ __forceinline__ unsigned cluster_rank() {
   unsigned r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
@@ -199,22 +232,9 @@ __device__ __forceinline__ void cluster_arrive() {
 __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
-// store a double into the shared memory of CTA `rank` of this cluster
-__device__ __forceinline__ void st_cluster(const double* local, unsigned rank, double v) {
-  unsigned a = (unsigned)__cvta_generic_to_shared(local), ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(a), "r"(rank));
-  asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(ra), "d"(v) : "memory");
-}
-
 // mbarrier helpers (band-boundary signalling between the CTAs of a cluster)
 __device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_remote(unsigned bar_local, unsigned rank) {
-  unsigned ra;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(bar_local), "r"(rank));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(ra)
-               : "memory");
 }
 // st.async of (x, y) into CTA `rank`'s shared memory at local-equivalent
 // address a; completion is counted (16 bytes) on that CTA's mbarrier bar
@@ -244,39 +264,7 @@ __device__ __forceinline__ void mbar_wait_parity(unsigned bar, unsigned parity) 
       "r"(parity)
       : "memory");
 }
-
-// The wavefront SOR kernel (see the file header).
-//
-// Thread (sweep t, row group g) owns RT consecutive rows of a band and, at
-// step k, computes pixel x = k - y - 2t of each of them (all on diagonal
-// j = k - 2t).  Its rows are independent within a step (every neighbour
-// value is from an earlier step), so a thread carries RT independent update
-// chains.  A pair's rows are split over a cluster of C CTAs (1..16); CTA c
-// owns the band [c*Hc, c*Hc + Hc).  Shared memory holds
-//   ring[R][Hp+2][kPitch] : records of the live diagonals (+ one halo row
-//                           above and below the band), filled by cp.async
-//                           kLookahead steps ahead; entries outside the
-//                           level are zero-filled
-//   xuv[2][S][Hp+2][2]    : U, V produced at the last two steps
-//   xd [3][S][Hp+2][2]    : du, dv of the last three steps (own previous)
-// Neighbours of (x, y, t): left = own registers (step k-1); up = the
-// thread's own row above (registers, step k-1) or xuv[k-1][t][y-1] for its
-// first row; right = xuv[k-1][t-1][y]; down = xuv[k-1][t-1][y+1]; own
-// previous du/dv = xd[k-2][t-1][y]; for t = 0 the initial values come from
-// the ring (du = 0, or the carried du of a chained pass).  The band's
-// boundary rows write their U, V straight into the neighbouring CTA's halo
-// rows of xuv (distributed shared memory) and signal it with a remote
-// mbarrier arrive; the consumer waits on its local mbarrier — neighbour to
-// neighbour, no cluster-wide barrier per step.  A thread whose pixel is
-// outside the level computes finite garbage from zero-filled entries and
-// never stores it, so no selects are needed.
-// explicit shared-space accesses (32-bit addresses; keeps the compiler
-// from re-deriving generic->shared windows every step)
-__device__ __forceinline__ double lds(unsigned a) {
-  double v;
-  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a) : "memory");
-  return v;
-}
+// explicit shared-space accesses (32-bit addresses)
 __device__ __forceinline__ void sts2(unsigned a, double x, double y) {
   asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a), "d"(x), "d"(y) : "memory");
 }
@@ -284,100 +272,169 @@ __device__ __forceinline__ void lds2(unsigned a, double& x, double& y) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(a) : "memory");
 }
 
-template <int S, int RT, bool HZ>
-__global__ void __launch_bounds__(S * kMaxBandRows / RT, 1)
+__device__ __forceinline__ void bulk_g2s(unsigned smem_dst, const void* gsrc, unsigned bytes,
+                                         unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_dst),
+      "l"(gsrc), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity_cta(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// The wavefront SOR kernel.
+//
+// Thread (sweep t, band row r) computes, at step k, pixel x = k - y - 2t of
+// row y = y0 + r (diagonal j = k - 2t).  A pair's rows are split over a
+// cluster of C CTAs (1..16); CTA c owns the band [c*Hc, c*Hc + Hc), padded to
+// Hp rows (a multiple of 32).  Shared memory:
+//   ring[R][6][Hp+1] x 16 B : the 96-byte records of the live diagonals (band
+//                             rows + the row below, sweep 0's down
+//                             neighbour), chunk-major like the global layout:
+//                             one diagonal = six cp.async.bulk copies issued
+//                             by one thread kLookahead steps ahead, completion
+//                             counted on the slot's mbarrier
+//   xuv[2][S][Hp+2] x 16 B  : U, V of the last two steps (+ halo row above
+//                             and below the band)
+//   xd [3][S][Hp+2] x 16 B  : du, dv of the last three steps
+// Neighbours of (x, y, t): left = own registers (step k-1); up =
+// xuv[k-1][t][y-1]; right = xuv[k-1][t-1][y]; down = xuv[k-1][t-1][y+1]; own
+// previous du/dv = xd[k-2][t-1][y]; for t = 0 the right/down values are the
+// records' u, v (+ du = 0, or the carried du of a chained pass).  The
+// static terms (neighbour weights, sw, denominators) come precomputed in
+// the record.  The band's boundary rows write their U, V straight into the
+// neighbouring CTA's halo rows (distributed shared memory, st.async counted
+// on that CTA's mbarrier).
+//
+// Idle pixels (outside the level: ramp-up/down of the wavefront, rows past
+// the band) see zero records, so they never update and publish U = du = 0;
+// a valid pixel's absent neighbour enters its sums as +0 * 0.  A warp whose
+// 32 pixels are all idle skips the arithmetic (and publishes zeros).
+template <int S, bool HZ>
+__global__ void __launch_bounds__(S * kMaxBandRows + 32, 1)
     k_sor(const double* __restrict__ rec, int B, int W, int H, int Hc, size_t Ls, double omega,
           const double* du_in, const double* dv_in, double* du_out, double* dv_out,
-          double* __restrict__ fu, double* __restrict__ fv, uint32_t* status) {
-  extern __shared__ double smem[];
+          double* __restrict__ fu, double* __restrict__ fv, uint32_t* status,
+          const double* __restrict__ zeros) {
+  extern __shared__ __align__(16) unsigned char smem[];
   constexpr int R = ring_slots<S>();
-  constexpr int kFieldsPerThread = (8 + S - 1) / S;
-  constexpr unsigned kRowB = kPitch * 8;  // ring row bytes
   const int C = (int)(gridDim.x / (unsigned)B) > 0 ? (int)(gridDim.x / (unsigned)B) : 1;
   const int c = C > 1 ? (int)cluster_rank() : 0;
   const int b = blockIdx.x / C;
-  const int TS = blockDim.x / S;          // threads per sweep
-  const int Hp = TS * RT;                 // band rows (padded)
-  const int t = threadIdx.x / TS;         // sweep
-  const int tg = threadIdx.x - t * TS;    // row group
+  const int Hp = (blockDim.x - 32) / S;  // band rows (padded); + one producer warp
+  const bool producer = threadIdx.x >= (unsigned)(S * Hp);  // ring fill, no pixels
+  const int t = producer ? 0 : threadIdx.x / Hp;  // sweep
+  const int r = producer ? Hp : threadIdx.x - t * Hp;  // band row (producer: none)
   const int y0 = c * Hc;
-  const int ty0 = tg * RT;                // first band row of this thread
+  const int y = y0 + r;
   const int nrows = min(Hc, H - y0);
   const int ndiag = W + H - 1;
-  const int rows = Hp + 2;  // + halo above and below
-  const unsigned slot_bytes = (unsigned)rows * kRowB;
-  double* ring = smem;                                // [R][rows][kPitch]
-  double* xuvp = ring + (size_t)R * rows * kPitch;   // [2][S][rows][2]
-  double* xdp = xuvp + (size_t)2 * S * rows * 2;     // [3][S][rows][2]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(xdp + (size_t)3 * S * rows * 2);
-  const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
+  const int rrows = Hp + 1;  // ring rows
+  const int xrows = Hp + 2;  // exchange rows
+  const unsigned slot_bytes = (unsigned)(kChunks * rrows * 16);
+  const unsigned ring_s = (unsigned)__cvta_generic_to_shared(smem);
   const unsigned ring_end = ring_s + (unsigned)R * slot_bytes;
-  const unsigned xuv_s = (unsigned)__cvta_generic_to_shared(xuvp);
-  const unsigned xd_s = (unsigned)__cvta_generic_to_shared(xdp);
-  const unsigned uv_par_b = (unsigned)(S * rows * 16);  // one parity of xuv, bytes
-  const unsigned d_ph_b = (unsigned)(S * rows * 16);    // one phase of xd, bytes
-  // mbarriers [above p0, above p1, below p0, below p1]: one per direction and
-  // step parity, so a barrier's phase n is step 2n + p and a neighbour (at
-  // most one step ahead) can never overrun a phase its consumer still waits on
-  const unsigned bar_above = (unsigned)__cvta_generic_to_shared(bars);
+  const unsigned xuv_s = ring_end;
+  const unsigned xd_s = xuv_s + (unsigned)(2 * S * xrows * 16);
+  const unsigned bar_above = xd_s + (unsigned)(3 * S * xrows * 16);  // 8-byte aligned
   const unsigned bar_below = bar_above + 16;
-  const double* __restrict__ base = rec + (size_t)b * Ls;
-  const size_t fstride = (size_t)B * Ls;
+  const unsigned bar_ring = bar_above + 32;  // [R] slot-fill barriers
+  const double2* __restrict__ base =
+      reinterpret_cast<const double2*>(rec + (size_t)b * Ls * kRec);  // [d][chunk][H]
   const double* Dui = du_in ? du_in + (size_t)b * Ls : nullptr;  // may alias du_out
   const double* Dvi = dv_in ? dv_in + (size_t)b * Ls : nullptr;
   const double om1 = 1.0 - omega;
 
-  // cp.async of this thread's record fields (t, t+S, ...) of one ring row
-  auto fetch = [&](unsigned dst, const double* src, bool ok) {
-    const double* g = ok ? src : base;
-#pragma unroll
-    for (int i = 0; i < kFieldsPerThread; ++i) {
-      const int f = t + i * S;
-      if (f < 8) cp_async8(dst + 8 * f, g + f * fstride, ok ? 8u : 0u);
-    }
-  };
-
-  {  // ring + exchange buffers start at zero (idle threads read them)
-    const int nx = R * rows * kPitch + (2 + 3) * S * rows * 2;
-    for (int i = threadIdx.x; i < nx; i += blockDim.x) ring[i] = 0.0;
+  {  // ring + exchange buffers start at zero
+    const unsigned nz = (unsigned)(R * kChunks * rrows + 5 * S * xrows);  // 16-byte entries
+    for (unsigned i = threadIdx.x; i < nz; i += blockDim.x) sts2(ring_s + 16 * i, 0.0, 0.0);
   }
-  if (threadIdx.x == 0 && C > 1) {
-    // one local arrive (the consumer's expect_tx) per phase; the neighbour's
-    // S st.async (16 bytes each) complete the phase's transaction count
-    mbar_init(bar_above, 1);
-    mbar_init(bar_above + 8, 1);
-    mbar_init(bar_below, 1);
-    mbar_init(bar_below + 8, 1);
+  if (threadIdx.x == 0) {
+    if (C > 1) {
+      // one local arrive (the consumer's expect_tx) per phase; the neighbour's
+      // S st.async (16 bytes each) complete the phase's transaction count
+      mbar_init(bar_above, 1);
+      mbar_init(bar_above + 8, 1);
+      mbar_init(bar_below, 1);
+      mbar_init(bar_below + 8, 1);
+    }
+    for (int i = 0; i < R; ++i) mbar_init(bar_ring + 8u * i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+
+  // ring fill (producer warp): diagonal jn -> slot jn % R.  Invariant: a
+  // slot's row holds the record of (jn - y, y) when that pixel is inside the
+  // level and zero otherwise, so idle pixels compute exactly like the
+  // reference would on zeros (no update: den = 0) and publish U = du = 0.
+  // The valid rows y in [max(y0, jn - W + 1), min(y0 + Hp, H - 1, jn)] are
+  // six bulk copies (one per chunk run); the rows that were valid for the
+  // slot's previous diagonal jn - R but are not any more (the ramp-down
+  // edge) are zeroed by a copy from a zeroed global line.
+  const int ylast = min(y0 + rrows, H) - 1;
+  const unsigned lane = threadIdx.x & 31;
   int jn = 0;
-  unsigned sin_s = ring_s;
-  const double* gsrc = base + y0 + ty0;  // &record[jn * H + y0 + ty0]
-  const unsigned my_ring_row = (unsigned)(ty0 + 1) * kRowB;
+  unsigned sin_s = ring_s, sin_bar = bar_ring;
   auto issue_next = [&]() {
-    if (jn < ndiag) {
+    const int ya = max(y0, jn - W + 1), yb = min(ylast, jn);
+    const int jo = jn - R;  // the slot's previous diagonal
+    const int pa = max(y0, jo - W + 1), pb = min(ylast, jo);
+    const int za = pa, zb = min(pb, ya <= yb ? ya - 1 : pb);
+    const unsigned zrun = (jo >= 0 && zb >= za) ? (unsigned)(zb - za + 1) * 16u : 0u;
+    const unsigned run = yb >= ya ? (unsigned)(yb - ya + 1) * 16u : 0u;
+    if (lane == 0) {
+      // everything written into the ring goes through the async proxy (the
+      // zeros are copied from a zeroed global line), in disjoint row ranges
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sin_bar),
+                   "r"(kChunks * (run + zrun))
+                   : "memory");
+      if (zrun) {
+        const unsigned dst = sin_s + (unsigned)((za - y0) * 16);
 #pragma unroll
-      for (int i = 0; i < RT; ++i) {
-        const int yy = y0 + ty0 + i;
-        const int x = jn - yy;
-        fetch(sin_s + my_ring_row + i * kRowB, gsrc + i, yy < H && x >= 0 && x < W);
+        for (int cc = 0; cc < kChunks; ++cc)
+          bulk_g2s(dst + (unsigned)(cc * rrows * 16), zeros, zrun, sin_bar);
       }
-      if (tg == 0) fetch(sin_s, gsrc - 1, y0 > 0 && jn - (y0 - 1) >= 0 && jn - (y0 - 1) < W);
-      if (tg == TS - 1) {
-        const int yy = y0 + Hp;
-        fetch(sin_s + (unsigned)(Hp + 1) * kRowB, gsrc + RT, yy < H && jn - yy >= 0 &&
-                                                                 jn - yy < W);
+      if (run) {
+        const double2* g = base + (size_t)jn * kChunks * H + ya;
+        const unsigned dst = sin_s + (unsigned)((ya - y0) * 16);
+#pragma unroll
+        for (int cc = 0; cc < kChunks; ++cc)
+          bulk_g2s(dst + (unsigned)(cc * rrows * 16), g + (size_t)cc * H, run, sin_bar);
       }
     }
-    cp_async_commit();
     ++jn;
-    gsrc += H;
     sin_s += slot_bytes;
-    if (sin_s == ring_end) sin_s = ring_s;
+    sin_bar += 8;
+    if (sin_s == ring_end) {
+      sin_s = ring_s;
+      sin_bar = bar_ring;
+    }
   };
-  for (int j = 0; j < kLookahead; ++j) issue_next();
-  cp_async_wait<kLookahead - 2>();
+  // slot readiness: fill n of slot s (diagonal s + nR) completes phase n
+  auto wait_diag = [&](int j) {
+    if (j >= 0 && j < jn)
+      mbar_wait_parity_cta(bar_ring + 8u * (unsigned)(j % R), (unsigned)((j / R) & 1));
+  };
+  const bool filler = threadIdx.x == (unsigned)(S * Hp);  // lane 0 of the producer warp
+  if (producer) {
+    // the start-up clear (generic proxy) before any async-proxy copy
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    for (int j = 0; j < kLookahead; ++j) issue_next();
+    if (filler) {
+      wait_diag(0);
+      wait_diag(1);
+    }
+  }
   if (C > 1) {  // barriers initialised everywhere before any remote arrive
     cluster_arrive();
     cluster_wait();
@@ -385,195 +442,143 @@ __global__ void __launch_bounds__(S * kMaxBandRows / RT, 1)
     __syncthreads();
   }
 
-  double lU[RT], lV[RT], lW[RT];  // each row's previous pixel (left neighbour / up of next row)
-#pragma unroll
-  for (int i = 0; i < RT; ++i) lU[i] = lV[i] = lW[i] = 0.0;
+  double lU = 0.0, lV = 0.0;  // this row's previous pixel (left neighbour)
   bool bad = false;
   const int nsteps = ndiag + 2 * (S - 1);
-  // ring slot address of diagonal j = k - 2t (rotates by one slot per step)
-  unsigned a_j = ring_s + (unsigned)(((-2 * t) % R + R) % R) * slot_bytes;
-  // exchange-buffer offsets of (t, my first row) and (t-1, my first row)
-  const unsigned uv_me = (unsigned)((t * rows + ty0 + 1) * 16);
-  const unsigned uv_prev = (unsigned)(((t > 0 ? t - 1 : 0) * rows + ty0 + 1) * 16);
-  unsigned uv_r = xuv_s + uv_par_b, uv_w = xuv_s;  // parity of step k-1 / step k
-  unsigned d_w = xd_s, d_r = xd_s + d_ph_b;       // phase k mod 3 / (k-2) mod 3
+  unsigned a_j = ring_s + (unsigned)(((-2 * t) % R + R) % R) * slot_bytes;  // slot of j = k - 2t
+  const unsigned rrow = (unsigned)(r * 16);
+  const unsigned cstride = (unsigned)(rrows * 16);
+  const unsigned uv_me = (unsigned)((t * xrows + r + 1) * 16);
+  const unsigned uv_prev = (unsigned)(((t > 0 ? t - 1 : 0) * xrows + r + 1) * 16);
+  unsigned uv_r = xuv_s + (unsigned)(S * xrows * 16), uv_w = xuv_s;  // step k-1 / step k
+  const unsigned d_ph_b = (unsigned)(S * xrows * 16);
+  unsigned d_w = xd_s, d_r = xd_s + d_ph_b;  // phase k mod 3 / (k-2) mod 3
   const unsigned d_end = xd_s + 3 * d_ph_b;
   const size_t fplane = (size_t)W * H;
-  // band-boundary roles
-  const bool first_owner = C > 1 && c > 0 && tg == 0;                  // needs "up" of row 0
-  const int last_ty = nrows - 1;
-  const bool last_owner = C > 1 && c < C - 1 && ty0 <= last_ty && last_ty < ty0 + RT;
-  int xk = -y0 - ty0 - 2 * t;  // x of my first row at step k
-  for (int k = 0; k < nsteps; ++k, ++xk) {
-    if (C > 1) {
-      // post this step's expected halo bytes (phase k>>1 of barrier k&1; the
-      // barrier's previous phase, step k-2, completed before step k-1 began)
+  const int last_r = nrows - 1;
+  const int wr0 = r & ~31;  // first row of my warp
+  // warps holding a band-boundary row (the only ones touching the halo
+  // mbarriers): warp-uniform
+  const bool halo_warp = C > 1 && ((c > 0 && wr0 == 0) || (c < C - 1 && (last_r & ~31) == wr0));
+  const bool first_owner = C > 1 && c > 0 && r == 0;
+  const bool last_owner = C > 1 && c < C - 1 && r == last_r;
+  int x = -y0 - r - 2 * t;  // my pixel at step k
+  int xw = -y0 - wr0 - 2 * t;  // lane 0's pixel (largest x of the warp)
+  const unsigned wact = (!producer && wr0 < nrows) ? (unsigned)(W + 31) : 0u;
+  for (int k = 0; k < nsteps; ++k, ++x, ++xw) {
+    if (halo_warp) {
       if (first_owner && t == 0) mbar_expect_tx(bar_above + (unsigned)(k & 1) * 8u, 16u * S);
       if (last_owner && t == 0) mbar_expect_tx(bar_below + (unsigned)(k & 1) * 8u, 16u * S);
       if (k > 0) {  // halo values of step k-1 from the neighbouring bands
         const unsigned sel = (unsigned)((k - 1) & 1) * 8u;
         const unsigned par = (unsigned)(((k - 1) >> 1) & 1);
         if (first_owner) mbar_wait_parity(bar_above + sel, par);
-        // every boundary-row thread waits (t = 0 does not read the halo, but
-        // its next write into the neighbour's halo must not overtake the
-        // neighbour's read of the previous one)
         if (last_owner) mbar_wait_parity(bar_below + sel, par);
       }
     }
-    issue_next();
+    if (producer) issue_next();
     const int j = k - 2 * t;
-    const unsigned a_m = (a_j == ring_s ? ring_end : a_j) - slot_bytes;
-    const unsigned a_p = a_j + slot_bytes == ring_end ? ring_s : a_j + slot_bytes;
-    const unsigned rp0 = a_j + my_ring_row;          // (x, y) of my first row
-    const unsigned rm0 = a_m + my_ring_row - kRowB;  // (x, y-1)
-    const unsigned rn0 = a_p + my_ring_row;          // (x+1, y); + kRowB: (x, y+1)
-    double nU[RT], nV[RT], mU[RT], mV[RT], dU[RT], dV[RT], ucA[RT], vcA[RT], wpA[RT],
-        m01A[RT], den_uA[RT], den_vA[RT], r1svA[RT];
-    // Phase A (all rows, straight-line): neighbour values, weights, the four
-    // sums and the u numerator.  Decreasing i: the "up" value of row i is
-    // row i-1's step k-1 value (registers).
-#pragma unroll
-    for (int i = RT - 1; i >= 0; --i) {
-      const int y = y0 + ty0 + i;
-      const int x = xk - i;
-      const bool hasU = y > 0, hasD = y < H - 1;
-      const unsigned rp = rp0 + i * kRowB, rm = rm0 + i * kRowB, rn = rn0 + i * kRowB;
-      const double uc = lds(rp + 8 * F_U), vc = lds(rp + 8 * F_V), wp = lds(rp + 8 * F_WS);
-      const double m00 = lds(rp + 8 * F_M00), m01 = lds(rp + 8 * F_M01);
-      const double m11 = lds(rp + 8 * F_M11);
-      const double r0 = lds(rp + 8 * F_R0), r1 = lds(rp + 8 * F_R1);
-      double upU, upV;
-      if (i > 0) {  // row above is mine: its value from step k-1 (not yet updated)
-        upU = lU[i - 1];
-        upV = lV[i - 1];
-      } else {
-        lds2(uv_r + uv_me - 16, upU, upV);
-      }
-      const double upW = lds(rm + 8 * F_WS);
-      const double rW = lds(rn + 8 * F_WS);
-      const double dnW = lds(rn + kRowB + 8 * F_WS);
-      double rU, rV, dnU, dnV, du, dv;
+    const unsigned a_p = a_j + slot_bytes == ring_end ? ring_s : a_j + slot_bytes;  // j + 1
+    double U = 0.0, V = 0.0, du = 0.0, dv = 0.0;
+    // warp-uniform: any of my warp's 32 pixels inside the level?  (lane 0
+    // holds the warp's largest x)
+    if ((unsigned)xw < wact) {
+      // ---- record (6 x LDS.128) ----
+      double uc, vc, m01, r0, r1, den_u, den_v, wqL, wqR, wqU, wqD, dok;
+      lds2(a_j + rrow, uc, vc);
+      lds2(a_j + cstride + rrow, m01, r0);
+      lds2(a_j + 2 * cstride + rrow, r1, den_u);
+      lds2(a_j + 3 * cstride + rrow, den_v, wqL);
+      lds2(a_j + 4 * cstride + rrow, wqR, wqU);
+      lds2(a_j + 5 * cstride + rrow, wqD, dok);
+      const bool dfast = dok != 0.0;
+      // ---- neighbours ----
+      double upU, upV, rU, rV, dnU, dnV;
+      lds2(uv_r + uv_me - 16, upU, upV);
       if (t > 0) {
-        lds2(uv_r + uv_prev + 16 * i, rU, rV);
-        lds2(uv_r + uv_prev + 16 * (i + 1), dnU, dnV);
-        lds2(d_r + uv_prev + 16 * i, du, dv);
-      } else if (Dui) {  // chained pass: the carried du/dv of the previous sweeps
-        const int jp = j + 1;
-        const bool okp = jp >= 0 && jp < ndiag;
-        const bool ok = j >= 0 && j < ndiag && y < H;
-        const int yc = y < H ? y : H - 1;
-        rU = lds(rn + 8 * F_U) + Dui[okp ? (size_t)jp * H + yc : 0];
-        rV = lds(rn + 8 * F_V) + Dvi[okp ? (size_t)jp * H + yc : 0];
-        dnU = lds(rn + kRowB + 8 * F_U) + Dui[okp && hasD ? (size_t)jp * H + yc + 1 : 0];
-        dnV = lds(rn + kRowB + 8 * F_V) + Dvi[okp && hasD ? (size_t)jp * H + yc + 1 : 0];
-        du = Dui[ok ? (size_t)j * H + y : 0];
-        dv = Dvi[ok ? (size_t)j * H + y : 0];
+        lds2(uv_r + uv_prev, rU, rV);
+        lds2(uv_r + uv_prev + 16, dnU, dnV);
+        lds2(d_r + uv_prev, du, dv);
       } else {
-        rU = lds(rn + 8 * F_U) + 0.0;  // u + du with du = 0 (reference: u[q] + du[q])
-        rV = lds(rn + 8 * F_V) + 0.0;
-        dnU = lds(rn + kRowB + 8 * F_U) + 0.0;
-        dnV = lds(rn + kRowB + 8 * F_V) + 0.0;
-        du = 0.0;
-        dv = 0.0;
+        // (x+1, y) and (x, y+1) of sweep "-1": u + du of the records, du = 0
+        // or the carried du of a chained pass; absent ones -> 0 (the slot may
+        // hold anything there)
+        lds2(a_p + rrow, rU, rV);
+        lds2(a_p + rrow + 16, dnU, dnV);
+        if (Dui) {
+          const bool hasD = y < H - 1;
+          const int jp = j + 1;
+          const bool okp = jp >= 0 && jp < ndiag;
+          const bool ok = j >= 0 && j < ndiag && y < H;
+          const int yc = y < H ? y : H - 1;
+          rU = rU + Dui[okp ? (size_t)jp * H + yc : 0];
+          rV = rV + Dvi[okp ? (size_t)jp * H + yc : 0];
+          dnU = dnU + Dui[okp && hasD ? (size_t)jp * H + yc + 1 : 0];
+          dnV = dnV + Dvi[okp && hasD ? (size_t)jp * H + yc + 1 : 0];
+          du = Dui[ok ? (size_t)j * H + y : 0];
+          dv = Dvi[ok ? (size_t)j * H + y : 0];
+        } else {
+          rU = rU + 0.0;  // the reference's u[q] + du[q]
+          rV = rV + 0.0;
+          dnU = dnU + 0.0;
+          dnV = dnV + 0.0;
+        }
       }
-      // absent neighbours (borders) contribute wq = +0 times a finite value:
-      // adding an exact zero leaves the reference's partial sums unchanged
-      const double wqL = x > 0 ? 0.5 * (wp + lW[i]) : 0.0;
-      const double wqR = x < W - 1 ? 0.5 * (wp + rW) : 0.0;
-      const double wqU = hasU ? 0.5 * (wp + upW) : 0.0;
-      const double wqD = hasD ? 0.5 * (wp + dnW) : 0.0;
-      const double sw = (((0.0 + wqL) + wqR) + wqU) + wqD;
-      const double su = (((0.0 + wqL * (lU[i] - uc)) + wqR * (rU - uc)) + wqU * (upU - uc)) +
+      // ---- the update (variational.py:133-165): absent neighbours have
+      // wq = +0, which adds an exact zero to the partial sums ----
+      const double su = (((0.0 + wqL * (lU - uc)) + wqR * (rU - uc)) + wqU * (upU - uc)) +
                         wqD * (dnU - uc);
-      const double sv = (((0.0 + wqL * (lV[i] - vc)) + wqR * (rV - vc)) + wqU * (upV - vc)) +
+      const double sv = (((0.0 + wqL * (lV - vc)) + wqR * (rV - vc)) + wqU * (upV - vc)) +
                         wqD * (dnV - vc);
-      ucA[i] = uc;
-      vcA[i] = vc;
-      wpA[i] = wp;
-      m01A[i] = m01;
-      den_uA[i] = m00 + sw;
-      den_vA[i] = m11 + sw;
-      r1svA[i] = r1 + sv;
-      dU[i] = du;
-      dV[i] = dv;
-      nU[i] = r0 + su - m01 * dv;
-    }
-    // Phase B: u quotients (straight-line fast division; rare IEEE fallback;
-    // quotients of rows with den <= 1e-12 are discarded, whatever they are)
-    bool slow = false;
-#pragma unroll
-    for (int i = 0; i < RT; ++i) {
-      slow = slow | ((den_uA[i] > 1e-12) & !div_fast_ok(nU[i], den_uA[i]));
-      mU[i] = div_fast_rn(nU[i], den_uA[i]);
-    }
-    if (slow) {
-#pragma unroll
-      for (int i = 0; i < RT; ++i) mU[i] = exact_div_pos(nU[i], den_uA[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < RT; ++i) {
-      const double q = nU[i] == 0.0 ? nU[i] : mU[i];
-      const double nu = om1 * dU[i] + omega * q;
-      dU[i] = den_uA[i] > 1e-12 ? nu : dU[i];
-      nV[i] = r1svA[i] - m01A[i] * dU[i];
-    }
-    // Phase C: v quotients (none in stereo mode: horizontal_only skips the
-    // dv update, variational.py:161)
-    if (!HZ) {
-      slow = false;
-#pragma unroll
-      for (int i = 0; i < RT; ++i) {
-        slow = slow | ((den_vA[i] > 1e-12) & !div_fast_ok(nV[i], den_vA[i]));
-        mV[i] = div_fast_rn(nV[i], den_vA[i]);
+      const double nU = r0 + su - m01 * dv;
+      {
+        const bool slow = (den_u > 1e-12) && !(dfast && num_fast_ok(nU));
+        double m = div_fast_rn(nU, den_u);
+        if (slow) m = exact_div_pos(nU, den_u);
+        const double q = nU == 0.0 ? nU : m;
+        const double nu = om1 * du + omega * q;
+        du = den_u > 1e-12 ? nu : du;
       }
-      if (slow) {
-#pragma unroll
-        for (int i = 0; i < RT; ++i) mV[i] = exact_div_pos(nV[i], den_vA[i]);
-      }
-    }
-    // Phase D: updates, exchange stores, halo, output
-#pragma unroll
-    for (int i = 0; i < RT; ++i) {
-      const int ty = ty0 + i;
-      const int y = y0 + ty;
-      const int x = xk - i;
-      double dv = dV[i];
       if (!HZ) {
-        const double q = nV[i] == 0.0 ? nV[i] : mV[i];
-        const double nv = om1 * dV[i] + omega * q;
-        dv = den_vA[i] > 1e-12 ? nv : dV[i];
+        const double nV = r1 + sv - m01 * du;
+        const bool slow = (den_v > 1e-12) && !(dfast && num_fast_ok(nV));
+        double m = div_fast_rn(nV, den_v);
+        if (slow) m = exact_div_pos(nV, den_v);
+        const double q = nV == 0.0 ? nV : m;
+        const double nv = om1 * dv + omega * q;
+        dv = den_v > 1e-12 ? nv : dv;
       }
-      const double du = dU[i];
-      const double U = ucA[i] + du, V = vcA[i] + dv;
-      lU[i] = U;
-      lV[i] = V;
-      lW[i] = wpA[i];
-      if (ty < nrows) {  // padding rows never store: row nrows+1 is the halo
-        sts2(uv_w + uv_me + 16 * i, U, V);
-        sts2(d_w + uv_me + 16 * i, du, dv);
+      U = uc + du;
+      V = vc + dv;
+    }
+    lU = U;
+    lV = V;
+    // ---- exchange, halo, output ----
+    if (r < nrows) {  // padding rows never store
+      sts2(uv_w + uv_me, U, V);
+      sts2(d_w + uv_me, du, dv);
+    }
+    if (halo_warp) {
+      if (r == 0 && c > 0)  // band's first row -> CTA c-1's row below its band
+        st_async2(uv_w + (unsigned)((t * xrows + Hc + 1) * 16),
+                  bar_below + (unsigned)(k & 1) * 8u, c - 1, U, V);
+      if (r == last_r && c < C - 1)  // band's last row -> CTA c+1's row above its band
+        st_async2(uv_w + (unsigned)(t * xrows * 16), bar_above + (unsigned)(k & 1) * 8u, c + 1,
+                  U, V);
+    }
+    if (t == S - 1 && r < nrows && x >= 0 && x < W) {
+      if (du_out) {
+        du_out[(size_t)b * Ls + (size_t)j * H + y] = du;
+        dv_out[(size_t)b * Ls + (size_t)j * H + y] = dv;
       }
-      if (C > 1) {
-        if (ty == 0 && c > 0)  // band's first row -> CTA c-1's row below its band
-          st_async2(uv_w + (unsigned)((t * rows + Hc + 1) * 16), bar_below + (unsigned)(k & 1) * 8u,
-                    c - 1, U, V);
-        if (ty == last_ty && c < C - 1)  // band's last row -> CTA c+1's row above its band
-          st_async2(uv_w + (unsigned)(t * rows * 16), bar_above + (unsigned)(k & 1) * 8u, c + 1,
-                    U, V);
-      }
-      if (t == S - 1 && ty < nrows && x >= 0 && x < W) {
-        if (du_out) {
-          du_out[(size_t)b * Ls + (size_t)j * H + y] = du;
-          dv_out[(size_t)b * Ls + (size_t)j * H + y] = dv;
-        }
-        if (fu) {
-          const size_t oo = (size_t)b * fplane + (size_t)y * W + x;
-          fu[oo] = U;
-          fv[oo] = V;
-          bad |= !(isfinite(U) && isfinite(V));
-        }
+      if (fu) {
+        const size_t oo = (size_t)b * fplane + (size_t)y * W + x;
+        fu[oo] = U;
+        fv[oo] = V;
+        bad |= !(isfinite(U) && isfinite(V));
       }
     }
-    cp_async_wait<kLookahead - 2>();
+    if (filler) wait_diag(k + 2);  // sweep 0 reads k+1 and k+2 next step
     __syncthreads();
     a_j = a_p;
     const unsigned tu = uv_r;
@@ -593,69 +598,52 @@ __global__ void __launch_bounds__(S * kMaxBandRows / RT, 1)
 
 template <int S>
 static size_t sor_smem_bytes(int hp) {
-  const size_t rows = (size_t)hp + 2;
-  return ((size_t)ring_slots<S>() * rows * kPitch + (size_t)(2 + 3) * S * rows * 2) *
-             sizeof(double) +
-         4 * sizeof(uint64_t);
-}
-
-// rows per thread (RT): a thread carries RT independent row updates per
-// step; fewer rows per thread = more warps to hide latency.
-static int sor_rows_per_thread() {
-  static const int rt = [] {
-    const char* e = getenv("DIS_SOR_RT");  // experiments only
-    const int v = e ? atoi(e) : 1;
-    return (v == 1 || v == 2 || v == 4) ? v : 1;
-  }();
-  return rt;
+  const size_t rrows = (size_t)hp + 1, xrows = (size_t)hp + 2;
+  return (size_t)ring_slots<S>() * kChunks * rrows * 16 + (size_t)5 * S * xrows * 16 +
+         (4 + ring_slots<S>()) * sizeof(uint64_t);
 }
 
 constexpr size_t kMaxSmem = 227 * 1024;
 
-// rows-per-CTA split: enough CTAs per pair to keep every band <= 256 rows and
+// rows-per-CTA split: enough CTAs per pair to keep every band <= 128 rows and
 // its ring in shared memory, and, for small batches, to spread a pair over
-// several SMs (the step rate of one band is bound by its SM's FP64 pipe).
+// several SMs (the step rate of one band is bound by its SM).
 template <int S>
-static int choose_cluster(int B, int H, int RT) {
+static int choose_cluster(int B, int H) {
   static const int forced = [] {
     const char* e = getenv("DIS_SOR_CLUSTER");  // experiments only
     return e ? atoi(e) : 0;
   }();
   if (forced > 0) return forced;
-  const int q = 32 * RT;
-  auto hp = [&](int C) { return ((H + C - 1) / C + q - 1) / q * q; };
+  auto hp = [&](int C) { return ((H + C - 1) / C + 31) / 32 * 32; };
   int C = 1;
-  while (C < 16 && (hp(C) > kMaxBandRows || hp(C) / RT * S > S * kMaxBandRows / RT ||
-                    sor_smem_bytes<S>(hp(C)) > kMaxSmem))
-    ++C;
-  // a band's step time scales with its rows: while the batch leaves SMs idle,
-  // split the rows further (bands of >= 32 rows; the st.async halo exchange
-  // costs ~0.15 us per step)
+  while (C < 16 && (hp(C) > kMaxBandRows || sor_smem_bytes<S>(hp(C)) > kMaxSmem)) ++C;
   static const int sms = [] {
     int dev = 0, n = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n > 0 ? n : 148;
   }();
+  // while the batch leaves SMs idle, split the rows further (bands of >= 32
+  // rows; the st.async halo exchange costs ~0.15 us per step)
   while (C < 16 && B * (C + 1) <= sms && (H + C) / (C + 1) >= 32) ++C;
   return C;
 }
 
-template <int S, int RT, bool HZ>
-static int launch_sor_rt(const RefineArgs& a, size_t Ls, const double* dui, const double* dvi,
-                         double* duo, double* dvo, bool final_pass, cudaStream_t st) {
-  const int C = choose_cluster<S>(a.B, a.H, RT);
+template <int S, bool HZ>
+static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const double* dvi,
+                        double* duo, double* dvo, bool final_pass, cudaStream_t st) {
+  const int C = choose_cluster<S>(a.B, a.H);
   const int Hc = (a.H + C - 1) / C;
-  const int q = 32 * RT;
-  const int hp = (Hc + q - 1) / q * q;
-  const int threads = hp / RT * S;
+  const int hp = (Hc + 31) / 32 * 32;
+  const int threads = hp * S + 32;  // + the producer warp
   const size_t smem = sor_smem_bytes<S>(hp);
   if (hp > kMaxBandRows || smem > kMaxSmem) return DIS_ERR_VALUE;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_sor<S, RT, HZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_sor<S, HZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kMaxSmem);
-    cudaFuncSetAttribute(k_sor<S, RT, HZ>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_sor<S, HZ>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -672,30 +660,21 @@ static int launch_sor_rt(const RefineArgs& a, size_t Ls, const double* dui, cons
   cfg.numAttrs = 1;
   double* fu = final_pass ? a.fu : nullptr;
   double* fv = final_pass ? a.fv : nullptr;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_sor<S, RT, HZ>, (const double*)a.rec, a.B, a.W, a.H,
-                                     Hc, Ls, a.omega, dui, dvi, duo, dvo, fu, fv, a.status);
+  const double* zeros = a.rec + (size_t)(kRec + 2) * a.B * Ls;  // zeroed by k_tensor_assemble
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_sor<S, HZ>, (const double*)a.rec, a.B, a.W, a.H,
+                                     Hc, Ls, a.omega, dui, dvi, duo, dvo, fu, fv, a.status,
+                                     zeros);
   return e == cudaSuccess ? DIS_OK : DIS_ERR_CUDA;
-}
-
-template <int S>
-static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const double* dvi,
-                        double* duo, double* dvo, bool final_pass, cudaStream_t st) {
-  // stereo (horizontal_only): one row per thread
-  if (a.horizontal) return launch_sor_rt<S, 1, true>(a, Ls, dui, dvi, duo, dvo, final_pass, st);
-  // more than 5 sweeps: the per-row shared memory grows, keep one row per thread
-  const int rt = S > 5 ? 1 : sor_rows_per_thread();
-  if (rt == 4) return launch_sor_rt<S, 4, false>(a, Ls, dui, dvi, duo, dvo, final_pass, st);
-  if (rt == 2) return launch_sor_rt<S, 2, false>(a, Ls, dui, dvi, duo, dvo, final_pass, st);
-  return launch_sor_rt<S, 1, false>(a, Ls, dui, dvi, duo, dvo, final_pass, st);
 }
 
 static int launch_sor(const RefineArgs& a, size_t Ls, int S, const double* dui,
                       const double* dvi, double* duo, double* dvo, bool final_pass,
                       cudaStream_t st) {
   switch (S) {
-#define DIS_SOR_CASE(n) \
-  case n:               \
-    return launch_sor_t<n>(a, Ls, dui, dvi, duo, dvo, final_pass, st);
+#define DIS_SOR_CASE(n)                                                                 \
+  case n:                                                                               \
+    return a.horizontal ? launch_sor_t<n, true>(a, Ls, dui, dvi, duo, dvo, final_pass, st) \
+                        : launch_sor_t<n, false>(a, Ls, dui, dvi, duo, dvo, final_pass, st);
     DIS_SOR_CASE(1)
     DIS_SOR_CASE(2)
     DIS_SOR_CASE(3)
@@ -711,9 +690,9 @@ static int launch_sor(const RefineArgs& a, size_t Ls, int S, const double* dui,
 }
 
 int launch_refine(const RefineArgs& a, cudaStream_t st) {
-  if (a.H > 2048) return DIS_ERR_VALUE;  // at most 8 CTAs of <= 256 rows per pair
+  if (a.H > 2048) return DIS_ERR_VALUE;  // at most 16 CTAs of <= 128 rows per pair
   const size_t Ls = (size_t)(a.W + a.H - 1) * a.H;
-  double* carry_u = a.rec + (size_t)kRecords * a.B * Ls;
+  double* carry_u = a.rec + (size_t)kRec * a.B * Ls;
   double* carry_v = carry_u + (size_t)a.B * Ls;
   dim3 tb(256);
   dim3 tg((a.W + kTTX - 1) / kTTX, (a.H + kTTY - 1) / kTTY, a.B);
