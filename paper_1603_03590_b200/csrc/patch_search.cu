@@ -358,35 +358,46 @@ __device__ __forceinline__ bool window_regular(double bx, double by, int W, int 
 
 // One window evaluation (the reference's two passes, inverse_search.py:
 // 130-152) for a regular window: rows loaded once each as contiguous
-// segments with immediate-offset loads.  Sample (oy, c) is _bilin's
-// a + fy*(b - a) with a = row(oy)[c] + fx_c*(row(oy)[c+1] - row(oy)[c]) and b
-// the same expression on row oy+1; since fx_c depends on the column alone,
-// b of row oy IS a of row oy+1 (same operands, same operations), so each
-// row's horizontal interpolants are computed once and carried down.
-template <int PS>
+// segments with immediate-offset loads, one row ahead of the arithmetic (the
+// next row's loads are in flight while this row is interpolated).  Sample
+// (oy, c) is _bilin's a + fy*(b - a) with a = row(oy)[c] + fx_c*(row(oy)[c+1]
+// - row(oy)[c]) and b the same expression on row oy+1; since fx_c depends on
+// the column alone, b of row oy IS a of row oy+1 (same operands, same
+// operations), so each row's horizontal interpolants are computed once and
+// carried down.  CODE is the residual norm (_transform_residual).
+template <int PS, int CODE>
 __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
                                              const double* __restrict__ ref,
                                              const double* __restrict__ rgx,
                                              const double* __restrict__ rgy, int W, int H,
                                              int x0i, int y0i, double by, const double* FX,
                                              int xbase, int ybase, double mean_t, bool mean_norm,
-                                             int code, double hb, bool tmpl128, double& off,
-                                             double& ssd, double& b0, double& b1, double& mar) {
+                                             double hb, bool tmpl128, double& off, double& ssd,
+                                             double& b0, double& b1, double& mar) {
   constexpr int S1 = PS + 1;
   const double dn = (double)(PS * PS);
+  // row oy of the window: elements idx .. idx + PS, idx = (ybase + oy)W + xbase
+  auto load_row = [&](size_t idx, double* s) {
+#pragma unroll
+    for (int c = 0; c < S1; ++c) s[c] = __ldg(qry + idx + c);
+  };
   double wsum = 0.0;
   {
-    const double* g = qry + (size_t)ybase * W + xbase;
-    double A[PS], s1[S1];
-#pragma unroll
-    for (int c = 0; c < S1; ++c) s1[c] = __ldg(g + c);
+    size_t idx = (size_t)ybase * W + xbase;
+    double A[PS], s1[S1], s2[S1];
+    load_row(idx, s1);
+    idx += W;
+    load_row(idx, s2);
 #pragma unroll
     for (int c = 0; c < PS; ++c) A[c] = s1[c] + FX[c] * (s1[c + 1] - s1[c]);
     for (int oy = 0; oy < PS; ++oy) {
-      const double fy = axis_sample(by + oy, H).f;
-      g += W;
 #pragma unroll
-      for (int c = 0; c < S1; ++c) s1[c] = __ldg(g + c);
+      for (int c = 0; c < S1; ++c) s1[c] = s2[c];
+      if (oy + 1 < PS) {  // row oy + 2 in flight during this row's arithmetic
+        idx += W;
+        load_row(idx, s2);
+      }
+      const double fy = axis_sample(by + oy, H).f;
 #pragma unroll
       for (int ox = 0; ox < PS; ++ox) {
         const double Bv = s1[ox] + FX[ox] * (s1[ox + 1] - s1[ox]);
@@ -403,26 +414,30 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
   auto accumulate = [&](double val, double t, double gxv, double gyv) {
     const double e = val - off - t;
     mar += fabs(e);
-    const double et = transform_residual(e, code, hb);
+    const double et = transform_residual(e, CODE, hb);
     ssd += et * et;
     b0 += gxv * et;
     b1 += gyv * et;
   };
   {
-    const double* g = qry + (size_t)ybase * W + xbase;
-    double A[PS], s1[S1];
-#pragma unroll
-    for (int c = 0; c < S1; ++c) s1[c] = __ldg(g + c);
+    size_t idx = (size_t)ybase * W + xbase;
+    double A[PS], s1[S1], s2[S1];
+    load_row(idx, s1);
+    idx += W;
+    load_row(idx, s2);
 #pragma unroll
     for (int c = 0; c < PS; ++c) A[c] = s1[c] + FX[c] * (s1[c + 1] - s1[c]);
     const double* tr = ref + (size_t)y0i * W + x0i;
     const double* gxr = rgx + (size_t)y0i * W + x0i;
     const double* gyr = rgy + (size_t)y0i * W + x0i;
     for (int oy = 0; oy < PS; ++oy) {
-      const double fy = axis_sample(by + oy, H).f;
-      g += W;
 #pragma unroll
-      for (int c = 0; c < S1; ++c) s1[c] = __ldg(g + c);
+      for (int c = 0; c < S1; ++c) s1[c] = s2[c];
+      if (oy + 1 < PS) {
+        idx += W;
+        load_row(idx, s2);
+      }
+      const double fy = axis_sample(by + oy, H).f;
       if (tmpl128) {
 #pragma unroll
         for (int ox = 0; ox < PS; ox += 2) {
@@ -505,7 +520,7 @@ __device__ __forceinline__ void eval_general(const double* __restrict__ qry,
 // lanes read the same image rows and share L1 lines).  A patch whose next
 // window is not regular is parked (state to the spill list) and finished by
 // k_patch_gn_general — this keeps the warp on one code path.
-template <int PS>
+template <int PS, int CODE>
 __global__ void __launch_bounds__(256, 2) k_patch_gn(SearchArgs a,
                                                      const double* __restrict__ prep,
                                                      unsigned* counter, double* spill,
@@ -518,7 +533,10 @@ __global__ void __launch_bounds__(256, 2) k_patch_gn(SearchArgs a,
   const int W = a.W, H = a.H;
   const size_t plane = (size_t)W * H;
   const bool mean_norm = a.mean_norm != 0;
-  Lane L;
+  // the lane's Gauss-Newton state lives in shared memory (touched a few
+  // times per window evaluation): the registers go to the window rows
+  __shared__ Lane lanes[256];
+  Lane& L = lanes[threadIdx.x];
   L.pid = -1;
   bool done = false;
   unsigned pool_next = 0, pool_end = 0;  // warp-uniform
@@ -565,9 +583,9 @@ __global__ void __launch_bounds__(256, 2) k_patch_gn(SearchArgs a,
     const bool tmpl128 = (PS & 1) == 0 && __all_sync(__activemask(), tal);
     const size_t po = (size_t)L.b * plane;
     double off, ssd, b0, b1, mar;
-    eval_regular<PS>(a.qry + po, a.ref + po, a.rgx + po, a.rgy + po, W, H, L.x0i, L.y0i, by,
-                     FX, xbase, ybase, L.mean_t, mean_norm, a.code, a.hb, tmpl128, off, ssd, b0,
-                     b1, mar);
+    eval_regular<PS, CODE>(a.qry + po, a.ref + po, a.rgx + po, a.rgy + po, W, H, L.x0i, L.y0i,
+                           by, FX, xbase, ybase, L.mean_t, mean_norm, a.hb, tmpl128, off, ssd,
+                           b0, b1, mar);
     gn_update(L, a, PS, off, ssd, b0, b1, mar);
   }
 }
@@ -768,6 +786,35 @@ static void launch_gn_group(const SearchArgs& a, const double* prep, unsigned* c
                                                    from_spill);
 }
 
+template <int PS, int CODE>
+static void launch_gn_lane_code(const SearchArgs& a, const double* prep, unsigned* counter,
+                                double* spill, unsigned* spill_count, size_t n, int sms,
+                                cudaStream_t st) {
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_patch_gn<PS, CODE>, 256, 0);
+    if (per_sm < 1) per_sm = 1;
+  }
+  size_t blocks = (size_t)per_sm * sms;
+  const size_t need = (n + 255) / 256;
+  if (blocks > need) blocks = need;
+  k_patch_gn<PS, CODE><<<(unsigned)blocks, 256, 0, st>>>(a, prep, counter, spill, spill_count);
+}
+
+static int sm_count();
+
+template <int PS>
+static void launch_gn_lane(const SearchArgs& a, const double* prep, unsigned* counter,
+                           double* spill, unsigned* spill_count, size_t n, cudaStream_t st) {
+  const int sms = sm_count();
+  if (a.code == DIS_NORM_L1)
+    launch_gn_lane_code<PS, DIS_NORM_L1>(a, prep, counter, spill, spill_count, n, sms, st);
+  else if (a.code == DIS_NORM_HUBER)
+    launch_gn_lane_code<PS, DIS_NORM_HUBER>(a, prep, counter, spill, spill_count, n, sms, st);
+  else
+    launch_gn_lane_code<PS, DIS_NORM_L2>(a, prep, counter, spill, spill_count, n, sms, st);
+}
+
 static int sm_count() {
   static int sms = 0;
   if (!sms) {
@@ -809,22 +856,10 @@ void launch_patch_search(const SearchArgs& a, void* scratch, cudaStream_t st) {
       launch_gn_group<12, 16>(a, prep, counter, n, st);
     note_launch();
   } else if (a.ps == 8 || a.ps == 12) {
-    static int per_sm8 = 0, per_sm12 = 0;
-    int& per_sm = a.ps == 8 ? per_sm8 : per_sm12;
-    if (!per_sm) {
-      if (a.ps == 8)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_patch_gn<8>, 256, 0);
-      else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_patch_gn<12>, 256, 0);
-      if (per_sm < 1) per_sm = 1;
-    }
-    size_t blocks = (size_t)per_sm * sm_count();
-    const size_t need = (n + 255) / 256;
-    if (blocks > need) blocks = need;
     if (a.ps == 8)
-      k_patch_gn<8><<<(unsigned)blocks, 256, 0, st>>>(a, prep, counter, spill, spill_count);
+      launch_gn_lane<8>(a, prep, counter, spill, spill_count, n, st);
     else
-      k_patch_gn<12><<<(unsigned)blocks, 256, 0, st>>>(a, prep, counter, spill, spill_count);
+      launch_gn_lane<12>(a, prep, counter, spill, spill_count, n, st);
     note_launch();
     // parked (irregular-window) patches: a lane group per patch
     if (a.ps == 8)
