@@ -332,6 +332,13 @@ __device__ __forceinline__ double seg_sample(double i00, double i01, double i10,
   return a + fy * (bb - a);
 }
 
+// 256-bit read-only load of 4 doubles (32-byte aligned address)
+__device__ __forceinline__ void ldg256(const double* p, double* v) {
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+      : "l"(p));
+}
+
 // Is the window at (bx, by) "regular": its ps sample columns (rows) are the ps
 // consecutive pixels xbase.. (ybase..), each with its right (lower)
 // neighbour unclamped?  Then each sample's bilinear operands are segment
@@ -372,14 +379,27 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
                                              const double* __restrict__ rgy, int W, int H,
                                              int x0i, int y0i, double by, const double* FX,
                                              int xbase, int ybase, double mean_t, bool mean_norm,
-                                             double hb, bool tmpl128, double& off, double& ssd,
-                                             double& b0, double& b1, double& mar) {
+                                             double hb, bool tmpl128, bool tmpl256, double& off,
+                                             double& ssd, double& b0, double& b1, double& mar) {
   constexpr int S1 = PS + 1;
   const double dn = (double)(PS * PS);
-  // row oy of the window: elements idx .. idx + PS, idx = (ybase + oy)W + xbase
+  // row oy of the window: elements idx .. idx + PS, idx = (ybase + oy)W + xbase,
+  // read as 256-bit loads from the 32-byte aligned element at or below idx
+  // (one sector per lane per load instead of one per element) and shifted
+  // into place by the lane's offset o = idx mod 4 (two select levels)
   auto load_row = [&](size_t idx, double* s) {
+    constexpr int NV = (S1 + 3 + 3) / 4;  // 256-bit loads per row
+    const double* p = qry + idx;
+    const unsigned o = (unsigned)(((uintptr_t)p >> 3) & 3u);
+    const double* pa = p - o;
+    double v[4 * NV];
 #pragma unroll
-    for (int c = 0; c < S1; ++c) s[c] = __ldg(qry + idx + c);
+    for (int q = 0; q < NV; ++q) ldg256(pa + 4 * q, v + 4 * q);
+    double w[S1 + 1];
+#pragma unroll
+    for (int i = 0; i <= S1; ++i) w[i] = (o & 2u) ? v[i + 2] : v[i];
+#pragma unroll
+    for (int c = 0; c < S1; ++c) s[c] = (o & 1u) ? w[c + 1] : w[c];
   };
   double wsum = 0.0;
   {
@@ -438,7 +458,21 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
         load_row(idx, s2);
       }
       const double fy = axis_sample(by + oy, H).f;
-      if (tmpl128) {
+      if (tmpl256) {  // template rows 32-byte aligned across the warp
+#pragma unroll
+        for (int ox = 0; ox < PS; ox += 4) {
+          double t[4], gx[4], gy[4];
+          ldg256(tr + ox, t);
+          ldg256(gxr + ox, gx);
+          ldg256(gyr + ox, gy);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double Bv = s1[ox + q] + FX[ox + q] * (s1[ox + q + 1] - s1[ox + q]);
+            accumulate(A[ox + q] + fy * (Bv - A[ox + q]), t[q], gx[q], gy[q]);
+            A[ox + q] = Bv;
+          }
+        }
+      } else if (tmpl128) {
 #pragma unroll
         for (int ox = 0; ox < PS; ox += 2) {
           const double2 t = __ldg(reinterpret_cast<const double2*>(tr + ox));
@@ -579,13 +613,17 @@ __global__ void __launch_bounds__(256, 2) k_patch_gn(SearchArgs a,
       L.pid = -1;
       continue;
     }
-    const bool tal = ((((size_t)L.y0i * W + L.x0i) | (size_t)W) & 1) == 0;
-    const bool tmpl128 = (PS & 1) == 0 && __all_sync(__activemask(), tal);
     const size_t po = (size_t)L.b * plane;
+    // template rows at (y0i + oy) W + x0i of the pair's rasters: 16 / 32-byte
+    // aligned when the element offset and the row pitch are even / multiples of 4
+    const size_t toff = po + (size_t)L.y0i * W + L.x0i;
+    const unsigned am = __activemask();
+    const bool tmpl128 = (PS & 1) == 0 && __all_sync(am, ((toff | (size_t)W) & 1) == 0);
+    const bool tmpl256 = (PS & 3) == 0 && __all_sync(am, ((toff | (size_t)W) & 3) == 0);
     double off, ssd, b0, b1, mar;
     eval_regular<PS, CODE>(a.qry + po, a.ref + po, a.rgx + po, a.rgy + po, W, H, L.x0i, L.y0i,
-                           by, FX, xbase, ybase, L.mean_t, mean_norm, a.hb, tmpl128, off, ssd,
-                           b0, b1, mar);
+                           by, FX, xbase, ybase, L.mean_t, mean_norm, a.hb, tmpl128, tmpl256, off,
+                           ssd, b0, b1, mar);
     gn_update(L, a, PS, off, ssd, b0, b1, mar);
   }
 }

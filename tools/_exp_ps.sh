@@ -4,4 +4,4 @@ timeout 300 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu --config c1 
 import json,sys
 d=json.loads(sys.stdin.read())
 print('value %.0f ms %.3f' % (d['value'], d['ms_per_step']), {k: round(v['ms_per_step'],3) for k,v in d['kernels'].items()})"
-KERNELS="k_patch_gn:0" bash tools/_exp_prof.sh c > /dev/null 2>&1
+KERNELS="k_patch_gn:0" bash tools/_exp_prof.sh d > /dev/null 2>&1
