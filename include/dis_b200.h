@@ -254,9 +254,12 @@ DIS_API int dis_densify_bidirectional(const double* ref_img, const double* qry_i
 DIS_API size_t dis_refine_workspace_bytes(int32_t B, int32_t W, int32_t H);
 
 /* refine (variational.py:220-275) in place on flow_u/flow_v (p->mode == 1:
- * horizontal_only), running
- * `outer_iters` fixed-point iterations (pass params->outer_iters_fixed or
- * scale_index + 1).  ref_dd/qry_dd: 4 rasters each (gxx, gxy, gyx, gyy). */
+ * horizontal_only), running `outer_iters` fixed-point iterations (pass
+ * params->outer_iters_fixed or scale_index + 1).  ref_dd/qry_dd (the 4
+ * second-derivative rasters gxx, gxy, gyx, gyy of each level) are accepted
+ * for interface compatibility and may be NULL: the kernel forms them from
+ * the gradient rasters on the fly (_second_derivatives, variational.py:
+ * 168-171). */
 DIS_API int dis_refine(const double* ref_img, const double* ref_gx, const double* ref_gy,
                const double* ref_dd, const double* qry_img, const double* qry_gx,
                const double* qry_gy, const double* qry_dd, int32_t B, int32_t W,

@@ -156,7 +156,8 @@ void make_plan(const dis_params_t* p, int B, int H, int W, Plan* pl) {
       const bool used = s >= pl->sf;
       pl->off_gx[f][s] = used ? take(cur, n * d) : kNone;
       pl->off_gy[f][s] = used ? take(cur, n * d) : kNone;
-      pl->off_dd[f][s] = (used && pl->var) ? take(cur, 4 * n * d) : kNone;
+      // second derivatives are formed on the fly by the refinement
+      pl->off_dd[f][s] = kNone;
     }
   for (int s = pl->sf; s <= pl->ss; ++s) {
     const size_t P = (size_t)B * pl->ax[s].n * pl->ay[s].n;
@@ -284,11 +285,9 @@ int refine_scale(const Plan& pl, const dis_params_t* p, void* ws, int s, int dir
   r.ref = at<double>(ws, pl.off_img[dir][s]);
   r.rgx = at<double>(ws, pl.off_gx[dir][s]);
   r.rgy = at<double>(ws, pl.off_gy[dir][s]);
-  r.rdd = at<double>(ws, pl.off_dd[dir][s]);
   r.qry = at<double>(ws, pl.off_img[1 - dir][s]);
   r.qgx = at<double>(ws, pl.off_gx[1 - dir][s]);
   r.qgy = at<double>(ws, pl.off_gy[1 - dir][s]);
-  r.qdd = at<double>(ws, pl.off_dd[1 - dir][s]);
   r.B = pl.B;
   r.W = pl.ws[s];
   r.H = pl.hs[s];
@@ -1021,11 +1020,11 @@ int dis_refine(const double* ref_img, const double* ref_gx, const double* ref_gy
   r.ref = ref_img;
   r.rgx = ref_gx;
   r.rgy = ref_gy;
-  r.rdd = ref_dd;
+  (void)ref_dd;  // second derivatives are formed on the fly
   r.qry = qry_img;
   r.qgx = qry_gx;
   r.qgy = qry_gy;
-  r.qdd = qry_dd;
+  (void)qry_dd;
   r.B = B;
   r.W = W;
   r.H = H;

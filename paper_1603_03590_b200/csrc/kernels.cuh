@@ -79,11 +79,9 @@ struct RefineArgs {
   const double* ref;
   const double* rgx;
   const double* rgy;
-  const double* rdd;
   const double* qry;
   const double* qgx;
   const double* qgy;
-  const double* qdd;
   int B, W, H;
   double delta, gamma, alpha, eps, omega;
   int sweeps, outer;

@@ -58,8 +58,63 @@ size_t refine_scratch_doubles(int B, int W, int H) {
 // Tile of kTTX x kTTY pixels per block (one pixel per thread).
 constexpr int kTTX = 32, kTTY = 8;
 
+// image_gradients (core.py:75-85) of raster f at one pixel, computed on the
+// fly: the one-sided border forms are the central form with the index
+// clamped, 0.5 * (f[x+1] - f[x-1]) -> 0.5 * (f[1] - f[0]) at x = 0 and
+// 0.5 * (f[W-1] - f[W-2]) at x = W-1 (W, H >= 2).  Used for the second
+// derivatives _second_derivatives (variational.py:168-171) = the gradients
+// of the gradient rasters, so they never go through HBM.
+__device__ __forceinline__ double dx_at(const double* __restrict__ f, int W, int x, int y) {
+  const int xm = x > 0 ? x - 1 : 0, xp = x < W - 1 ? x + 1 : W - 1;
+  const size_t row = (size_t)y * W;
+  return 0.5 * (__ldg(f + row + xp) - __ldg(f + row + xm));
+}
+__device__ __forceinline__ double dy_at(const double* __restrict__ f, int W, int H, int x, int y) {
+  const int ym = y > 0 ? y - 1 : 0, yp = y < H - 1 ? y + 1 : H - 1;
+  return 0.5 * (__ldg(f + (size_t)yp * W + x) - __ldg(f + (size_t)ym * W + x));
+}
+
+// _bilin (inverse_search.py:34-58) set-up shared by every raster sampled at
+// the same warped coordinate (clamp, truncate, fractions)
+struct BilinAt {
+  int x0, x1, y0, y1;
+  double fx, fy;
+};
+__device__ __forceinline__ BilinAt bilin_at(int W, int H, double x, double y) {
+  if (!(x >= 0.0))
+    x = 0.0;
+  else if (x > W - 1.0)
+    x = W - 1.0;
+  if (!(y >= 0.0))
+    y = 0.0;
+  else if (y > H - 1.0)
+    y = H - 1.0;
+  BilinAt b;
+  b.x0 = (int)x;
+  b.y0 = (int)y;
+  b.x1 = b.x0 + 1 > W - 1 ? W - 1 : b.x0 + 1;
+  b.y1 = b.y0 + 1 > H - 1 ? H - 1 : b.y0 + 1;
+  b.fx = x - (double)b.x0;
+  b.fy = y - (double)b.y0;
+  return b;
+}
+__device__ __forceinline__ double bilin_mix(const BilinAt& b, double i00, double i01, double i10,
+                                            double i11) {
+  const double a = i00 + b.fx * (i01 - i00);
+  const double bb = i10 + b.fx * (i11 - i10);
+  return a + b.fy * (bb - a);
+}
+__device__ __forceinline__ double bilin_raster(const double* __restrict__ f, int W,
+                                               const BilinAt& b) {
+  const double* r0 = f + (size_t)b.y0 * W;
+  const double* r1 = f + (size_t)b.y1 * W;
+  return bilin_mix(b, __ldg(r0 + b.x0), __ldg(r0 + b.x1), __ldg(r1 + b.x0), __ldg(r1 + b.x1));
+}
+
 // _tensor_fields (variational.py:36-88) + the system part of _assemble_system
-// (91-118) at one pixel: u, v, m00, m01, m11, r0, r1.
+// (91-118) at one pixel: u, v, m00, m01, m11, r0, r1.  The second
+// derivatives of both levels (and their bilinear samples at the warped
+// position) are formed from the gradient rasters on the fly.
 __device__ __forceinline__ void pixel_system(const RefineArgs& a, int b, int x, int y,
                                              double* r) {
   const int W = a.W, H = a.H;
@@ -70,11 +125,9 @@ __device__ __forceinline__ void pixel_system(const RefineArgs& a, int b, int x, 
   const double* __restrict__ ref = a.ref + b * plane;
   const double* __restrict__ rgx = a.rgx + b * plane;
   const double* __restrict__ rgy = a.rgy + b * plane;
-  const double* __restrict__ rdd = a.rdd + b * 4 * plane;
   const double* __restrict__ qry = a.qry + b * plane;
   const double* __restrict__ qgx = a.qgx + b * plane;
   const double* __restrict__ qgy = a.qgy + b * plane;
-  const double* __restrict__ qdd = a.qdd + b * 4 * plane;
 
   const double up_ = u[p], vp_ = v[p];
   double t0xx = 0.0, t0xy = 0.0, t0xz = 0.0, t0yy = 0.0, t0yz = 0.0, t0zz = 0.0;
@@ -83,9 +136,10 @@ __device__ __forceinline__ void pixel_system(const RefineArgs& a, int b, int x, 
   const double wyp = y + vp_;
   if (!(x == 0 || x == W - 1 || y == 0 || y == H - 1 || wxp < 0.0 || wxp > W - 1.0 ||
         wyp < 0.0 || wyp > H - 1.0)) {
-    const double iw = bilin_nb(qry, W, H, wxp, wyp);
-    const double gxw = bilin_nb(qgx, W, H, wxp, wyp);
-    const double gyw = bilin_nb(qgy, W, H, wxp, wyp);
+    const BilinAt bl = bilin_at(W, H, wxp, wyp);
+    const double iw = bilin_raster(qry, W, bl);
+    const double gxw = bilin_raster(qgx, W, bl);
+    const double gyw = bilin_raster(qgy, W, bl);
     const double rgxp = rgx[p], rgyp = rgy[p];
     const double ix = 0.5 * (rgxp + gxw);
     const double iy = 0.5 * (rgyp + gyw);
@@ -97,11 +151,23 @@ __device__ __forceinline__ void pixel_system(const RefineArgs& a, int b, int x, 
     t0yy = b0 * iy * iy;
     t0yz = b0 * iy * iz;
     t0zz = b0 * iz * iz;
-    const double ixx = 0.5 * (rdd[p] + bilin_nb(qdd, W, H, wxp, wyp));
-    const double ixy = 0.5 * (rdd[plane + p] + bilin_nb(qdd + plane, W, H, wxp, wyp));
+    // second derivatives: reference level at the pixel, query level sampled
+    // at the warped position from its four corners
+    const double qxx = bilin_mix(bl, dx_at(qgx, W, bl.x0, bl.y0), dx_at(qgx, W, bl.x1, bl.y0),
+                                 dx_at(qgx, W, bl.x0, bl.y1), dx_at(qgx, W, bl.x1, bl.y1));
+    const double qxy =
+        bilin_mix(bl, dy_at(qgx, W, H, bl.x0, bl.y0), dy_at(qgx, W, H, bl.x1, bl.y0),
+                  dy_at(qgx, W, H, bl.x0, bl.y1), dy_at(qgx, W, H, bl.x1, bl.y1));
+    const double qyx = bilin_mix(bl, dx_at(qgy, W, bl.x0, bl.y0), dx_at(qgy, W, bl.x1, bl.y0),
+                                 dx_at(qgy, W, bl.x0, bl.y1), dx_at(qgy, W, bl.x1, bl.y1));
+    const double qyy =
+        bilin_mix(bl, dy_at(qgy, W, H, bl.x0, bl.y0), dy_at(qgy, W, H, bl.x1, bl.y0),
+                  dy_at(qgy, W, H, bl.x0, bl.y1), dy_at(qgy, W, H, bl.x1, bl.y1));
+    const double ixx = 0.5 * (dx_at(rgx, W, x, y) + qxx);
+    const double ixy = 0.5 * (dy_at(rgx, W, H, x, y) + qxy);
     const double ixz = gxw - rgxp;
-    const double iyx = 0.5 * (rdd[2 * plane + p] + bilin_nb(qdd + 2 * plane, W, H, wxp, wyp));
-    const double iyy = 0.5 * (rdd[3 * plane + p] + bilin_nb(qdd + 3 * plane, W, H, wxp, wyp));
+    const double iyx = 0.5 * (dx_at(rgy, W, x, y) + qyx);
+    const double iyy = 0.5 * (dy_at(rgy, W, H, x, y) + qyy);
     const double iyz = gyw - rgyp;
     const double bx = 1.0 / (ixx * ixx + ixy * ixy + 0.01);
     const double by = 1.0 / (iyx * iyx + iyy * iyy + 0.01);
@@ -195,16 +261,20 @@ __global__ void __launch_bounds__(256, 3) k_tensor_assemble(RefineArgs a, size_t
   __syncthreads();
   // diagonal runs: diagonal d = X0 + Y0 + dd holds tile rows ly with
   // lx = dd - ly in the tile; chunk c of those records is the contiguous run
-  // [(d * kChunks + c) * H + y] of the layout
-  const int ndd = kTTX + kTTY - 1;
+  // [(d * kChunks + c) * H + y] of the layout.  Lane -> (row ly = lane % 8,
+  // slot = lane / 8); the warp's four slots take consecutive (diagonal,
+  // chunk) pairs, so 8 lanes write one 128-byte run.
+  static_assert(kTTY == 8, "one 8-lane group per diagonal run");
+  constexpr int ndd = kTTX + kTTY - 1;
+  constexpr int npairs = ndd * kChunks;
   double2* __restrict__ out = reinterpret_cast<double2*>(a.rec + (size_t)b * Ls * kRec);
-  for (int i = threadIdx.x; i < kChunks * ndd * kTTY; i += 256) {
-    const int ly = i % kTTY;
-    const int rest = i / kTTY;
-    const int c = rest % kChunks;
-    const int dd = rest / kChunks;
+  const int ly = threadIdx.x & 7;
+  const int y = Y0 + ly;
+  for (int m = (threadIdx.x >> 3); m < npairs; m += 32) {
+    const int dd = m / kChunks;
+    const int c = m - dd * kChunks;
     const int lxx = dd - ly;
-    const int x = X0 + lxx, y = Y0 + ly;
+    const int x = X0 + lxx;
     if (lxx < 0 || lxx >= kTTX || x >= W || y >= H) continue;
     const size_t d = (size_t)(x + y);
     out[(d * kChunks + c) * H + y] = rs[ly * kTTX + lxx][c];
