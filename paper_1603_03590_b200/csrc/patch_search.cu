@@ -382,12 +382,18 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
                                              double hb, bool tmpl128, bool tmpl256, double& off,
                                              double& ssd, double& b0, double& b1, double& mar) {
   constexpr int S1 = PS + 1;
+  constexpr bool kPre = PS <= 8;  // one-row-ahead loads (register budget)
   const double dn = (double)(PS * PS);
   // row oy of the window: elements idx .. idx + PS, idx = (ybase + oy)W + xbase,
   // read as 256-bit loads from the 32-byte aligned element at or below idx
   // (one sector per lane per load instead of one per element) and shifted
   // into place by the lane's offset o = idx mod 4 (two select levels)
   auto load_row = [&](size_t idx, double* s) {
+    if (PS > 8) {  // (wider rows: the shift registers cost more than the loads save)
+#pragma unroll
+      for (int c = 0; c < S1; ++c) s[c] = __ldg(qry + idx + c);
+      return;
+    }
     constexpr int NV = (S1 + 3 + 3) / 4;  // 256-bit loads per row
     const double* p = qry + idx;
     const unsigned o = (unsigned)(((uintptr_t)p >> 3) & 3u);
@@ -404,18 +410,25 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
   double wsum = 0.0;
   {
     size_t idx = (size_t)ybase * W + xbase;
-    double A[PS], s1[S1], s2[S1];
+    double A[PS], s1[S1], s2[kPre ? S1 : 1];
     load_row(idx, s1);
-    idx += W;
-    load_row(idx, s2);
+    if (kPre) {
+      idx += W;
+      load_row(idx, s2);
+    }
 #pragma unroll
     for (int c = 0; c < PS; ++c) A[c] = s1[c] + FX[c] * (s1[c + 1] - s1[c]);
     for (int oy = 0; oy < PS; ++oy) {
+      if (kPre) {
 #pragma unroll
-      for (int c = 0; c < S1; ++c) s1[c] = s2[c];
-      if (oy + 1 < PS) {  // row oy + 2 in flight during this row's arithmetic
+        for (int c = 0; c < S1; ++c) s1[c] = s2[c];
+        if (oy + 1 < PS) {  // row oy + 2 in flight during this row's arithmetic
+          idx += W;
+          load_row(idx, s2);
+        }
+      } else {
         idx += W;
-        load_row(idx, s2);
+        load_row(idx, s1);
       }
       const double fy = axis_sample(by + oy, H).f;
 #pragma unroll
@@ -441,21 +454,28 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
   };
   {
     size_t idx = (size_t)ybase * W + xbase;
-    double A[PS], s1[S1], s2[S1];
+    double A[PS], s1[S1], s2[kPre ? S1 : 1];
     load_row(idx, s1);
-    idx += W;
-    load_row(idx, s2);
+    if (kPre) {
+      idx += W;
+      load_row(idx, s2);
+    }
 #pragma unroll
     for (int c = 0; c < PS; ++c) A[c] = s1[c] + FX[c] * (s1[c + 1] - s1[c]);
     const double* tr = ref + (size_t)y0i * W + x0i;
     const double* gxr = rgx + (size_t)y0i * W + x0i;
     const double* gyr = rgy + (size_t)y0i * W + x0i;
     for (int oy = 0; oy < PS; ++oy) {
+      if (kPre) {
 #pragma unroll
-      for (int c = 0; c < S1; ++c) s1[c] = s2[c];
-      if (oy + 1 < PS) {
+        for (int c = 0; c < S1; ++c) s1[c] = s2[c];
+        if (oy + 1 < PS) {
+          idx += W;
+          load_row(idx, s2);
+        }
+      } else {
         idx += W;
-        load_row(idx, s2);
+        load_row(idx, s1);
       }
       const double fy = axis_sample(by + oy, H).f;
       if (tmpl256) {  // template rows 32-byte aligned across the warp
