@@ -10,6 +10,7 @@
 #include <mutex>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -543,9 +544,20 @@ size_t dis_workspace_bytes(int32_t B, int32_t H, int32_t W, const dis_params_t* 
 // overlap (the two copy directions run on separate copy engines, concurrently
 // with the kernels of other chunks).
 namespace {
-constexpr int kHostChunksMax = 4;
+constexpr int kHostChunksMax = 16;
 
-int host_chunks(int B) { return B >= kHostChunksMax ? kHostChunksMax : (B < 1 ? 1 : B); }
+// chunks of the host-buffer pipeline: more chunks overlap more of the copies
+// (the first H2D and the last D2H are exposed) at the cost of smaller kernels
+// (measured on c1/c3: 8 pairs per chunk, 4..16 chunks)
+int host_chunks(int B) {
+  static const int forced = [] {
+    const char* e = getenv("DIS_HOST_CHUNKS");  // experiments only
+    return e ? atoi(e) : 0;
+  }();
+  int want = forced > 0 ? forced : B / 8;
+  want = want < 4 ? 4 : (want > kHostChunksMax ? kHostChunksMax : want);
+  return B >= want ? want : (B < 1 ? 1 : B);
+}
 
 size_t host_chunk_bytes(int Bc, int H, int W, int dtype, const dis_params_t* p) {
   size_t base = dis_workspace_bytes(Bc, H, W, p);
