@@ -52,6 +52,13 @@ __device__ __forceinline__ bool hypot_gt(double a, double b, int ps) {
   return (s - t_hi) + (lo - t_lo) > 0.0;
 }
 
+// 256-bit read-only load of 4 doubles (32-byte aligned address)
+__device__ __forceinline__ void ldg256(const double* p, double* v) {
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+      : "l"(p));
+}
+
 // ---------------------------------------------------------------------------
 // Stage 1 — per-patch prep (one thread per patch): init_patches,
 // _patch_precompute and _condition_hessians.  Writes the kPrep record the
@@ -97,16 +104,32 @@ __global__ void __launch_bounds__(128) k_patch_prep(SearchArgs a, double* __rest
   // ---- _patch_precompute (inverse_search.py:75-98) ----
   // samples at integer coordinates: the reference's _bilin returns the pixel
   double tsum = 0.0, h00 = 0.0, h01 = 0.0, h11 = 0.0;
-  for (int oy = 0; oy < ps; ++oy) {
-    const size_t row = (size_t)(y0i + oy) * W + x0i;
-    for (int ox = 0; ox < ps; ++ox) {
-      const double t = __ldg(ref + row + ox);
-      const double gxv = __ldg(rgx + row + ox);
-      const double gyv = __ldg(rgy + row + ox);
-      tsum += t;
-      h00 += gxv * gxv;
-      h01 += gxv * gyv;
-      h11 += gyv * gyv;
+  auto add = [&](double t, double gxv, double gyv) {
+    tsum += t;
+    h00 += gxv * gxv;
+    h01 += gxv * gyv;
+    h11 += gyv * gyv;
+  };
+  // rows 32-byte aligned (element offset and pitch multiples of 4, e.g. grid
+  // spacing 4): 256-bit loads, one sector per lane per load
+  const size_t off0 = (size_t)b * plane + (size_t)y0i * W + x0i;
+  if ((ps & 3) == 0 && ((off0 | (size_t)W) & 3) == 0) {
+    for (int oy = 0; oy < ps; ++oy) {
+      const size_t row = (size_t)(y0i + oy) * W + x0i;
+      for (int ox = 0; ox < ps; ox += 4) {
+        double t[4], gx4[4], gy4[4];
+        ldg256(ref + row + ox, t);
+        ldg256(rgx + row + ox, gx4);
+        ldg256(rgy + row + ox, gy4);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) add(t[q], gx4[q], gy4[q]);
+      }
+    }
+  } else {
+    for (int oy = 0; oy < ps; ++oy) {
+      const size_t row = (size_t)(y0i + oy) * W + x0i;
+      for (int ox = 0; ox < ps; ++ox)
+        add(__ldg(ref + row + ox), __ldg(rgx + row + ox), __ldg(rgy + row + ox));
     }
   }
   const double dn = (double)(ps * ps);
@@ -330,13 +353,6 @@ __device__ __forceinline__ double seg_sample(double i00, double i01, double i10,
   const double a = i00 + fx * (i01 - i00);
   const double bb = i10 + fx * (i11 - i10);
   return a + fy * (bb - a);
-}
-
-// 256-bit read-only load of 4 doubles (32-byte aligned address)
-__device__ __forceinline__ void ldg256(const double* p, double* v) {
-  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
-      : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
-      : "l"(p));
 }
 
 // Is the window at (bx, by) "regular": its ps sample columns (rows) are the ps
