@@ -709,7 +709,7 @@ __global__ void __launch_bounds__(128) k_patch_gn_general(SearchArgs a,
 // same order as the reference's loop.  All lanes of a group hold the same
 // patch state and apply the same update.
 // ---------------------------------------------------------------------------
-template <int PS, int G>
+template <int PS, int G, int CODE>
 __global__ void __launch_bounds__(128) k_patch_gn_group(SearchArgs a,
                                                          const double* __restrict__ prep,
                                                          unsigned* counter,
@@ -808,14 +808,28 @@ __global__ void __launch_bounds__(128) k_patch_gn_group(SearchArgs a,
     // pass 2: the addends of my row, then the four sums in row order
     const size_t row = po + (size_t)(L.y0i + rr_row) * W + L.x0i;
     double EA[PS], E2[PS], EX[PS], EY[PS];
-#pragma unroll
-    for (int c = 0; c < PS; ++c) {
-      const double e = val[c] - off - __ldg(a.ref + row + c);
+    auto addends = [&](int c, double t, double gxv, double gyv) {
+      const double e = val[c] - off - t;
       EA[c] = fabs(e);
-      const double et = transform_residual(e, a.code, a.hb);
+      const double et = transform_residual(e, CODE, a.hb);
       E2[c] = et * et;
-      EX[c] = __ldg(a.rgx + row + c) * et;
-      EY[c] = __ldg(a.rgy + row + c) * et;
+      EX[c] = gxv * et;
+      EY[c] = gyv * et;
+    };
+    if ((PS & 3) == 0 && ((row | (size_t)W) & 3) == 0) {  // 32-byte aligned template row
+#pragma unroll
+      for (int c = 0; c < PS; c += 4) {
+        double t[4], gx4[4], gy4[4];
+        ldg256(a.ref + row + c, t);
+        ldg256(a.rgx + row + c, gx4);
+        ldg256(a.rgy + row + c, gy4);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) addends(c + q, t[q], gx4[q], gy4[q]);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < PS; ++c)
+        addends(c, __ldg(a.ref + row + c), __ldg(a.rgx + row + c), __ldg(a.rgy + row + c));
     }
     double mar = 0.0, ssd = 0.0, b0 = 0.0, b1 = 0.0;
 #pragma unroll
@@ -840,14 +854,15 @@ __global__ void __launch_bounds__(128) k_patch_gn_group(SearchArgs a,
   }
 }
 
-template <int PS, int G>
-static void launch_gn_group(const SearchArgs& a, const double* prep, unsigned* counter,
-                            size_t n, cudaStream_t st, const double* spill = nullptr,
-                            const unsigned* spill_count = nullptr, bool from_spill = false) {
+template <int PS, int G, int CODE>
+static void launch_gn_group_code(const SearchArgs& a, const double* prep, unsigned* counter,
+                                 size_t n, cudaStream_t st, const double* spill,
+                                 const unsigned* spill_count, bool from_spill) {
   static int cap = 0;
   if (!cap) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_patch_gn_group<PS, G>, 128, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_patch_gn_group<PS, G, CODE>, 128,
+                                                  0);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -856,8 +871,23 @@ static void launch_gn_group(const SearchArgs& a, const double* prep, unsigned* c
   const size_t need = (n * G + 127) / 128;
   int blocks = (int)(need < (size_t)cap ? need : (size_t)cap);
   if (blocks < 1) blocks = 1;
-  k_patch_gn_group<PS, G><<<blocks, 128, 0, st>>>(a, prep, counter, spill, spill_count,
-                                                   from_spill);
+  k_patch_gn_group<PS, G, CODE><<<blocks, 128, 0, st>>>(a, prep, counter, spill, spill_count,
+                                                         from_spill);
+}
+
+template <int PS, int G>
+static void launch_gn_group(const SearchArgs& a, const double* prep, unsigned* counter,
+                            size_t n, cudaStream_t st, const double* spill = nullptr,
+                            const unsigned* spill_count = nullptr, bool from_spill = false) {
+  if (a.code == DIS_NORM_L1)
+    launch_gn_group_code<PS, G, DIS_NORM_L1>(a, prep, counter, n, st, spill, spill_count,
+                                             from_spill);
+  else if (a.code == DIS_NORM_HUBER)
+    launch_gn_group_code<PS, G, DIS_NORM_HUBER>(a, prep, counter, n, st, spill, spill_count,
+                                                from_spill);
+  else
+    launch_gn_group_code<PS, G, DIS_NORM_L2>(a, prep, counter, n, st, spill, spill_count,
+                                             from_spill);
 }
 
 template <int PS, int CODE>
