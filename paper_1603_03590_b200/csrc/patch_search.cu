@@ -59,6 +59,24 @@ __device__ __forceinline__ void ldg256(const double* p, double* v) {
       : "l"(p));
 }
 
+// N consecutive doubles p[0 .. N-1] (8-byte aligned p) as 256-bit loads from
+// the 32-byte aligned address at or below p, shifted into place by the
+// lane's offset o = (p / 8) mod 4 with two select levels
+template <int N>
+__device__ __forceinline__ void load_run256(const double* p, double* s) {
+  constexpr int NV = (N + 3 + 3) / 4;
+  const unsigned o = (unsigned)(((uintptr_t)p >> 3) & 3u);
+  const double* pa = p - o;
+  double v[4 * NV];
+#pragma unroll
+  for (int q = 0; q < NV; ++q) ldg256(pa + 4 * q, v + 4 * q);
+  double w[N + 1];
+#pragma unroll
+  for (int i = 0; i <= N; ++i) w[i] = (o & 2u) ? v[i + 2] : v[i];
+#pragma unroll
+  for (int c = 0; c < N; ++c) s[c] = (o & 1u) ? w[c + 1] : w[c];
+}
+
 // ---------------------------------------------------------------------------
 // Stage 1 — per-patch prep (one thread per patch): init_patches,
 // _patch_precompute and _condition_hessians.  Writes the kPrep record the
@@ -410,18 +428,7 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
       for (int c = 0; c < S1; ++c) s[c] = __ldg(qry + idx + c);
       return;
     }
-    constexpr int NV = (S1 + 3 + 3) / 4;  // 256-bit loads per row
-    const double* p = qry + idx;
-    const unsigned o = (unsigned)(((uintptr_t)p >> 3) & 3u);
-    const double* pa = p - o;
-    double v[4 * NV];
-#pragma unroll
-    for (int q = 0; q < NV; ++q) ldg256(pa + 4 * q, v + 4 * q);
-    double w[S1 + 1];
-#pragma unroll
-    for (int i = 0; i <= S1; ++i) w[i] = (o & 2u) ? v[i + 2] : v[i];
-#pragma unroll
-    for (int c = 0; c < S1; ++c) s[c] = (o & 1u) ? w[c + 1] : w[c];
+    load_run256<S1>(qry + idx, s);
   };
   double wsum = 0.0;
   {
@@ -777,10 +784,15 @@ __global__ void __launch_bounds__(128) k_patch_gn_group(SearchArgs a,
       const double* r0 = qry + (size_t)ay.i0 * W + xbase;
       const double* r1 = qry + (size_t)ay.i1 * W + xbase;
       double s0[PS + 1], s1[PS + 1];
+      if (PS <= 8) {
+        load_run256<PS + 1>(r0, s0);
+        load_run256<PS + 1>(r1, s1);
+      } else {
 #pragma unroll
-      for (int c = 0; c <= PS; ++c) {
-        s0[c] = __ldg(r0 + c);
-        s1[c] = __ldg(r1 + c);
+        for (int c = 0; c <= PS; ++c) {
+          s0[c] = __ldg(r0 + c);
+          s1[c] = __ldg(r1 + c);
+        }
       }
 #pragma unroll
       for (int c = 0; c < PS; ++c)
