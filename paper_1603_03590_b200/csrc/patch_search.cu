@@ -784,7 +784,7 @@ __global__ void __launch_bounds__(128) k_patch_gn_group(SearchArgs a,
       const double* r0 = qry + (size_t)ay.i0 * W + xbase;
       const double* r1 = qry + (size_t)ay.i1 * W + xbase;
       double s0[PS + 1], s1[PS + 1];
-      if (PS <= 8) {
+      if (PS <= 12) {
         load_run256<PS + 1>(r0, s0);
         load_run256<PS + 1>(r1, s1);
       } else {
