@@ -137,6 +137,21 @@ DIS_API int dis_flow_batch(const void* frame1, const void* frame2, int32_t dtype
                    double* flow_out, void* workspace, size_t workspace_bytes,
                    void* stream);
 
+/* dis_flow_on_pyramids (pipeline.py:136-147) for a batch: the pyramids are
+ * given (device arrays of level pointers, index 0..coarsest; each level
+ * B x (H>>s) x (W>>s) float64 row-major: image and build_pyramid's
+ * image_gradients).  Only the levels the parameters read are used (images of
+ * levels >= 1 or of the finest level, gradients of levels >= finest_scale);
+ * they are copied into the workspace (dis_workspace_bytes) and the
+ * coarse-to-fine loop runs as in dis_flow_batch.  Stereo-mode parameters
+ * raise ValueError (pipeline.py:141-142). */
+DIS_API int dis_flow_batch_levels(const double* const* img1, const double* const* gx1,
+                                  const double* const* gy1, const double* const* img2,
+                                  const double* const* gx2, const double* const* gy2,
+                                  int32_t B, int32_t H, int32_t W, const dis_params_t* p,
+                                  double* flow_out, void* workspace, size_t workspace_bytes,
+                                  void* stream);
+
 /* dis_stereo (pipeline.py:166-183) for a batch of rectified pairs: the
  * same pipeline with horizontal-only conditioning (inverse_search.py:
  * 259-264) and SOR (variational.py:161); v comes out identically 0.  Same

@@ -15,6 +15,14 @@ from .params import (
     VarParams,
     coarsest_scale_for,
 )
+from .pyramid import (
+    ImagePyramid,
+    PyramidLevel,
+    as_image,
+    build_pyramid,
+    dis_flow_on_pyramids,
+    warmup,
+)
 from .pipeline import (
     FlowEngine,
     SparseMatch,
@@ -41,4 +49,10 @@ __all__ = [
     "dis_stereo_batch",
     "sparse_correspondences",
     "SparseMatch",
+    "ImagePyramid",
+    "PyramidLevel",
+    "as_image",
+    "build_pyramid",
+    "dis_flow_on_pyramids",
+    "warmup",
 ]

@@ -37,7 +37,7 @@ EXPORTED = (
     "dis_census_read", "dis_selftest_fp64_peak", "dis_compose_flows", "dis_stereo_batch",
     "dis_stereo_batch_host", "dis_densify_bidirectional",
     "dis_densify_bidirectional_workspace_bytes", "dis_sparse_workspace_bytes",
-    "dis_sparse_correspondences",
+    "dis_sparse_correspondences", "dis_flow_batch_levels",
 )
 
 KERNEL_CLASSES = ("pyramid", "patch_search", "densify", "tensor_assemble", "sor", "upsample")
@@ -94,6 +94,8 @@ def lib() -> ctypes.CDLL:
     L.dis_refine.restype = ctypes.c_int
     L.dis_upsample_flow.argtypes = [_vp, _vp, _i32, _i32, _i32, _vp, _vp, _i32, _i32, _vp]
     L.dis_upsample_flow.restype = ctypes.c_int
+    L.dis_flow_batch_levels.argtypes = [_vp] * 6 + [_i32, _i32, _i32, _pp, _vp, _vp, _sz, _vp]
+    L.dis_flow_batch_levels.restype = ctypes.c_int
     L.dis_stereo_batch.argtypes = L.dis_flow_batch.argtypes
     L.dis_stereo_batch.restype = ctypes.c_int
     L.dis_stereo_batch_host.argtypes = L.dis_flow_batch_host.argtypes

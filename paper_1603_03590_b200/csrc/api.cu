@@ -632,6 +632,45 @@ int dis_flow_batch(const void* frame1, const void* frame2, int32_t dtype, int32_
                          workspace_bytes, stream, false);
 }
 
+int dis_flow_batch_levels(const double* const* img1, const double* const* gx1,
+                          const double* const* gy1, const double* const* img2,
+                          const double* const* gx2, const double* const* gy2, int32_t B,
+                          int32_t H, int32_t W, const dis_params_t* p, double* flow_out,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = dis_params_validate(p);
+  if (rc) return rc;
+  if (p->mode == 1) return fail(DIS_ERR_VALUE, "use dis_stereo for stereo-mode parameters");
+  rc = check_dims(p, B, H, W);
+  if (rc) return rc;
+  Plan pl;
+  make_plan(p, B, H, W, &pl);
+  if (workspace_bytes < pl.total)
+    return fail(DIS_ERR_WORKSPACE, "workspace holds %zu bytes, need %zu", workspace_bytes,
+                pl.total);
+  cudaStream_t st = as_stream(stream);
+  g_launches = 0;
+  cudaMemsetAsync(at<char>(workspace, pl.off_status), 0, 256, st);
+  // the levels this parameter set reads (images of levels >= 1 or the finest,
+  // gradients of levels >= finest) into the workspace's pyramid slots
+  const double* const* src[2][3] = {{img1, gx1, gy1}, {img2, gx2, gy2}};
+  for (int f = 0; f < 2; ++f)
+    for (int s = 0; s <= pl.ss; ++s) {
+      const size_t bytes = (size_t)B * pl.hs[s] * pl.ws[s] * sizeof(double);
+      const size_t offs[3] = {pl.off_img[f][s], pl.off_gx[f][s], pl.off_gy[f][s]};
+      for (int k = 0; k < 3; ++k) {
+        if (offs[k] == kNone) continue;
+        if (!src[f][k] || !src[f][k][s])
+          return fail(DIS_ERR_VALUE, "pyramid %d level %d: missing %s raster", f + 1, s,
+                      k == 0 ? "image" : (k == 1 ? "grad_x" : "grad_y"));
+        cudaMemcpyAsync(at<char>(workspace, offs[k]), src[f][k][s], bytes,
+                        cudaMemcpyDeviceToDevice, st);
+      }
+    }
+  rc = check_cuda("dis_flow_batch_levels");
+  if (rc) return rc;
+  return run_pipeline(pl, p, flow_out, workspace, st, false);
+}
+
 int dis_stereo_batch(const void* left, const void* right, int32_t dtype, int32_t B, int32_t H,
                      int32_t W, const dis_params_t* p, double* flow_out, void* workspace,
                      size_t workspace_bytes, void* stream) {

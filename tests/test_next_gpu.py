@@ -200,3 +200,60 @@ def test_sparse_no_valid_seed_and_single_seed(torch):
     assert all(x.displacement == (0.0, 0.0) for x in m)
     m = sparse_correspondences(a, a, (10.0, 20.0), p)  # a single seed (atleast_2d)
     assert len(m) == 1 and m[0].valid
+
+
+# ---- pyramid-level entry point (pipeline.py:136-147, core.py:33-128) --------
+
+def test_build_pyramid_matches_reference_golden(torch):
+    from paper_1603_03590_b200 import build_pyramid
+
+    g = golden("pyramid.npz")
+    pyr = build_pyramid(g["img"], 4)
+    assert len(pyr) == 5 and pyr.downscale == 2
+    for s in range(5):
+        lv = pyr[s]
+        assert lv.scale_index == s and lv.width == g[f"L{s}_img"].shape[1]
+        assert np.array_equal(lv.image.cpu().numpy(), g[f"L{s}_img"]), s
+        assert np.array_equal(lv.grad_x.cpu().numpy(), g[f"L{s}_gx"]), s
+        assert np.array_equal(lv.grad_y.cpu().numpy(), g[f"L{s}_gy"]), s
+
+
+@pytest.mark.parametrize("case", ["c1", "c2"])
+def test_dis_flow_on_pyramids_equals_dis_flow(torch, orc, case):
+    """Our GPU pyramids and numpy pyramids in the reference's layout (oracle)
+    both give the reference's flow."""
+    from paper_1603_03590_b200 import (ImagePyramid, PyramidLevel, build_pyramid,
+                                       dis_flow_on_pyramids)
+    from tests.test_gpu_parity import _params_from
+
+    g = golden(f"e2e_{case}.npz")
+    p = _params_from(g)
+    got = dis_flow_on_pyramids(build_pyramid(g["f1"], p.coarsest_scale),
+                               build_pyramid(g["f2"], p.coarsest_scale), p)
+    assert got.is_cuda
+    assert np.array_equal(got.cpu().numpy(), g["flow"])
+
+    def np_pyr(f):
+        lv = orc.build_pyramid(f, p.coarsest_scale)
+        return ImagePyramid(tuple(PyramidLevel(i, gx, gy, s) for s, (i, gx, gy) in
+                                  enumerate(lv)), 2)
+
+    got = dis_flow_on_pyramids(np_pyr(g["f1"]), np_pyr(g["f2"]), p)
+    assert isinstance(got, np.ndarray) and np.array_equal(got, g["flow"])
+
+
+def test_dis_flow_on_pyramids_errors_and_warmup(torch):
+    from paper_1603_03590_b200 import (DisParams, ParameterError, build_pyramid,
+                                       dis_flow_on_pyramids, warmup)
+
+    warmup()
+    a = build_pyramid(np.random.default_rng(0).uniform(0, 255, (40, 64)), 2)
+    b = build_pyramid(np.random.default_rng(1).uniform(0, 255, (40, 66)), 2)
+    with pytest.raises(ValueError):
+        dis_flow_on_pyramids(a, b, DisParams(coarsest_scale=2, finest_scale=1))
+    with pytest.raises(ValueError):
+        dis_flow_on_pyramids(a, a, DisParams.preset(2, stereo=True, coarsest_scale=2))
+    with pytest.raises(ValueError):  # coarsest level 16x10 cannot hold a 12 px patch
+        dis_flow_on_pyramids(a, a, DisParams(patch_size=12, coarsest_scale=2, finest_scale=1))
+    with pytest.raises(ParameterError):
+        build_pyramid(np.zeros((8, 8)), -1)
