@@ -1,0 +1,199 @@
+"""The reference's known-answer cases, restated against this
+package's GPU API: pyramid dimensions and gradients, grid spacing and
+clamping, densification worked examples, upsampling, refinement and patch
+search identities.  Everything runs through the C ABI on the GPU."""
+
+import numpy as np
+import pytest
+
+from paper_1603_03590_b200.params import DisParams, VarParams
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA GPU")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def st(torch):
+    from paper_1603_03590_b200 import stages
+
+    return stages
+
+
+def _cu(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+# ---- pyramid (core.py:75-128) ------------------------------------------------
+
+def test_pyramid_sintel_level_sizes(torch):
+    from paper_1603_03590_b200 import build_pyramid
+
+    pyr = build_pyramid(np.zeros((436, 1024), dtype=np.float32), 5)
+    assert [lv.height for lv in pyr.levels] == [436, 218, 109, 54, 27, 13]
+    assert [lv.width for lv in pyr.levels] == [1024, 512, 256, 128, 64, 32]
+
+
+@pytest.mark.parametrize("h,w,coarsest", [(9, 2047, 2), (1080, 1920, 4), (31, 17, 3), (8, 8, 2)])
+def test_pyramid_floor_dimension_law(torch, h, w, coarsest):
+    from paper_1603_03590_b200 import build_pyramid
+
+    pyr = build_pyramid(np.zeros((h, w)), coarsest)
+    for s, lv in enumerate(pyr.levels):
+        assert (lv.height, lv.width) == (h >> s, w >> s)
+
+
+def test_pyramid_refuses_levels_below_two_pixels(torch):
+    from paper_1603_03590_b200 import build_pyramid
+
+    with pytest.raises(ValueError):
+        build_pyramid(np.zeros((8, 8)), 3)
+
+
+def test_constant_image_has_zero_gradients_at_every_level(torch):
+    from paper_1603_03590_b200 import build_pyramid
+
+    for lv in build_pyramid(np.full((40, 56), 77.0), 3).levels:
+        assert not lv.grad_x.any() and not lv.grad_y.any()
+
+
+def test_linear_ramp_gradients_are_exact(torch):
+    from paper_1603_03590_b200 import build_pyramid
+
+    ys, xs = np.mgrid[0:20, 0:32].astype(np.float64)
+    lv = build_pyramid(3.0 * xs + 7.0 * ys, 0)[0]
+    assert (lv.grad_x.cpu().numpy()[:, 1:-1] == 3.0).all()
+    assert (lv.grad_y.cpu().numpy()[1:-1, :] == 7.0).all()
+
+
+def test_box_mean_of_two_by_two_blocks(torch):
+    from paper_1603_03590_b200 import build_pyramid
+
+    block = np.array([[0.0, 2.0, 10.0, 10.0], [4.0, 6.0, 10.0, 10.0]])
+    lv1 = build_pyramid(np.vstack([block, block]), 1)[1]
+    assert lv1.image.cpu().numpy()[0].tolist() == [3.0, 10.0]
+
+
+# ---- patch grid (densification.py:50-79) -----------------------------------
+
+@pytest.mark.parametrize("dim,ps,ov,spacing", [(32, 8, 0.0, 8), (32, 8, 0.3, 6),
+                                                (32, 8, 0.4, 5), (48, 12, 0.75, 3)])
+def test_grid_spacing_floors_the_overlap(torch, st, dim, ps, ov, spacing):
+    xo = st.grid_axis(dim, ps, ov)
+    assert xo[0] == 0 and xo[1] - xo[0] == spacing
+    assert xo[-1] == dim - ps
+
+
+def test_grid_clamps_the_last_origin(torch, st):
+    assert st.grid_axis(17, 8, 0.0).tolist() == [0, 8, 9]
+    assert st.grid_axis(16, 8, 0.0).tolist() == [0, 8]
+
+
+def test_grid_refuses_levels_smaller_than_a_patch(torch, st):
+    with pytest.raises(ValueError):
+        st.grid_axis(7, 8, 0.0)
+
+
+# ---- densification (densification.py:110-191) -------------------------------
+
+def _densify(torch, st, ref, qry, ps, ov, disp, offs):
+    p = DisParams(patch_size=ps, overlap=ov)
+    d = np.asarray(disp, dtype=np.float64)
+    u, v = st.densify(_cu(torch, ref[None]), _cu(torch, qry[None]), p, _cu(torch, d[None, :, 0]),
+                      _cu(torch, d[None, :, 1]), _cu(torch, np.asarray(offs)[None]))
+    return u[0].cpu().numpy(), v[0].cpu().numpy()
+
+
+def test_densify_single_patch_gives_its_displacement(torch, st):
+    u, v = _densify(torch, st, np.zeros((8, 8)), np.full((8, 8), 0.5), 8, 0.0,
+                    [[1.25, -0.5]], [0.0])
+    assert (u == 1.25).all() and (v == -0.5).all()
+
+
+def test_densify_two_patch_weighted_average(torch, st):
+    # two patches of a 12x8 level (origins x = 0 and 4); at pixel (5, 3) their
+    # residuals are 1 and 4 -> weights 1 and 1/4 for u = 1 and u = 3
+    qry = np.zeros((8, 12))
+    qry[3, 6] = 1.0
+    qry[3, 8] = 4.0
+    u, v = _densify(torch, st, np.zeros((8, 12)), qry, 8, 0.5, [[1.0, 0.0], [3.0, 0.0]],
+                    [0.0, 0.0])
+    assert u[3, 5] == pytest.approx((1.0 * 1.0 + 0.25 * 3.0) / 1.25, abs=1e-12)
+    assert v[3, 5] == 0.0
+
+
+def test_densify_shared_displacement_is_exact(torch, st):
+    rng = np.random.default_rng(13)
+    ref = rng.uniform(0, 255, (14, 20))
+    qry = rng.uniform(0, 255, (14, 20))
+    n = len(st.grid_axis(20, 8, 0.5)) * len(st.grid_axis(14, 8, 0.5))
+    u, v = _densify(torch, st, ref, qry, 8, 0.5, np.tile([2.5, -1.0], (n, 1)), np.zeros(n))
+    assert np.abs(u - 2.5).max() <= 1e-12 and np.abs(v + 1.0).max() <= 1e-12
+
+
+def test_densify_is_convex_and_covers_random_layouts(torch, st):
+    rng = np.random.default_rng(14)
+    for _ in range(10):
+        ps = int(rng.integers(4, 10))
+        w, h = int(rng.integers(ps, 40)), int(rng.integers(ps, 40))
+        ov = float(rng.uniform(0, 0.9))
+        n = len(st.grid_axis(w, ps, ov)) * len(st.grid_axis(h, ps, ov))
+        disp = rng.normal(0, 2, (n, 2))
+        u, v = _densify(torch, st, rng.uniform(0, 255, (h, w)), rng.uniform(0, 255, (h, w)), ps,
+                        ov, disp, rng.normal(0, 1, n))
+        for comp, c in ((u, 0), (v, 1)):
+            assert comp.min() >= disp[:, c].min() - 1e-12
+            assert comp.max() <= disp[:, c].max() + 1e-12
+
+
+# ---- upsampling (core.py:154-190) -------------------------------------------
+
+def test_upsample_constant_field_doubles_exactly(torch, st):
+    u = _cu(torch, np.full((1, 13, 17), 1.75))
+    v = _cu(torch, np.full((1, 13, 17), -0.5))
+    ou, ov = st.upsample_flow(u, v, 34, 27)
+    assert (ou.cpu().numpy() == 3.5).all() and (ov.cpu().numpy() == -1.0).all()
+
+
+def test_compose_with_zero_first_field_returns_the_second(torch):
+    from paper_1603_03590_b200 import compose_flows
+
+    bc = np.random.default_rng(3).normal(0, 3, (9, 11, 2))
+    assert np.array_equal(compose_flows(np.zeros_like(bc), bc), bc)
+
+
+# ---- refinement (variational.py:220-275) ------------------------------------
+
+def test_refine_on_constant_images_is_the_identity(torch, st):
+    lv = st.build_pyramid(np.full((20, 26), 64.0), 0)[0]
+    fu = _cu(torch, np.full((1, 20, 26), 3.25))
+    fv = _cu(torch, np.full((1, 20, 26), -1.5))
+    u, v = st.refine(fu, fv, lv, lv, DisParams(variational=VarParams()), 3)
+    assert (u.cpu().numpy() == 3.25).all() and (v.cpu().numpy() == -1.5).all()
+
+
+# ---- patch search (inverse_search.py:113-189) -------------------------------
+
+def test_patch_search_on_identical_frames_stays_at_zero(torch, st):
+    img = np.random.default_rng(21).uniform(0, 255, (32, 48))
+    lv = st.build_pyramid(img, 0)[0]
+    out = st.patch_search(lv, lv["img"], DisParams(patch_size=8, overlap=0.5, iterations=16))
+    assert not out["u"].any() and not out["v"].any()
+    assert not out["off"].any() and not out["mar"].any()
+
+
+def test_constant_patches_are_invalid_and_keep_their_init(torch, st):
+    lv = st.build_pyramid(np.full((24, 24), 9.0), 0)[0]
+    q = st.build_pyramid(np.random.default_rng(2).uniform(0, 255, (24, 24)), 0)[0]
+    coarse = _cu(torch, np.full((1, 12, 12), 0.75))
+    out = st.patch_search(lv, q["img"], DisParams(patch_size=8, overlap=0.0, iterations=8),
+                          coarse, coarse)
+    assert not out["valid"].any()
+    assert (out["u"].cpu().numpy() == 1.5).all() and (out["v"].cpu().numpy() == 1.5).all()
