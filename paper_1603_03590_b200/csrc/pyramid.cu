@@ -230,6 +230,27 @@ __global__ void __launch_bounds__(256) k_gradients_tile(const double* __restrict
   }
 }
 
+// gx / gy only (no second derivatives): one thread per pixel, the image_gradients
+// stencil (core.py:75-85) read straight from the level (rows coalesced, the
+// vertical neighbours hit L1/L2), gx and gy written coalesced
+__global__ void __launch_bounds__(256) k_gradients_xy(const double* __restrict__ img_all, int H,
+                                                      int W, double* __restrict__ gx_all,
+                                                      double* __restrict__ gy_all) {
+  const int b = blockIdx.z;
+  const int x = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (x >= W || y >= H) return;
+  const size_t plane = (size_t)W * H;
+  const double* row = img_all + b * plane + (size_t)y * W;
+  const int xm = x > 0 ? x - 1 : 0, xp = x < W - 1 ? x + 1 : W - 1;
+  const double* up = img_all + b * plane + (size_t)(y > 0 ? y - 1 : 0) * W;
+  const double* dn = img_all + b * plane + (size_t)(y < H - 1 ? y + 1 : H - 1) * W;
+  const size_t o = b * plane + (size_t)y * W + x;
+  // clamped indices = the one-sided border forms (x = 0: f[1] - f[0], ...)
+  if (gx_all) gx_all[o] = 0.5 * (__ldg(row + xp) - __ldg(row + xm));
+  if (gy_all) gy_all[o] = 0.5 * (__ldg(dn + x) - __ldg(up + x));
+}
+
 // level 1 straight from the frames + the finiteness check of every input
 // pixel (as_image, core.py:65-72), one pass over the frames
 template <typename T>
@@ -300,7 +321,12 @@ static void launch_pyramid_t(const T* frames, int B, int H, int W, int coarsest,
   for (int s = 0; s <= coarsest; ++s) {
     if (gx[s] || gy[s] || (dd && dd[s])) {
       dim3 g((unsigned)((w + kGTX - 1) / kGTX), (unsigned)((h + kGTY - 1) / kGTY), (unsigned)B);
-      k_gradients_tile<<<g, 256, 0, st>>>(img[s], h, w, gx[s], gy[s], dd ? dd[s] : nullptr);
+      if (dd && dd[s]) {
+        k_gradients_tile<<<g, 256, 0, st>>>(img[s], h, w, gx[s], gy[s], dd[s]);
+      } else {
+        dim3 g2((unsigned)((w + 31) / 32), (unsigned)((h + 7) / 8), (unsigned)B);
+        k_gradients_xy<<<g2, 256, 0, st>>>(img[s], h, w, gx[s], gy[s]);
+      }
       note_launch();
     }
     h /= 2;
