@@ -17,6 +17,14 @@
 
 namespace disb200 {
 
+// the densification weight 1 / max(1, |d|) (densification.py:122-123): the
+// divisor is >= 1, so div_fast_rn is exact up to 2^400 (den_fast_ok); IEEE
+// division beyond (only for absurd residuals)
+__device__ __forceinline__ double inv_weight(double ad) {
+  const double den = ad > 1.0 ? ad : 1.0;
+  return den < 0x1p400 ? div_fast_rn(1.0, den) : 1.0 / den;
+}
+
 struct Cover {
   int j0, j1;   // regular origins j0..j1 (inclusive; empty if j1 < j0)
   bool extra;   // the clamped last origin covers too
@@ -81,7 +89,7 @@ __global__ void __launch_bounds__(256) k_densify(const double* __restrict__ ref_
         const double off = __ldg(o_ + i);
         const double d = bilin_nb(qry, W, H, (double)x + u, (double)y + v) - off - r;
         const double ad = fabs(d);
-        const double wgt = 1.0 / (ad > 1.0 ? ad : 1.0);
+        const double wgt = inv_weight(ad);
         acc_u += wgt * u;
         acc_v += wgt * v;
         acc_w += wgt;
@@ -270,7 +278,7 @@ __global__ void __launch_bounds__(kBT * kBT) k_densify_bidir(
         const double off = __ldg(o_ + i);
         const double d = bilin_nb(qry, W, H, (double)x + u, (double)y + v) - off - r;
         const double ad = fabs(d);
-        const double wgt = 1.0 / (ad > 1.0 ? ad : 1.0);
+        const double wgt = inv_weight(ad);
         acc_u += wgt * u;
         acc_v += wgt * v;
         acc_w += wgt;
@@ -321,7 +329,7 @@ __global__ void __launch_bounds__(kBT * kBT) k_densify_bidir(
         const double ub = s_ub[k], vb = s_vb[k];
         const double d = r - s_off[k] - bilin_nb(qry, W, H, (double)x - ub, (double)y - vb);
         const double ad = fabs(d);
-        const double wgt = 1.0 / (ad > 1.0 ? ad : 1.0);
+        const double wgt = inv_weight(ad);
         b_u += wgt * (-ub);
         b_v += wgt * (-vb);
         b_w += wgt;
