@@ -21,8 +21,19 @@ from .pyramid import (
     as_image,
     build_pyramid,
     dis_flow_on_pyramids,
+    image_gradients,
+    upsample_flow,
     warmup,
 )
+from .densification import (
+    PatchGrid,
+    create_grid,
+    densify,
+    densify_bidirectional,
+    init_patches,
+    reset_outliers,
+)
+from .variational import refine
 from .pipeline import (
     FlowEngine,
     SparseMatch,
@@ -55,4 +66,13 @@ __all__ = [
     "build_pyramid",
     "dis_flow_on_pyramids",
     "warmup",
+    "image_gradients",
+    "upsample_flow",
+    "PatchGrid",
+    "create_grid",
+    "densify",
+    "densify_bidirectional",
+    "init_patches",
+    "reset_outliers",
+    "refine",
 ]

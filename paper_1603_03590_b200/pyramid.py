@@ -96,6 +96,29 @@ def build_pyramid(img, coarsest_scale: int, downscale: int = 2) -> ImagePyramid:
     return ImagePyramid(levels, 2)
 
 
+def image_gradients(img):
+    """Central differences with one-sided borders (core.py:75-85), on the GPU
+    (``dis_build_pyramid`` level 0); numpy in -> numpy (gx, gy)."""
+    lv = build_pyramid(img, 0)[0]
+    return lv.grad_x.cpu().numpy(), lv.grad_y.cpu().numpy()
+
+
+def upsample_flow(flow, new_width: int, new_height: int, scale_factor: int):
+    """output(x) = scale * flow(x / scale), bilinear_map form (core.py:178-190),
+    on the GPU (``dis_upsample_flow``); this path implements scale 2."""
+    from . import stages
+    from .pipeline import _require_cuda
+
+    torch = _require_cuda()
+    if scale_factor != 2:
+        raise ParameterError("this path implements downscale == 2 only")
+    f = np.asarray(flow, dtype=np.float64)
+    u = torch.from_numpy(np.ascontiguousarray(f[None, :, :, 0])).cuda()
+    v = torch.from_numpy(np.ascontiguousarray(f[None, :, :, 1])).cuda()
+    ou, ov = stages.upsample_flow(u, v, int(new_width), int(new_height))
+    return np.stack([ou[0].cpu().numpy(), ov[0].cpu().numpy()], axis=-1)
+
+
 def _dev64(x, device):
     import torch
 
