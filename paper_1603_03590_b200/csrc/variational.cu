@@ -698,11 +698,11 @@ static int choose_cluster(int B, int H) {
   // rows; the st.async halo exchange costs ~0.15 us per step)
   while (C < 16 && B * (C + 1) <= sms && (H + C) / (C + 1) >= 32) ++C;
   // several waves of CTAs: 64-row bands (two CTAs per SM, whose steps
-  // interleave) when they waste fewer padding rows (c3's 540-row level: 9
+  // interleave) when they pad no more rows (c3's 540-row level: 9
   // bands of 60 rows run 12 % faster than 5 of 108)
   if (B * C > sms) {
     const int C64 = (H + 63) / 64;
-    if (C64 <= 16 && (long)C64 * 64 < (long)C * hp(C) && sor_smem_bytes<S>(64) * 2 <= kMaxSmem)
+    if (C64 <= 16 && (long)C64 * 64 <= (long)C * hp(C) && sor_smem_bytes<S>(64) * 2 <= kMaxSmem)
       C = C64;
   }
   return C;
