@@ -716,8 +716,10 @@ __global__ void __launch_bounds__(128) k_patch_gn_general(SearchArgs a,
 // same order as the reference's loop.  All lanes of a group hold the same
 // patch state and apply the same update.
 // ---------------------------------------------------------------------------
+// (3 blocks per SM for 8px patches: 168 registers, measured best; 12px
+// patches keep the compiler's choice)
 template <int PS, int G, int CODE>
-__global__ void __launch_bounds__(128) k_patch_gn_group(SearchArgs a,
+__global__ void __launch_bounds__(128, PS == 8 ? 3 : 1) k_patch_gn_group(SearchArgs a,
                                                          const double* __restrict__ prep,
                                                          unsigned* counter,
                                                          const double* __restrict__ spill,
@@ -736,6 +738,10 @@ __global__ void __launch_bounds__(128) k_patch_gn_group(SearchArgs a,
   const size_t plane = (size_t)W * H;
   const bool mean_norm = a.mean_norm != 0;
   const double dn = (double)(PS * PS);
+  const int rr_row = r < PS ? r : PS - 1;
+  // my window row's template samples and gradients, constant per patch:
+  // loaded once per patch (not once per evaluation), lane-minor layout
+  __shared__ double2 Ts[3 * PS / 2][128];
   Lane L;
   L.pid = -1;
   L.b = L.x0i = L.y0i = 0;  // an idle group evaluates a harmless in-bounds window
@@ -758,6 +764,17 @@ __global__ void __launch_bounds__(128) k_patch_gn_group(SearchArgs a,
           lane_resume(L, a, prep, N, P, nx, spill + (size_t)g * kSpillStride);
         else
           lane_start(L, a, prep, N, P, nx, g);
+        if (!done) {  // my template row of the new patch -> shared memory
+          const size_t trow = (size_t)L.b * plane + (size_t)(L.y0i + rr_row) * W + L.x0i;
+#pragma unroll
+          for (int c = 0; c < PS; c += 2) {
+            Ts[c / 2][threadIdx.x] = make_double2(__ldg(a.ref + trow + c), __ldg(a.ref + trow + c + 1));
+            Ts[PS / 2 + c / 2][threadIdx.x] =
+                make_double2(__ldg(a.rgx + trow + c), __ldg(a.rgx + trow + c + 1));
+            Ts[PS + c / 2][threadIdx.x] =
+                make_double2(__ldg(a.rgy + trow + c), __ldg(a.rgy + trow + c + 1));
+          }
+        }
       }
     }
     if (__all_sync(FULL, done)) break;
@@ -777,7 +794,6 @@ __global__ void __launch_bounds__(128) k_patch_gn_group(SearchArgs a,
       regx = regx && ax.i0 == xbase + o && ax.i1 == ax.i0 + 1;
       FX[o] = ax.f;
     }
-    const int rr_row = r < PS ? r : PS - 1;
     const Axis1 ay = axis_sample(by + rr_row, H);
     double val[PS];
     if (regx) {
@@ -818,7 +834,6 @@ __global__ void __launch_bounds__(128) k_patch_gn_group(SearchArgs a,
     }
     const double off = mean_norm ? exact_div_pos(wsum, dn) - L.mean_t : 0.0;
     // pass 2: the addends of my row, then the four sums in row order
-    const size_t row = po + (size_t)(L.y0i + rr_row) * W + L.x0i;
     double EA[PS], E2[PS], EX[PS], EY[PS];
     auto addends = [&](int c, double t, double gxv, double gyv) {
       const double e = val[c] - off - t;
@@ -828,20 +843,13 @@ __global__ void __launch_bounds__(128) k_patch_gn_group(SearchArgs a,
       EX[c] = gxv * et;
       EY[c] = gyv * et;
     };
-    if ((PS & 3) == 0 && ((row | (size_t)W) & 3) == 0) {  // 32-byte aligned template row
 #pragma unroll
-      for (int c = 0; c < PS; c += 4) {
-        double t[4], gx4[4], gy4[4];
-        ldg256(a.ref + row + c, t);
-        ldg256(a.rgx + row + c, gx4);
-        ldg256(a.rgy + row + c, gy4);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) addends(c + q, t[q], gx4[q], gy4[q]);
-      }
-    } else {
-#pragma unroll
-      for (int c = 0; c < PS; ++c)
-        addends(c, __ldg(a.ref + row + c), __ldg(a.rgx + row + c), __ldg(a.rgy + row + c));
+    for (int c = 0; c < PS; c += 2) {
+      const double2 t = Ts[c / 2][threadIdx.x];
+      const double2 gx2 = Ts[PS / 2 + c / 2][threadIdx.x];
+      const double2 gy2 = Ts[PS + c / 2][threadIdx.x];
+      addends(c, t.x, gx2.x, gy2.x);
+      addends(c + 1, t.y, gx2.y, gy2.y);
     }
     double mar = 0.0, ssd = 0.0, b0 = 0.0, b1 = 0.0;
 #pragma unroll
