@@ -1,0 +1,30 @@
+"""Experiment: pinned H2D alone, D2H alone, and both at once (two streams)."""
+import torch
+n = 256 << 20
+h1 = torch.empty(n, dtype=torch.uint8).pin_memory()
+h2 = torch.empty(n, dtype=torch.uint8).pin_memory()
+d1 = torch.empty(n, dtype=torch.uint8, device='cuda')
+d2 = torch.empty(n, dtype=torch.uint8, device='cuda')
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+def t(fn, reps=10):
+    fn(); torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps): fn()
+    e1.record(); torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+def h2d():
+    with torch.cuda.stream(s1): d1.copy_(h1, non_blocking=True)
+    torch.cuda.current_stream().wait_stream(s1)
+def d2h():
+    with torch.cuda.stream(s2): h2.copy_(d2, non_blocking=True)
+    torch.cuda.current_stream().wait_stream(s2)
+def both():
+    ev = torch.cuda.current_stream().record_event()
+    s1.wait_event(ev); s2.wait_event(ev)
+    with torch.cuda.stream(s1): d1.copy_(h1, non_blocking=True)
+    with torch.cuda.stream(s2): h2.copy_(d2, non_blocking=True)
+    torch.cuda.current_stream().wait_stream(s1); torch.cuda.current_stream().wait_stream(s2)
+a = t(h2d); b = t(d2h); c = t(both)
+print('h2d %.1f GB/s  d2h %.1f GB/s  both %.2f ms -> combined %.1f GB/s (serial would be %.2f ms)' % (
+    n / a / 1e6, n / b / 1e6, c, 2 * n / c / 1e6, a + b))
