@@ -34,6 +34,7 @@
 // Neighbour terms use U_q = fl(u_q + du_q) exactly as the reference's
 // `u[y, x-1] + du[y, x-1]`; the last sweep's U is the updated flow.
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -281,7 +282,10 @@ __global__ void __launch_bounds__(256, 3) k_tensor_assemble(RefineArgs a, size_t
   }
 }
 
-constexpr int kLookahead = 5;      // diagonals fetched ahead of sweep 0 (~4 steps of latency cover)
+#ifndef DIS_SOR_LOOKAHEAD
+#define DIS_SOR_LOOKAHEAD 5
+#endif
+constexpr int kLookahead = DIS_SOR_LOOKAHEAD;  // diagonals fetched ahead of sweep 0
 constexpr int kMaxBandRows = 128;  // rows (threads per sweep) of one CTA's band
 
 template <int S>
@@ -666,6 +670,410 @@ __global__ void __launch_bounds__(S * kMaxBandRows + 32, 1)
   if (bad) set_status(status, DIS_STATUS_NONFINITE_FLOW);
 }
 
+// The wavefront SOR kernel, grouped form: thread (g, r) owns band row
+// y = y0 + r and a group of P consecutive sweeps t = gP .. gP+P-1 (the last
+// group may hold fewer), and computes, at step k, the pixels x_t = k - y - 2t
+// of its sweeps (independent within the step, so their chains interleave).
+// The per-step control, barrier and exchange work is shared by the group's
+// pixels, and inside a group three of the five neighbour terms come from
+// the thread's own registers:
+//   left  (x-1, y) of sweep t   = my sweep-t value of step k-1
+//   right (x+1, y) of sweep t-1 = my sweep-(t-1) value of step k-1
+//   self du of sweep t-1        = my sweep-(t-1) du of step k-2
+//   up    (x, y-1) of sweep t   = row r-1's sweep-t value of step k-1 (xuv)
+//   down  (x, y+1) of sweep t-1 = row r+1's sweep-(t-1) value of step k-1 (xuv)
+// A group's first sweep takes right from xuv and self du from xd (written
+// by the previous group's last sweep two steps before); sweep 0's come from
+// the records (+ the carried du of a chained pass), as in k_sor.  Shared
+// memory: the same record ring, xuv[2][S][Hp+2] x 16 B (U, V of the last
+// two steps + halo rows), xd[3][G-1][Hp] x 16 B.  The arithmetic of every
+// pixel update is k_sor's, operation for operation.
+#ifdef DIS_SOR_TRACE
+__device__ long long g_sor_trace[6][1024];
+#define SOR_TR(i) \
+  if (tr && k < 1024) g_sor_trace[i][k] = clock64();
+#else
+#define SOR_TR(i)
+#endif
+template <int S, bool HZ, int P>
+__global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
+    k_sor_rows(const double* __restrict__ rec, int B, int W, int H, int Hc, size_t Ls,
+               double omega, const double* du_in, const double* dv_in, double* du_out,
+               double* dv_out, double* __restrict__ fu, double* __restrict__ fv,
+               uint32_t* status, const double* __restrict__ zeros) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int R = ring_slots<S>();
+  constexpr int G = (S + P - 1) / P;       // sweep groups
+  constexpr int PL = S - (G - 1) * P;      // sweeps of the last group
+  const int C = (int)(gridDim.x / (unsigned)B) > 0 ? (int)(gridDim.x / (unsigned)B) : 1;
+  const int c = C > 1 ? (int)cluster_rank() : 0;
+  const int b = blockIdx.x / C;
+  const int Hp = ((int)blockDim.x - 32) / G;  // band rows (padded); + one producer warp
+  const bool producer = threadIdx.x >= (unsigned)(G * Hp);  // ring fill, no pixels
+  const int g = producer ? 0 : (int)threadIdx.x / Hp;
+  const int r = producer ? Hp : (int)threadIdx.x - g * Hp;
+  const int t0 = g * P;  // my first sweep
+  const int y0 = c * Hc;
+  const int y = y0 + r;
+  const int nrows = min(Hc, H - y0);
+  const int ndiag = W + H - 1;
+  const int rrows = Hp + 1;  // ring rows
+  const int xrows = Hp + 2;  // exchange rows
+  const unsigned slot_bytes = (unsigned)(kChunks * rrows * 16);
+  const unsigned ring_s = (unsigned)__cvta_generic_to_shared(smem);
+  const unsigned ring_end = ring_s + (unsigned)R * slot_bytes;
+  const unsigned xuv_s = ring_end;
+  const unsigned xd_s = xuv_s + (unsigned)(2 * S * xrows * 16);
+  const unsigned d_ph_b = (unsigned)((G > 1 ? G - 1 : 1) * Hp * 16);  // one xd phase
+  const unsigned bar_above = xd_s + 3 * d_ph_b;  // 8-byte aligned
+  const unsigned bar_below = bar_above + 16;
+  const unsigned bar_ring = bar_above + 32;  // [R] slot-fill barriers
+  const double2* __restrict__ base =
+      reinterpret_cast<const double2*>(rec + (size_t)b * Ls * kRec);  // [d][chunk][H]
+  const double* Dui = du_in ? du_in + (size_t)b * Ls : nullptr;  // may alias du_out
+  const double* Dvi = dv_in ? dv_in + (size_t)b * Ls : nullptr;
+  const double om1 = 1.0 - omega;
+
+  {  // ring + exchange buffers start at zero
+    const unsigned nz = (bar_above - ring_s) / 16u;  // 16-byte entries
+    for (unsigned i = threadIdx.x; i < nz; i += blockDim.x) sts2(ring_s + 16 * i, 0.0, 0.0);
+  }
+  if (threadIdx.x == 0) {
+    if (C > 1) {
+      mbar_init(bar_above, 1);
+      mbar_init(bar_above + 8, 1);
+      mbar_init(bar_below, 1);
+      mbar_init(bar_below + 8, 1);
+    }
+    for (int i = 0; i < R; ++i) mbar_init(bar_ring + 8u * i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  // ring fill by the producer warp: as in k_sor
+  const int ylast = min(y0 + rrows, H) - 1;
+  const unsigned lane = threadIdx.x & 31;
+  int jn = 0;
+  unsigned sin_s = ring_s, sin_bar = bar_ring;
+  auto issue_next = [&]() {
+    const int ya = max(y0, jn - W + 1), yb = min(ylast, jn);
+    const int jo = jn - R;  // the slot's previous diagonal
+    const int pa = max(y0, jo - W + 1), pb = min(ylast, jo);
+    const int za = pa, zb = min(pb, ya <= yb ? ya - 1 : pb);
+    const unsigned zrun = (jo >= 0 && zb >= za) ? (unsigned)(zb - za + 1) * 16u : 0u;
+    const unsigned run = yb >= ya ? (unsigned)(yb - ya + 1) * 16u : 0u;
+    // lane 0 arms the slot's barrier; lanes 0..5 copy one chunk run each (a
+    // complete_tx may land before the expect_tx: the phase cannot complete
+    // before lane 0's arrive)
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sin_bar),
+                   "r"(kChunks * (run + zrun))
+                   : "memory");
+    if (lane < (unsigned)kChunks) {
+      const unsigned cc = lane;
+      if (zrun)
+        bulk_g2s(sin_s + (unsigned)((za - y0) * 16) + cc * (unsigned)(rrows * 16), zeros, zrun,
+                 sin_bar);
+      if (run)
+        bulk_g2s(sin_s + (unsigned)((ya - y0) * 16) + cc * (unsigned)(rrows * 16),
+                 base + ((size_t)jn * kChunks + cc) * H + ya, run, sin_bar);
+    }
+    ++jn;
+    sin_s += slot_bytes;
+    sin_bar += 8;
+    if (sin_s == ring_end) {
+      sin_s = ring_s;
+      sin_bar = bar_ring;
+    }
+  };
+  // slot readiness: fill n of slot s (diagonal s + nR) completes phase n
+  auto wait_diag = [&](int j) {
+    if (j >= 0 && j < jn)
+      mbar_wait_parity_cta(bar_ring + 8u * (unsigned)(j % R), (unsigned)((j / R) & 1));
+  };
+  const bool filler = threadIdx.x == (unsigned)(G * Hp);  // lane 0 of the producer warp
+  if (producer) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // the start-up clear
+    for (int j = 0; j < kLookahead; ++j) issue_next();
+    if (filler) {
+      wait_diag(0);
+      wait_diag(1);
+    }
+  }
+  if (C > 1) {  // barriers initialised everywhere before any remote arrive
+    cluster_arrive();
+    cluster_wait();
+  } else {
+    __syncthreads();
+  }
+  const int nsteps = ndiag + 2 * (S - 1);
+  // my values of the last two steps, per sweep of my group
+  double Up[P], Vp[P], Dp[P], DVp[P], Dp2[P], DVp2[P], Un[P], Vn[P], Dn[P], DVn[P];
+#pragma unroll
+  for (int i = 0; i < P; ++i) Up[i] = Vp[i] = Dp[i] = DVp[i] = Dp2[i] = DVp2[i] = 0.0;
+  bool bad = false;
+  unsigned a_k = ring_s;  // slot of diagonal k
+  const unsigned rrow = (unsigned)(r * 16);
+  const unsigned cstride = (unsigned)(rrows * 16);
+  const unsigned xstride = (unsigned)(xrows * 16);
+  unsigned uv_r = xuv_s + (unsigned)S * xstride, uv_w = xuv_s;  // step k-1 / step k
+  unsigned d_w = xd_s, d_r = xd_s + d_ph_b;  // xd phase k mod 3 / (k-2) mod 3
+  const unsigned d_end = xd_s + 3 * d_ph_b;
+  const size_t fplane = (size_t)W * H;
+  const int last_r = nrows - 1;
+  const int wr0 = r & ~31;  // first row of my warp
+  const bool first_owner = C > 1 && c > 0 && r == 0 && !producer;
+  const bool last_owner = C > 1 && c < C - 1 && r == last_r && !producer;
+  const bool live_warp = !producer && wr0 < nrows;
+  const int nt = g == G - 1 ? PL : P;  // my sweeps (warp-uniform)
+
+  // one step of my group's NT sweeps (NT = P, or PL for the last group)
+  auto step = [&](auto ntc, int k, unsigned a_p) {
+    constexpr int NT = decltype(ntc)::value;
+#pragma unroll
+    for (int i = 0; i < NT; ++i) Un[i] = Vn[i] = Dn[i] = DVn[i] = 0.0;
+    // warp-uniform: any of my warp's pixels inside the level in any of my
+    // sweeps?  (lane 0 holds the warp's largest x; sweep t's x is k - y - 2t)
+    const int xw0 = k - y0 - wr0 - 2 * t0;
+    if (!(live_warp && xw0 >= 0 && xw0 - 2 * (NT - 1) < W + 31)) return;
+    // my first sweep's right / down neighbours and own du
+    double rUf, rVf, dnUf, dnVf, duf = 0.0, dvf = 0.0;
+    if (g == 0) {  // sweep 0: the records (+ the carried du of a chained pass)
+      lds2(a_p + rrow, rUf, rVf);
+      lds2(a_p + rrow + 16, dnUf, dnVf);
+      if (Dui) {
+        const int j = k;
+        const bool hasD = y < H - 1;
+        const int jp = j + 1;
+        const bool okp = jp >= 0 && jp < ndiag;
+        const bool ok = j >= 0 && j < ndiag && y < H;
+        const int yc = y < H ? y : H - 1;
+        rUf = rUf + Dui[okp ? (size_t)jp * H + yc : 0];
+        rVf = rVf + Dvi[okp ? (size_t)jp * H + yc : 0];
+        dnUf = dnUf + Dui[okp && hasD ? (size_t)jp * H + yc + 1 : 0];
+        dnVf = dnVf + Dvi[okp && hasD ? (size_t)jp * H + yc + 1 : 0];
+        duf = Dui[ok ? (size_t)j * H + y : 0];
+        dvf = Dvi[ok ? (size_t)j * H + y : 0];
+      } else {
+        rUf = rUf + 0.0;  // the reference's u[q] + du[q]
+        rVf = rVf + 0.0;
+        dnUf = dnUf + 0.0;
+        dnVf = dnVf + 0.0;
+      }
+    } else {  // the previous group's last sweep (exchange buffers)
+      lds2(uv_r + (unsigned)(t0 - 1) * xstride + rrow + 16, rUf, rVf);
+      lds2(uv_r + (unsigned)(t0 - 1) * xstride + rrow + 32, dnUf, dnVf);
+      lds2(d_r + (unsigned)((g - 1) * Hp * 16) + rrow, duf, dvf);
+    }
+    // all my sweeps' pixels, branch-free (independent chains interleave);
+    // idle pixels see zero records and never update.  The rare operands
+    // outside the fast division's exact range are redone after each pass.
+    double uc[NT], vc[NT], m01[NT], r1[NT], den_u[NT], den_v[NT], sv[NT], du[NT], dv[NT],
+        q[NT], nn[NT];
+    bool dfast[NT], slow[NT];
+    bool any_slow = false;
+    // slot of my first sweep's diagonal k - 2 t0 (mod R)
+    unsigned a_f = a_k - (unsigned)(2 * t0) * slot_bytes;
+    if ((int)(a_k - ring_s) < 2 * t0 * (int)slot_bytes) a_f += (unsigned)R * slot_bytes;
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+      const int t = t0 + i;
+      unsigned a_j = a_f - (unsigned)(2 * i) * slot_bytes;  // slot of k - 2t
+      if (i > 0 && (int)(a_f - ring_s) < 2 * i * (int)slot_bytes) a_j += (unsigned)R * slot_bytes;
+      double r0, wqL, wqR, wqU, wqD, dok;
+      lds2(a_j + rrow, uc[i], vc[i]);
+      lds2(a_j + cstride + rrow, m01[i], r0);
+      lds2(a_j + 2 * cstride + rrow, r1[i], den_u[i]);
+      lds2(a_j + 3 * cstride + rrow, den_v[i], wqL);
+      lds2(a_j + 4 * cstride + rrow, wqR, wqU);
+      lds2(a_j + 5 * cstride + rrow, wqD, dok);
+      dfast[i] = dok != 0.0;
+      double upU, upV, rU, rV, dnU, dnV;
+      lds2(uv_r + (unsigned)t * xstride + rrow, upU, upV);  // exchange row r = band row r-1
+      if (i > 0) {
+        rU = Up[i - 1];
+        rV = Vp[i - 1];
+        lds2(uv_r + (unsigned)(t - 1) * xstride + rrow + 32, dnU, dnV);  // band row r+1
+        du[i] = Dp2[i - 1];
+        dv[i] = DVp2[i - 1];
+      } else {
+        rU = rUf;
+        rV = rVf;
+        dnU = dnUf;
+        dnV = dnVf;
+        du[i] = duf;
+        dv[i] = dvf;
+      }
+      const double cu = uc[i], cv = vc[i];
+      const double su = (((0.0 + wqL * (Up[i] - cu)) + wqR * (rU - cu)) + wqU * (upU - cu)) +
+                        wqD * (dnU - cu);
+      sv[i] = (((0.0 + wqL * (Vp[i] - cv)) + wqR * (rV - cv)) + wqU * (upV - cv)) +
+              wqD * (dnV - cv);
+      nn[i] = r0 + su - m01[i] * dv[i];
+      q[i] = div_fast_rn(nn[i], den_u[i]);
+      slow[i] = (den_u[i] > 1e-12) && !(dfast[i] && num_fast_ok(nn[i]));
+      any_slow |= slow[i];
+    }
+    if (any_slow) {
+#pragma unroll
+      for (int i = 0; i < NT; ++i)
+        if (slow[i]) q[i] = exact_div_pos(nn[i], den_u[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+      const double qq = nn[i] == 0.0 ? nn[i] : q[i];
+      const double nu = om1 * du[i] + omega * qq;
+      du[i] = den_u[i] > 1e-12 ? nu : du[i];
+    }
+    if (!HZ) {
+      any_slow = false;
+#pragma unroll
+      for (int i = 0; i < NT; ++i) {
+        nn[i] = r1[i] + sv[i] - m01[i] * du[i];
+        q[i] = div_fast_rn(nn[i], den_v[i]);
+        slow[i] = (den_v[i] > 1e-12) && !(dfast[i] && num_fast_ok(nn[i]));
+        any_slow |= slow[i];
+      }
+      if (any_slow) {
+#pragma unroll
+        for (int i = 0; i < NT; ++i)
+          if (slow[i]) q[i] = exact_div_pos(nn[i], den_v[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < NT; ++i) {
+        const double qq = nn[i] == 0.0 ? nn[i] : q[i];
+        const double nv = om1 * dv[i] + omega * qq;
+        dv[i] = den_v[i] > 1e-12 ? nv : dv[i];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+      Un[i] = uc[i] + du[i];
+      Vn[i] = vc[i] + dv[i];
+      Dn[i] = du[i];
+      DVn[i] = dv[i];
+    }
+  };
+
+#ifdef DIS_SOR_TRACE
+  const bool tr = blockIdx.x == 0 && threadIdx.x == (unsigned)(DIS_SOR_TRACE);
+#endif
+  for (int k = 0; k < nsteps; ++k) {
+    SOR_TR(0)
+    if (first_owner) {
+      if (g == 0) mbar_expect_tx(bar_above + (unsigned)(k & 1) * 8u, 16u * S);
+      if (k > 0)
+        mbar_wait_parity(bar_above + (unsigned)((k - 1) & 1) * 8u, (unsigned)(((k - 1) >> 1) & 1));
+    }
+    if (last_owner) {
+      if (g == 0) mbar_expect_tx(bar_below + (unsigned)(k & 1) * 8u, 16u * S);
+      if (k > 0)
+        mbar_wait_parity(bar_below + (unsigned)((k - 1) & 1) * 8u, (unsigned)(((k - 1) >> 1) & 1));
+    }
+    if (producer) issue_next();
+    SOR_TR(1)
+    const unsigned a_p = a_k + slot_bytes == ring_end ? ring_s : a_k + slot_bytes;  // k + 1
+    if (PL == P || nt == P)
+      step(std::integral_constant<int, P>{}, k, a_p);
+    else
+      step(std::integral_constant<int, PL>{}, k, a_p);
+    SOR_TR(2)
+    // ---- exchange, halo, output ----
+    if (!producer && r < nrows) {  // padding rows never store
+#pragma unroll
+      for (int i = 0; i < P; ++i)
+        if (i < nt) sts2(uv_w + (unsigned)(t0 + i) * xstride + rrow + 16, Un[i], Vn[i]);
+    }
+    if (G > 1 && !producer && g < G - 1)  // my last sweep's du for the next group
+      sts2(d_w + (unsigned)(g * Hp * 16) + rrow, Dn[P - 1], DVn[P - 1]);
+    if (first_owner) {  // band's first row -> CTA c-1's row below its band
+#pragma unroll
+      for (int i = 0; i < P; ++i)
+        if (i < nt)
+          st_async2(uv_w + (unsigned)(t0 + i) * xstride + (unsigned)((Hc + 1) * 16),
+                    bar_below + (unsigned)(k & 1) * 8u, c - 1, Un[i], Vn[i]);
+    }
+    if (last_owner) {  // band's last row -> CTA c+1's row above its band
+#pragma unroll
+      for (int i = 0; i < P; ++i)
+        if (i < nt)
+          st_async2(uv_w + (unsigned)(t0 + i) * xstride, bar_above + (unsigned)(k & 1) * 8u,
+                    c + 1, Un[i], Vn[i]);
+    }
+    if (!producer && g == G - 1) {  // the last sweep's pixel: outputs
+      const int x = k - y - 2 * (S - 1);
+      const int j = k - 2 * (S - 1);
+      if (r < nrows && x >= 0 && x < W) {
+        const double uo = Un[PL - 1], vo = Vn[PL - 1];
+        if (du_out) {
+          du_out[(size_t)b * Ls + (size_t)j * H + y] = Dn[PL - 1];
+          dv_out[(size_t)b * Ls + (size_t)j * H + y] = DVn[PL - 1];
+        }
+        if (fu) {
+          const size_t oo = (size_t)b * fplane + (size_t)y * W + x;
+          fu[oo] = uo;
+          fv[oo] = vo;
+          bad |= !(isfinite(uo) && isfinite(vo));
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+      Up[i] = Un[i];
+      Vp[i] = Vn[i];
+      Dp2[i] = Dp[i];
+      DVp2[i] = DVp[i];
+      Dp[i] = Dn[i];
+      DVp[i] = DVn[i];
+    }
+    SOR_TR(3)
+    if (filler) wait_diag(k + 2);  // sweep 0 reads k+1 and k+2 next step
+    SOR_TR(4)
+    __syncthreads();
+    SOR_TR(5)
+    a_k = a_p;
+    const unsigned tu = uv_r;
+    uv_r = uv_w;
+    uv_w = tu;
+    d_w += d_ph_b;  // phases k mod 3 and (k-2) mod 3 both advance by one
+    if (d_w == d_end) d_w = xd_s;
+    d_r += d_ph_b;
+    if (d_r == d_end) d_r = xd_s;
+  }
+  if (C > 1) {  // no CTA may exit while a neighbour can still write into it
+    cluster_arrive();
+    cluster_wait();
+  }
+  if (bad) set_status(status, DIS_STATUS_NONFINITE_FLOW);
+}
+
+template <int S>
+static int sor_group_size() {
+  static const int p = [] {
+    const char* e = getenv("DIS_SOR_P");  // experiments only
+    const int v = e ? atoi(e) : 2;  // measured best (c1, c3)
+    return v == 1 || v == 2 || v == 3 ? v : S;
+  }();
+  return p < S ? p : S;
+}
+
+template <int S>
+static size_t sor_rows_smem_bytes(int hp) {
+  const int P = sor_group_size<S>();
+  const int G = (S + P - 1) / P;
+  const size_t rrows = (size_t)hp + 1, xrows = (size_t)hp + 2;
+  return (size_t)ring_slots<S>() * kChunks * rrows * 16 + (size_t)2 * S * xrows * 16 +
+         (size_t)3 * (G > 1 ? G - 1 : 1) * hp * 16 + (4 + ring_slots<S>()) * sizeof(uint64_t);
+}
+
+static bool sor_rows_on() {
+  static const bool on = [] {
+    const char* e = getenv("DIS_SOR_ROWS");  // experiments only
+    return e ? atoi(e) != 0 : true;
+  }();
+  return on;
+}
+
 template <int S>
 static size_t sor_smem_bytes(int hp) {
   const size_t rrows = (size_t)hp + 1, xrows = (size_t)hp + 2;
@@ -679,6 +1087,11 @@ constexpr size_t kMaxSmem = 227 * 1024;
 // its ring in shared memory, and, for small batches, to spread a pair over
 // several SMs (the step rate of one band is bound by its SM).
 template <int S>
+static size_t sor_any_smem_bytes(int hp) {
+  return sor_rows_on() ? sor_rows_smem_bytes<S>(hp) : sor_smem_bytes<S>(hp);
+}
+
+template <int S>
 static int choose_cluster(int B, int H) {
   static const int forced = [] {
     const char* e = getenv("DIS_SOR_CLUSTER");  // experiments only
@@ -687,7 +1100,7 @@ static int choose_cluster(int B, int H) {
   if (forced > 0) return forced;
   auto hp = [&](int C) { return ((H + C - 1) / C + 31) / 32 * 32; };
   int C = 1;
-  while (C < 16 && (hp(C) > kMaxBandRows || sor_smem_bytes<S>(hp(C)) > kMaxSmem)) ++C;
+  while (C < 16 && (hp(C) > kMaxBandRows || sor_any_smem_bytes<S>(hp(C)) > kMaxSmem)) ++C;
   static const int sms = [] {
     int dev = 0, n = 148;
     cudaGetDevice(&dev);
@@ -702,7 +1115,7 @@ static int choose_cluster(int B, int H) {
   // bands of 60 rows run 12 % faster than 5 of 108)
   if (B * C > sms) {
     const int C64 = (H + 63) / 64;
-    if (C64 <= 16 && (long)C64 * 64 <= (long)C * hp(C) && sor_smem_bytes<S>(64) * 2 <= kMaxSmem)
+    if (C64 <= 16 && (long)C64 * 64 <= (long)C * hp(C) && sor_any_smem_bytes<S>(64) * 2 <= kMaxSmem)
       C = C64;
   }
   return C;
@@ -714,14 +1127,30 @@ static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const
   const int C = choose_cluster<S>(a.B, a.H);
   const int Hc = (a.H + C - 1) / C;
   const int hp = (Hc + 31) / 32 * 32;
-  const int threads = hp * S + 32;  // + the producer warp
-  const size_t smem = sor_smem_bytes<S>(hp);
+  const bool rows = sor_rows_on();
+  const int P = sor_group_size<S>();
+  const int G = (S + P - 1) / P;
+  const int threads = (rows ? hp * G : hp * S) + 32;  // + the producer warp
+  const size_t smem = sor_any_smem_bytes<S>(hp);
   if (hp > kMaxBandRows || smem > kMaxSmem) return DIS_ERR_VALUE;
+  using KFn = void (*)(const double*, int, int, int, int, size_t, double, const double*,
+                       const double*, double*, double*, double*, double*, uint32_t*,
+                       const double*);
+  KFn kfn = k_sor<S, HZ>;
+  if (rows) {
+    if (P == 1)
+      kfn = k_sor_rows<S, HZ, 1>;
+    else if (P == 2)
+      kfn = k_sor_rows<S, HZ, (S >= 2 ? 2 : 1)>;
+    else if (P == 3)
+      kfn = k_sor_rows<S, HZ, (S >= 3 ? 3 : 1)>;
+    else
+      kfn = k_sor_rows<S, HZ, S>;
+  }
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_sor<S, HZ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kMaxSmem);
-    cudaFuncSetAttribute(k_sor<S, HZ>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -739,9 +1168,8 @@ static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const
   double* fu = final_pass ? a.fu : nullptr;
   double* fv = final_pass ? a.fv : nullptr;
   const double* zeros = a.rec + (size_t)(kRec + 2) * a.B * Ls;  // zeroed by k_tensor_assemble
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_sor<S, HZ>, (const double*)a.rec, a.B, a.W, a.H,
-                                     Hc, Ls, a.omega, dui, dvi, duo, dvo, fu, fv, a.status,
-                                     zeros);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, (const double*)a.rec, a.B, a.W, a.H, Hc, Ls, a.omega, dui,
+                                     dvi, duo, dvo, fu, fv, a.status, zeros);
   return e == cudaSuccess ? DIS_OK : DIS_ERR_CUDA;
 }
 
@@ -766,6 +1194,12 @@ static int launch_sor(const RefineArgs& a, size_t Ls, int S, const double* dui,
       return DIS_ERR_VALUE;
   }
 }
+
+#ifdef DIS_SOR_TRACE
+extern "C" __attribute__((visibility("default"))) int dis_debug_sor_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_sor_trace, sizeof(g_sor_trace)) == cudaSuccess ? 0 : -5;
+}
+#endif
 
 int launch_refine(const RefineArgs& a, cudaStream_t st) {
   if (a.H > 2048) return DIS_ERR_VALUE;  // at most 16 CTAs of <= 128 rows per pair
