@@ -12,13 +12,13 @@
 //                       den_v = m11 + sw — the same operations in the same
 //                       order, so bit-identical, computed once instead of
 //                       once per sweep.  Writes one 96-byte SOR record per
-//                       pixel (u, v, m01, r0, r1, den_u, den_v, wqL, wqR, wqU,
-//                       wqD, dok) as six 16-byte chunks (dok = 1 when both
-//                       denominators are in the fast-division range) in the skewed,
+//                       pixel (u, v, m01, r0, r1, den_u, den_v, rcp_u, wqR,
+//                       wqU, wqD, rcp_v) as six 16-byte chunks (rcp_* = the
+//                       denominators' refined reciprocals) in the skewed,
 //                       chunk-major layout [x + y][chunk][y]: one chunk of a
 //                       whole anti-diagonal is one contiguous run, so a band
 //                       of a diagonal is six bulk copies.
-//   k_sor<S>          : theta_vi in-place lexicographic SOR sweeps
+//   k_sor<S, HZ, P>   : theta_vi in-place lexicographic SOR sweeps
 //                       (_sor_sweeps, variational.py:124-165) + the update
 //                       u += du, v += dv (266-267) + the finiteness check.
 //
@@ -28,8 +28,8 @@
 // t-1.  Processing pixel (x, y) of sweep t at step k = x + y + 2t respects
 // every one of those dependencies (bit-identical), and at
 // a fixed step row y holds exactly one pixel per sweep, x = k - y - 2t.  A
-// thread owns one (row, sweep) pair; all rows of a band step together with
-// one barrier per step (see k_sor below).
+// thread owns one row and a group of P consecutive sweeps; all rows of a
+// band step together with one barrier per step (see k_sor below).
 //
 // Neighbour terms use U_q = fl(u_q + du_q) exactly as the reference's
 // `u[y, x-1] + du[y, x-1]`; the last sweep's U is the updated flow.
@@ -41,9 +41,11 @@
 
 namespace disb200 {
 
-// SOR record (doubles); 96 bytes = 6 chunks of 16 bytes
+// SOR record (doubles); 96 bytes = 6 chunks of 16 bytes.  RCPU/RCPV are the
+// denominators' refined reciprocals (rcp_refined); the left weight is not
+// stored: wq(x, x-1) == wq(x-1, x), the right weight of the previous pixel.
 enum RecField {
-  F_U = 0, F_V, F_M01, F_R0, F_R1, F_DENU, F_DENV, F_WL, F_WR, F_WU, F_WD, F_DOK, kRec
+  F_U = 0, F_V, F_M01, F_R0, F_R1, F_DENU, F_DENV, F_RCPU, F_WR, F_WU, F_WD, F_RCPV, kRec
 };
 constexpr int kChunks = kRec / 2;  // 16-byte chunks per record
 constexpr int kMaxSweepsPerPass = 8;
@@ -253,10 +255,10 @@ __global__ void __launch_bounds__(256, 3) k_tensor_assemble(RefineArgs a, size_t
       o[0] = make_double2(r[0], r[1]);       // u, v
       o[1] = make_double2(r[3], r[5]);       // m01, r0
       o[2] = make_double2(r[6], r[2] + sw);  // r1, den_u = m00 + sw
-      o[3] = make_double2(r[4] + sw, wqL);   // den_v = m11 + sw, wqL
-      o[4] = make_double2(wqR, wqU);
       const double den_u = r[2] + sw, den_v = r[4] + sw;
-      o[5] = make_double2(wqD, den_fast_ok(den_u) && den_fast_ok(den_v) ? 1.0 : 0.0);
+      o[3] = make_double2(den_v, rcp_refined(den_u));  // den_v = m11 + sw
+      o[4] = make_double2(wqR, wqU);
+      o[5] = make_double2(wqD, rcp_refined(den_v));
     }
   }
   __syncthreads();
@@ -368,336 +370,46 @@ __device__ __forceinline__ void mbar_wait_parity_cta(unsigned bar, unsigned pari
 
 // The wavefront SOR kernel.
 //
-// Thread (sweep t, band row r) computes, at step k, pixel x = k - y - 2t of
-// row y = y0 + r (diagonal j = k - 2t).  A pair's rows are split over a
-// cluster of C CTAs (1..16); CTA c owns the band [c*Hc, c*Hc + Hc), padded to
-// Hp rows (a multiple of 32).  Shared memory:
-//   ring[R][6][Hp+1] x 16 B : the 96-byte records of the live diagonals (band
-//                             rows + the row below, sweep 0's down
-//                             neighbour), chunk-major like the global layout:
-//                             one diagonal = six cp.async.bulk copies issued
-//                             by one thread kLookahead steps ahead, completion
-//                             counted on the slot's mbarrier
-//   xuv[2][S][Hp+2] x 16 B  : U, V of the last two steps (+ halo row above
-//                             and below the band)
-//   xd [3][S][Hp+2] x 16 B  : du, dv of the last three steps
-// Neighbours of (x, y, t): left = own registers (step k-1); up =
-// xuv[k-1][t][y-1]; right = xuv[k-1][t-1][y]; down = xuv[k-1][t-1][y+1]; own
-// previous du/dv = xd[k-2][t-1][y]; for t = 0 the right/down values are the
-// records' u, v (+ du = 0, or the carried du of a chained pass).  The
-// static terms (neighbour weights, sw, denominators) come precomputed in
-// the record.  The band's boundary rows write their U, V straight into the
-// neighbouring CTA's halo rows (distributed shared memory, st.async counted
-// on that CTA's mbarrier).
-//
-// Idle pixels (outside the level: ramp-up/down of the wavefront, rows past
-// the band) see zero records, so they never update and publish U = du = 0;
-// a valid pixel's absent neighbour enters its sums as +0 * 0.  A warp whose
-// 32 pixels are all idle skips the arithmetic (and publishes zeros).
-template <int S, bool HZ>
-__global__ void __launch_bounds__(S * kMaxBandRows + 32, 1)
-    k_sor(const double* __restrict__ rec, int B, int W, int H, int Hc, size_t Ls, double omega,
-          const double* du_in, const double* dv_in, double* du_out, double* dv_out,
-          double* __restrict__ fu, double* __restrict__ fv, uint32_t* status,
-          const double* __restrict__ zeros) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int R = ring_slots<S>();
-  const int C = (int)(gridDim.x / (unsigned)B) > 0 ? (int)(gridDim.x / (unsigned)B) : 1;
-  const int c = C > 1 ? (int)cluster_rank() : 0;
-  const int b = blockIdx.x / C;
-  const int Hp = (blockDim.x - 32) / S;  // band rows (padded); + one producer warp
-  const bool producer = threadIdx.x >= (unsigned)(S * Hp);  // ring fill, no pixels
-  const int t = producer ? 0 : threadIdx.x / Hp;  // sweep
-  const int r = producer ? Hp : threadIdx.x - t * Hp;  // band row (producer: none)
-  const int y0 = c * Hc;
-  const int y = y0 + r;
-  const int nrows = min(Hc, H - y0);
-  const int ndiag = W + H - 1;
-  const int rrows = Hp + 1;  // ring rows
-  const int xrows = Hp + 2;  // exchange rows
-  const unsigned slot_bytes = (unsigned)(kChunks * rrows * 16);
-  const unsigned ring_s = (unsigned)__cvta_generic_to_shared(smem);
-  const unsigned ring_end = ring_s + (unsigned)R * slot_bytes;
-  const unsigned xuv_s = ring_end;
-  const unsigned xd_s = xuv_s + (unsigned)(2 * S * xrows * 16);
-  const unsigned bar_above = xd_s + (unsigned)(3 * S * xrows * 16);  // 8-byte aligned
-  const unsigned bar_below = bar_above + 16;
-  const unsigned bar_ring = bar_above + 32;  // [R] slot-fill barriers
-  const double2* __restrict__ base =
-      reinterpret_cast<const double2*>(rec + (size_t)b * Ls * kRec);  // [d][chunk][H]
-  const double* Dui = du_in ? du_in + (size_t)b * Ls : nullptr;  // may alias du_out
-  const double* Dvi = dv_in ? dv_in + (size_t)b * Ls : nullptr;
-  const double om1 = 1.0 - omega;
-
-  {  // ring + exchange buffers start at zero
-    const unsigned nz = (unsigned)(R * kChunks * rrows + 5 * S * xrows);  // 16-byte entries
-    for (unsigned i = threadIdx.x; i < nz; i += blockDim.x) sts2(ring_s + 16 * i, 0.0, 0.0);
-  }
-  if (threadIdx.x == 0) {
-    if (C > 1) {
-      // one local arrive (the consumer's expect_tx) per phase; the neighbour's
-      // S st.async (16 bytes each) complete the phase's transaction count
-      mbar_init(bar_above, 1);
-      mbar_init(bar_above + 8, 1);
-      mbar_init(bar_below, 1);
-      mbar_init(bar_below + 8, 1);
-    }
-    for (int i = 0; i < R; ++i) mbar_init(bar_ring + 8u * i, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-
-  // ring fill (producer warp): diagonal jn -> slot jn % R.  Invariant: a
-  // slot's row holds the record of (jn - y, y) when that pixel is inside the
-  // level and zero otherwise, so idle pixels compute exactly like the
-  // reference would on zeros (no update: den = 0) and publish U = du = 0.
-  // The valid rows y in [max(y0, jn - W + 1), min(y0 + Hp, H - 1, jn)] are
-  // six bulk copies (one per chunk run); the rows that were valid for the
-  // slot's previous diagonal jn - R but are not any more (the ramp-down
-  // edge) are zeroed by a copy from a zeroed global line.
-  const int ylast = min(y0 + rrows, H) - 1;
-  const unsigned lane = threadIdx.x & 31;
-  int jn = 0;
-  unsigned sin_s = ring_s, sin_bar = bar_ring;
-  auto issue_next = [&]() {
-    const int ya = max(y0, jn - W + 1), yb = min(ylast, jn);
-    const int jo = jn - R;  // the slot's previous diagonal
-    const int pa = max(y0, jo - W + 1), pb = min(ylast, jo);
-    const int za = pa, zb = min(pb, ya <= yb ? ya - 1 : pb);
-    const unsigned zrun = (jo >= 0 && zb >= za) ? (unsigned)(zb - za + 1) * 16u : 0u;
-    const unsigned run = yb >= ya ? (unsigned)(yb - ya + 1) * 16u : 0u;
-    if (lane == 0) {
-      // everything written into the ring goes through the async proxy (the
-      // zeros are copied from a zeroed global line), in disjoint row ranges
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sin_bar),
-                   "r"(kChunks * (run + zrun))
-                   : "memory");
-      if (zrun) {
-        const unsigned dst = sin_s + (unsigned)((za - y0) * 16);
-#pragma unroll
-        for (int cc = 0; cc < kChunks; ++cc)
-          bulk_g2s(dst + (unsigned)(cc * rrows * 16), zeros, zrun, sin_bar);
-      }
-      if (run) {
-        const double2* g = base + (size_t)jn * kChunks * H + ya;
-        const unsigned dst = sin_s + (unsigned)((ya - y0) * 16);
-#pragma unroll
-        for (int cc = 0; cc < kChunks; ++cc)
-          bulk_g2s(dst + (unsigned)(cc * rrows * 16), g + (size_t)cc * H, run, sin_bar);
-      }
-    }
-    ++jn;
-    sin_s += slot_bytes;
-    sin_bar += 8;
-    if (sin_s == ring_end) {
-      sin_s = ring_s;
-      sin_bar = bar_ring;
-    }
-  };
-  // slot readiness: fill n of slot s (diagonal s + nR) completes phase n
-  auto wait_diag = [&](int j) {
-    if (j >= 0 && j < jn)
-      mbar_wait_parity_cta(bar_ring + 8u * (unsigned)(j % R), (unsigned)((j / R) & 1));
-  };
-  const bool filler = threadIdx.x == (unsigned)(S * Hp);  // lane 0 of the producer warp
-  if (producer) {
-    // the start-up clear (generic proxy) before any async-proxy copy
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    for (int j = 0; j < kLookahead; ++j) issue_next();
-    if (filler) {
-      wait_diag(0);
-      wait_diag(1);
-    }
-  }
-  if (C > 1) {  // barriers initialised everywhere before any remote arrive
-    cluster_arrive();
-    cluster_wait();
-  } else {
-    __syncthreads();
-  }
-
-  double lU = 0.0, lV = 0.0;  // this row's previous pixel (left neighbour)
-  bool bad = false;
-  const int nsteps = ndiag + 2 * (S - 1);
-  unsigned a_j = ring_s + (unsigned)(((-2 * t) % R + R) % R) * slot_bytes;  // slot of j = k - 2t
-  const unsigned rrow = (unsigned)(r * 16);
-  const unsigned cstride = (unsigned)(rrows * 16);
-  const unsigned uv_me = (unsigned)((t * xrows + r + 1) * 16);
-  const unsigned uv_prev = (unsigned)(((t > 0 ? t - 1 : 0) * xrows + r + 1) * 16);
-  unsigned uv_r = xuv_s + (unsigned)(S * xrows * 16), uv_w = xuv_s;  // step k-1 / step k
-  const unsigned d_ph_b = (unsigned)(S * xrows * 16);
-  unsigned d_w = xd_s, d_r = xd_s + d_ph_b;  // phase k mod 3 / (k-2) mod 3
-  const unsigned d_end = xd_s + 3 * d_ph_b;
-  const size_t fplane = (size_t)W * H;
-  const int last_r = nrows - 1;
-  const int wr0 = r & ~31;  // first row of my warp
-  // warps holding a band-boundary row (the only ones touching the halo
-  // mbarriers): warp-uniform
-  const bool halo_warp = C > 1 && ((c > 0 && wr0 == 0) || (c < C - 1 && (last_r & ~31) == wr0));
-  const bool first_owner = C > 1 && c > 0 && r == 0;
-  const bool last_owner = C > 1 && c < C - 1 && r == last_r;
-  int x = -y0 - r - 2 * t;  // my pixel at step k
-  int xw = -y0 - wr0 - 2 * t;  // lane 0's pixel (largest x of the warp)
-  const unsigned wact = (!producer && wr0 < nrows) ? (unsigned)(W + 31) : 0u;
-  for (int k = 0; k < nsteps; ++k, ++x, ++xw) {
-    if (halo_warp) {
-      if (first_owner && t == 0) mbar_expect_tx(bar_above + (unsigned)(k & 1) * 8u, 16u * S);
-      if (last_owner && t == 0) mbar_expect_tx(bar_below + (unsigned)(k & 1) * 8u, 16u * S);
-      if (k > 0) {  // halo values of step k-1 from the neighbouring bands
-        const unsigned sel = (unsigned)((k - 1) & 1) * 8u;
-        const unsigned par = (unsigned)(((k - 1) >> 1) & 1);
-        if (first_owner) mbar_wait_parity(bar_above + sel, par);
-        if (last_owner) mbar_wait_parity(bar_below + sel, par);
-      }
-    }
-    if (producer) issue_next();
-    const int j = k - 2 * t;
-    const unsigned a_p = a_j + slot_bytes == ring_end ? ring_s : a_j + slot_bytes;  // j + 1
-    double U = 0.0, V = 0.0, du = 0.0, dv = 0.0;
-    // warp-uniform: any of my warp's 32 pixels inside the level?  (lane 0
-    // holds the warp's largest x)
-    if ((unsigned)xw < wact) {
-      // ---- record (6 x LDS.128) ----
-      double uc, vc, m01, r0, r1, den_u, den_v, wqL, wqR, wqU, wqD, dok;
-      lds2(a_j + rrow, uc, vc);
-      lds2(a_j + cstride + rrow, m01, r0);
-      lds2(a_j + 2 * cstride + rrow, r1, den_u);
-      lds2(a_j + 3 * cstride + rrow, den_v, wqL);
-      lds2(a_j + 4 * cstride + rrow, wqR, wqU);
-      lds2(a_j + 5 * cstride + rrow, wqD, dok);
-      const bool dfast = dok != 0.0;
-      // ---- neighbours ----
-      double upU, upV, rU, rV, dnU, dnV;
-      lds2(uv_r + uv_me - 16, upU, upV);
-      if (t > 0) {
-        lds2(uv_r + uv_prev, rU, rV);
-        lds2(uv_r + uv_prev + 16, dnU, dnV);
-        lds2(d_r + uv_prev, du, dv);
-      } else {
-        // (x+1, y) and (x, y+1) of sweep "-1": u + du of the records, du = 0
-        // or the carried du of a chained pass; absent ones -> 0 (the slot may
-        // hold anything there)
-        lds2(a_p + rrow, rU, rV);
-        lds2(a_p + rrow + 16, dnU, dnV);
-        if (Dui) {
-          const bool hasD = y < H - 1;
-          const int jp = j + 1;
-          const bool okp = jp >= 0 && jp < ndiag;
-          const bool ok = j >= 0 && j < ndiag && y < H;
-          const int yc = y < H ? y : H - 1;
-          rU = rU + Dui[okp ? (size_t)jp * H + yc : 0];
-          rV = rV + Dvi[okp ? (size_t)jp * H + yc : 0];
-          dnU = dnU + Dui[okp && hasD ? (size_t)jp * H + yc + 1 : 0];
-          dnV = dnV + Dvi[okp && hasD ? (size_t)jp * H + yc + 1 : 0];
-          du = Dui[ok ? (size_t)j * H + y : 0];
-          dv = Dvi[ok ? (size_t)j * H + y : 0];
-        } else {
-          rU = rU + 0.0;  // the reference's u[q] + du[q]
-          rV = rV + 0.0;
-          dnU = dnU + 0.0;
-          dnV = dnV + 0.0;
-        }
-      }
-      // ---- the update (variational.py:133-165): absent neighbours have
-      // wq = +0, which adds an exact zero to the partial sums ----
-      const double su = (((0.0 + wqL * (lU - uc)) + wqR * (rU - uc)) + wqU * (upU - uc)) +
-                        wqD * (dnU - uc);
-      const double sv = (((0.0 + wqL * (lV - vc)) + wqR * (rV - vc)) + wqU * (upV - vc)) +
-                        wqD * (dnV - vc);
-      const double nU = r0 + su - m01 * dv;
-      {
-        const bool slow = (den_u > 1e-12) && !(dfast && num_fast_ok(nU));
-        double m = div_fast_rn(nU, den_u);
-        if (slow) m = exact_div_pos(nU, den_u);
-        const double q = nU == 0.0 ? nU : m;
-        const double nu = om1 * du + omega * q;
-        du = den_u > 1e-12 ? nu : du;
-      }
-      if (!HZ) {
-        const double nV = r1 + sv - m01 * du;
-        const bool slow = (den_v > 1e-12) && !(dfast && num_fast_ok(nV));
-        double m = div_fast_rn(nV, den_v);
-        if (slow) m = exact_div_pos(nV, den_v);
-        const double q = nV == 0.0 ? nV : m;
-        const double nv = om1 * dv + omega * q;
-        dv = den_v > 1e-12 ? nv : dv;
-      }
-      U = uc + du;
-      V = vc + dv;
-    }
-    lU = U;
-    lV = V;
-    // ---- exchange, halo, output ----
-    if (r < nrows) {  // padding rows never store
-      sts2(uv_w + uv_me, U, V);
-      sts2(d_w + uv_me, du, dv);
-    }
-    if (halo_warp) {
-      if (r == 0 && c > 0)  // band's first row -> CTA c-1's row below its band
-        st_async2(uv_w + (unsigned)((t * xrows + Hc + 1) * 16),
-                  bar_below + (unsigned)(k & 1) * 8u, c - 1, U, V);
-      if (r == last_r && c < C - 1)  // band's last row -> CTA c+1's row above its band
-        st_async2(uv_w + (unsigned)(t * xrows * 16), bar_above + (unsigned)(k & 1) * 8u, c + 1,
-                  U, V);
-    }
-    if (t == S - 1 && r < nrows && x >= 0 && x < W) {
-      if (du_out) {
-        du_out[(size_t)b * Ls + (size_t)j * H + y] = du;
-        dv_out[(size_t)b * Ls + (size_t)j * H + y] = dv;
-      }
-      if (fu) {
-        const size_t oo = (size_t)b * fplane + (size_t)y * W + x;
-        fu[oo] = U;
-        fv[oo] = V;
-        bad |= !(isfinite(U) && isfinite(V));
-      }
-    }
-    if (filler) wait_diag(k + 2);  // sweep 0 reads k+1 and k+2 next step
-    __syncthreads();
-    a_j = a_p;
-    const unsigned tu = uv_r;
-    uv_r = uv_w;
-    uv_w = tu;
-    d_w += d_ph_b;  // phases k mod 3 and (k-2) mod 3 both advance by one
-    if (d_w == d_end) d_w = xd_s;
-    d_r += d_ph_b;
-    if (d_r == d_end) d_r = xd_s;
-  }
-  if (C > 1) {  // no CTA may exit while a neighbour can still write into it
-    cluster_arrive();
-    cluster_wait();
-  }
-  if (bad) set_status(status, DIS_STATUS_NONFINITE_FLOW);
-}
-
-// The wavefront SOR kernel, grouped form: thread (g, r) owns band row
-// y = y0 + r and a group of P consecutive sweeps t = gP .. gP+P-1 (the last
-// group may hold fewer), and computes, at step k, the pixels x_t = k - y - 2t
-// of its sweeps (independent within the step, so their chains interleave).
-// The per-step control, barrier and exchange work is shared by the group's
-// pixels, and inside a group three of the five neighbour terms come from
-// the thread's own registers:
+// Thread (g, r) owns band row y = y0 + r and a group of P consecutive sweeps
+// t = gP .. gP+P-1 (the last group may hold fewer), and computes, at step k,
+// the pixels x_t = k - y - 2t of its sweeps (diagonals j = k - 2t;
+// independent within the step, so their chains interleave).  A pair's rows
+// are split over a cluster of C CTAs (1..16); CTA c owns the band
+// [c*Hc, c*Hc + Hc), padded to Hp rows (a multiple of 32).  Inside a group
+// three of the five neighbour terms come from the thread's own registers:
 //   left  (x-1, y) of sweep t   = my sweep-t value of step k-1
 //   right (x+1, y) of sweep t-1 = my sweep-(t-1) value of step k-1
 //   self du of sweep t-1        = my sweep-(t-1) du of step k-2
 //   up    (x, y-1) of sweep t   = row r-1's sweep-t value of step k-1 (xuv)
 //   down  (x, y+1) of sweep t-1 = row r+1's sweep-(t-1) value of step k-1 (xuv)
 // A group's first sweep takes right from xuv and self du from xd (written
-// by the previous group's last sweep two steps before); sweep 0's come from
-// the records (+ the carried du of a chained pass), as in k_sor.  Shared
-// memory: the same record ring, xuv[2][S][Hp+2] x 16 B (U, V of the last
-// two steps + halo rows), xd[3][G-1][Hp] x 16 B.  The arithmetic of every
-// pixel update is k_sor's, operation for operation.
-#ifdef DIS_SOR_TRACE
-__device__ long long g_sor_trace[6][1024];
-#define SOR_TR(i) \
-  if (tr && k < 1024) g_sor_trace[i][k] = clock64();
-#else
-#define SOR_TR(i)
-#endif
+// by the previous group's last sweep two steps before); sweep 0's right,
+// down and self terms are the records' u, v (+ du = 0, or the carried du of
+// a chained pass).  The left weight is the previous pixel's right weight
+// (same operands, commutative add) and the denominators' reciprocals come
+// refined in the record, so an update is operation for operation the
+// reference's: su, sv in its neighbour order, then the two divisions.
+// Shared memory:
+//   ring[R][6][Hp+1] x 16 B : the 96-byte records of the live diagonals (band
+//                             rows + the row below, sweep 0's down
+//                             neighbour), chunk-major like the global layout:
+//                             one diagonal = six cp.async.bulk copies issued
+//                             by the producer warp kLookahead steps ahead,
+//                             completion counted on the slot's mbarrier
+//   xuv[2][S][Hp+2] x 16 B  : U, V of the last two steps (+ halo rows above
+//                             and below the band)
+//   xd [3][G-1][Hp] x 16 B  : group-boundary du, dv of the last three steps
+// The band's boundary rows write their U, V straight into the neighbouring
+// CTA's halo rows (distributed shared memory, st.async counted on that
+// CTA's mbarrier).
+//
+// Idle pixels (outside the level: ramp-up/down of the wavefront, rows past
+// the band) see zero records, so they never update and publish U = du = 0;
+// a valid pixel's absent neighbour enters its sums as +0 * 0.  A warp whose
+// pixels are all idle skips the arithmetic (and publishes zeros).
 template <int S, bool HZ, int P>
 __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
-    k_sor_rows(const double* __restrict__ rec, int B, int W, int H, int Hc, size_t Ls,
+    k_sor(const double* __restrict__ rec, int B, int W, int H, int Hc, size_t Ls,
                double omega, const double* du_in, const double* dv_in, double* du_out,
                double* dv_out, double* __restrict__ fu, double* __restrict__ fv,
                uint32_t* status, const double* __restrict__ zeros) {
@@ -750,7 +462,13 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
   }
   __syncthreads();
 
-  // ring fill by the producer warp: as in k_sor
+  // ring fill (producer warp): diagonal jn -> slot jn % R.  Invariant: a
+  // slot's row holds the record of (jn - y, y) when that pixel is inside the
+  // level and zero otherwise.  The valid rows y in [max(y0, jn - W + 1),
+  // min(y0 + Hp, H - 1, jn)] are six bulk copies (one per chunk run); the
+  // rows that were valid for the slot's previous diagonal jn - R but are not
+  // any more (the ramp-down edge) are zeroed by a copy from a zeroed global
+  // line.
   const int ylast = min(y0 + rrows, H) - 1;
   const unsigned lane = threadIdx.x & 31;
   int jn = 0;
@@ -808,9 +526,10 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
   }
   const int nsteps = ndiag + 2 * (S - 1);
   // my values of the last two steps, per sweep of my group
-  double Up[P], Vp[P], Dp[P], DVp[P], Dp2[P], DVp2[P], Un[P], Vn[P], Dn[P], DVn[P];
+  double Up[P], Vp[P], Dp[P], DVp[P], Dp2[P], DVp2[P], WRp[P], Un[P], Vn[P], Dn[P], DVn[P],
+      WRn[P];
 #pragma unroll
-  for (int i = 0; i < P; ++i) Up[i] = Vp[i] = Dp[i] = DVp[i] = Dp2[i] = DVp2[i] = 0.0;
+  for (int i = 0; i < P; ++i) Up[i] = Vp[i] = Dp[i] = DVp[i] = Dp2[i] = DVp2[i] = WRp[i] = 0.0;
   bool bad = false;
   unsigned a_k = ring_s;  // slot of diagonal k
   const unsigned rrow = (unsigned)(r * 16);
@@ -831,7 +550,7 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
   auto step = [&](auto ntc, int k, unsigned a_p) {
     constexpr int NT = decltype(ntc)::value;
 #pragma unroll
-    for (int i = 0; i < NT; ++i) Un[i] = Vn[i] = Dn[i] = DVn[i] = 0.0;
+    for (int i = 0; i < NT; ++i) Un[i] = Vn[i] = Dn[i] = DVn[i] = WRn[i] = 0.0;
     // warp-uniform: any of my warp's pixels inside the level in any of my
     // sweeps?  (lane 0 holds the warp's largest x; sweep t's x is k - y - 2t)
     const int xw0 = k - y0 - wr0 - 2 * t0;
@@ -868,8 +587,8 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
     // all my sweeps' pixels, branch-free (independent chains interleave);
     // idle pixels see zero records and never update.  The rare operands
     // outside the fast division's exact range are redone after each pass.
-    double uc[NT], vc[NT], m01[NT], r1[NT], den_u[NT], den_v[NT], sv[NT], du[NT], dv[NT],
-        q[NT], nn[NT];
+    double uc[NT], vc[NT], m01[NT], r1[NT], den_u[NT], den_v[NT], rcp_v[NT], sv[NT], du[NT],
+        dv[NT], q[NT], nn[NT];
     bool dfast[NT], slow[NT];
     bool any_slow = false;
     // slot of my first sweep's diagonal k - 2 t0 (mod R)
@@ -880,14 +599,16 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
       const int t = t0 + i;
       unsigned a_j = a_f - (unsigned)(2 * i) * slot_bytes;  // slot of k - 2t
       if (i > 0 && (int)(a_f - ring_s) < 2 * i * (int)slot_bytes) a_j += (unsigned)R * slot_bytes;
-      double r0, wqL, wqR, wqU, wqD, dok;
+      double r0, rcp_u, wqR, wqU, wqD;
       lds2(a_j + rrow, uc[i], vc[i]);
       lds2(a_j + cstride + rrow, m01[i], r0);
       lds2(a_j + 2 * cstride + rrow, r1[i], den_u[i]);
-      lds2(a_j + 3 * cstride + rrow, den_v[i], wqL);
+      lds2(a_j + 3 * cstride + rrow, den_v[i], rcp_u);
       lds2(a_j + 4 * cstride + rrow, wqR, wqU);
-      lds2(a_j + 5 * cstride + rrow, wqD, dok);
-      dfast[i] = dok != 0.0;
+      lds2(a_j + 5 * cstride + rrow, wqD, rcp_v[i]);
+      const double wqL = WRp[i];  // the previous pixel's right weight
+      WRn[i] = wqR;
+      dfast[i] = den_fast_ok(den_u[i]) && den_fast_ok(den_v[i]);
       double upU, upV, rU, rV, dnU, dnV;
       lds2(uv_r + (unsigned)t * xstride + rrow, upU, upV);  // exchange row r = band row r-1
       if (i > 0) {
@@ -910,7 +631,7 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
       sv[i] = (((0.0 + wqL * (Vp[i] - cv)) + wqR * (rV - cv)) + wqU * (upV - cv)) +
               wqD * (dnV - cv);
       nn[i] = r0 + su - m01[i] * dv[i];
-      q[i] = div_fast_rn(nn[i], den_u[i]);
+      q[i] = div_by_rcp(nn[i], den_u[i], rcp_u);
       slow[i] = (den_u[i] > 1e-12) && !(dfast[i] && num_fast_ok(nn[i]));
       any_slow |= slow[i];
     }
@@ -930,7 +651,7 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
 #pragma unroll
       for (int i = 0; i < NT; ++i) {
         nn[i] = r1[i] + sv[i] - m01[i] * du[i];
-        q[i] = div_fast_rn(nn[i], den_v[i]);
+        q[i] = div_by_rcp(nn[i], den_v[i], rcp_v[i]);
         slow[i] = (den_v[i] > 1e-12) && !(dfast[i] && num_fast_ok(nn[i]));
         any_slow |= slow[i];
       }
@@ -955,11 +676,7 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
     }
   };
 
-#ifdef DIS_SOR_TRACE
-  const bool tr = blockIdx.x == 0 && threadIdx.x == (unsigned)(DIS_SOR_TRACE);
-#endif
   for (int k = 0; k < nsteps; ++k) {
-    SOR_TR(0)
     if (first_owner) {
       if (g == 0) mbar_expect_tx(bar_above + (unsigned)(k & 1) * 8u, 16u * S);
       if (k > 0)
@@ -971,13 +688,11 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
         mbar_wait_parity(bar_below + (unsigned)((k - 1) & 1) * 8u, (unsigned)(((k - 1) >> 1) & 1));
     }
     if (producer) issue_next();
-    SOR_TR(1)
     const unsigned a_p = a_k + slot_bytes == ring_end ? ring_s : a_k + slot_bytes;  // k + 1
     if (PL == P || nt == P)
       step(std::integral_constant<int, P>{}, k, a_p);
     else
       step(std::integral_constant<int, PL>{}, k, a_p);
-    SOR_TR(2)
     // ---- exchange, halo, output ----
     if (!producer && r < nrows) {  // padding rows never store
 #pragma unroll
@@ -1021,16 +736,14 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
     for (int i = 0; i < P; ++i) {
       Up[i] = Un[i];
       Vp[i] = Vn[i];
+      WRp[i] = WRn[i];
       Dp2[i] = Dp[i];
       DVp2[i] = DVp[i];
       Dp[i] = Dn[i];
       DVp[i] = DVn[i];
     }
-    SOR_TR(3)
     if (filler) wait_diag(k + 2);  // sweep 0 reads k+1 and k+2 next step
-    SOR_TR(4)
     __syncthreads();
-    SOR_TR(5)
     a_k = a_p;
     const unsigned tu = uv_r;
     uv_r = uv_w;
@@ -1051,8 +764,8 @@ template <int S>
 static int sor_group_size() {
   static const int p = [] {
     const char* e = getenv("DIS_SOR_P");  // experiments only
-    const int v = e ? atoi(e) : 2;  // measured best (c1, c3)
-    return v == 1 || v == 2 || v == 3 ? v : S;
+    const int v = e ? atoi(e) : 1;  // measured best (c1, c3, c4)
+    return v == 1 || v == 2 ? v : S;
   }();
   return p < S ? p : S;
 }
@@ -1066,30 +779,7 @@ static size_t sor_rows_smem_bytes(int hp) {
          (size_t)3 * (G > 1 ? G - 1 : 1) * hp * 16 + (4 + ring_slots<S>()) * sizeof(uint64_t);
 }
 
-static bool sor_rows_on() {
-  static const bool on = [] {
-    const char* e = getenv("DIS_SOR_ROWS");  // experiments only
-    return e ? atoi(e) != 0 : true;
-  }();
-  return on;
-}
-
-template <int S>
-static size_t sor_smem_bytes(int hp) {
-  const size_t rrows = (size_t)hp + 1, xrows = (size_t)hp + 2;
-  return (size_t)ring_slots<S>() * kChunks * rrows * 16 + (size_t)5 * S * xrows * 16 +
-         (4 + ring_slots<S>()) * sizeof(uint64_t);
-}
-
 constexpr size_t kMaxSmem = 227 * 1024;
-
-// rows-per-CTA split: enough CTAs per pair to keep every band <= 128 rows and
-// its ring in shared memory, and, for small batches, to spread a pair over
-// several SMs (the step rate of one band is bound by its SM).
-template <int S>
-static size_t sor_any_smem_bytes(int hp) {
-  return sor_rows_on() ? sor_rows_smem_bytes<S>(hp) : sor_smem_bytes<S>(hp);
-}
 
 template <int S>
 static int choose_cluster(int B, int H) {
@@ -1100,7 +790,7 @@ static int choose_cluster(int B, int H) {
   if (forced > 0) return forced;
   auto hp = [&](int C) { return ((H + C - 1) / C + 31) / 32 * 32; };
   int C = 1;
-  while (C < 16 && (hp(C) > kMaxBandRows || sor_any_smem_bytes<S>(hp(C)) > kMaxSmem)) ++C;
+  while (C < 16 && (hp(C) > kMaxBandRows || sor_rows_smem_bytes<S>(hp(C)) > kMaxSmem)) ++C;
   static const int sms = [] {
     int dev = 0, n = 148;
     cudaGetDevice(&dev);
@@ -1115,7 +805,7 @@ static int choose_cluster(int B, int H) {
   // bands of 60 rows run 12 % faster than 5 of 108)
   if (B * C > sms) {
     const int C64 = (H + 63) / 64;
-    if (C64 <= 16 && (long)C64 * 64 <= (long)C * hp(C) && sor_any_smem_bytes<S>(64) * 2 <= kMaxSmem)
+    if (C64 <= 16 && (long)C64 * 64 <= (long)C * hp(C) && sor_rows_smem_bytes<S>(64) * 2 <= kMaxSmem)
       C = C64;
   }
   return C;
@@ -1127,26 +817,19 @@ static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const
   const int C = choose_cluster<S>(a.B, a.H);
   const int Hc = (a.H + C - 1) / C;
   const int hp = (Hc + 31) / 32 * 32;
-  const bool rows = sor_rows_on();
   const int P = sor_group_size<S>();
   const int G = (S + P - 1) / P;
-  const int threads = (rows ? hp * G : hp * S) + 32;  // + the producer warp
-  const size_t smem = sor_any_smem_bytes<S>(hp);
+  const int threads = hp * G + 32;  // + the producer warp
+  const size_t smem = sor_rows_smem_bytes<S>(hp);
   if (hp > kMaxBandRows || smem > kMaxSmem) return DIS_ERR_VALUE;
   using KFn = void (*)(const double*, int, int, int, int, size_t, double, const double*,
                        const double*, double*, double*, double*, double*, uint32_t*,
                        const double*);
-  KFn kfn = k_sor<S, HZ>;
-  if (rows) {
-    if (P == 1)
-      kfn = k_sor_rows<S, HZ, 1>;
-    else if (P == 2)
-      kfn = k_sor_rows<S, HZ, (S >= 2 ? 2 : 1)>;
-    else if (P == 3)
-      kfn = k_sor_rows<S, HZ, (S >= 3 ? 3 : 1)>;
-    else
-      kfn = k_sor_rows<S, HZ, S>;
-  }
+  KFn kfn = k_sor<S, HZ, S>;
+  if (P == 1)
+    kfn = k_sor<S, HZ, 1>;
+  else if (P == 2)
+    kfn = k_sor<S, HZ, (S >= 2 ? 2 : 1)>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
@@ -1194,12 +877,6 @@ static int launch_sor(const RefineArgs& a, size_t Ls, int S, const double* dui,
       return DIS_ERR_VALUE;
   }
 }
-
-#ifdef DIS_SOR_TRACE
-extern "C" __attribute__((visibility("default"))) int dis_debug_sor_trace(long long* out) {
-  return cudaMemcpyFromSymbol(out, g_sor_trace, sizeof(g_sor_trace)) == cudaSuccess ? 0 : -5;
-}
-#endif
 
 int launch_refine(const RefineArgs& a, cudaStream_t st) {
   if (a.H > 2048) return DIS_ERR_VALUE;  // at most 16 CTAs of <= 128 rows per pair
