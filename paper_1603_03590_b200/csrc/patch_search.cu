@@ -423,7 +423,8 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
   // (one sector per lane per load instead of one per element) and shifted
   // into place by the lane's offset o = idx mod 4 (two select levels)
   auto load_row = [&](size_t idx, double* s) {
-    if (PS > 8) {  // (wider rows: the shift registers cost more than the loads save)
+    if (PS > 12) {  // (wider rows: the shift registers cost more than the loads save;
+                    // measured at 12: c4's patch search 46.8 -> 39.0 ms)
 #pragma unroll
       for (int c = 0; c < S1; ++c) s[c] = __ldg(qry + idx + c);
       return;
