@@ -218,7 +218,9 @@ __device__ __forceinline__ double pixel_ws(const RefineArgs& a, int b, int x, in
 // one-pixel ring (the neighbours' ws), then each pixel's record (system +
 // static SOR terms) staged in shared memory and written out as contiguous
 // diagonal runs of 96-byte records (16-byte stores, coalesced).
-__global__ void __launch_bounds__(256, 3) k_tensor_assemble(RefineArgs a, size_t Ls) {
+// 4 blocks per SM (64 registers): the gathers are latency-bound; measured
+// 3 -> 4 blocks: c1 0.62 -> 0.57 ms, c3 10.7 -> 9.7 ms (5 blocks spill)
+__global__ void __launch_bounds__(256, 4) k_tensor_assemble(RefineArgs a, size_t Ls) {
   constexpr int HX = kTTX + 2, HY = kTTY + 2;
   constexpr int kPad = kChunks + 1;  // 7 x 16 B per staged record: conflict-free writes
   __shared__ double ws_t[HY][HX];
