@@ -51,8 +51,7 @@ __device__ __forceinline__ Cover cover_range(const GridAxis& ax, int ps, int y, 
 
 // one thread per pixel (2D tiles of 32 x 8): covering patches in ascending
 // (grid row, grid column) order = the reference's ascending patch index
-// 6 blocks per SM (40 registers; measured c3 4.95 -> 4.78 ms)
-__global__ void __launch_bounds__(256, 6) k_densify(const double* __restrict__ ref_all,
+__global__ void __launch_bounds__(256) k_densify(const double* __restrict__ ref_all,
                                                  const double* __restrict__ qry_all, int W,
                                                  int H, GridAxis ax, GridAxis ay, int ps,
                                                  unsigned magic, const double* __restrict__ pu,
