@@ -388,23 +388,48 @@ def run_ours(args, cfg, params):
     fp64_peak_tflops = min(dadd.value, dmul.value) / 1e3
 
     # ---- timed region: device-resident inputs (> L2: 2 x B x H x W x 4 B) ----
-    L.dis_profile_reset()
-    L.dis_profile_enable(1)
+    # `value`: the step replayed as one CUDA graph (FlowEngine.run(graph=True):
+    # the same kernels and arguments, without the per-launch gaps); captured
+    # and replayed once before timing.  Then a second timed pass of the same
+    # steps with eager launches and per-kernel-class CUDA events gives the
+    # kernel breakdown and the rooflines (events between launches add a
+    # little time, so that pass's step time is reported beside `value`).
+    gstream = torch.cuda.Stream(device=dev)
+    gstream.wait_stream(stream)
+    use_graph = not args.no_graph
+    if use_graph:
+        eng.run(f1, f2, out=out, stream=gstream, check=True, graph=True)
+    torch.cuda.synchronize(dev)
     clocks = ClockSampler(dev.index).start()
     barrier()
     torch.cuda.synchronize(dev)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
+    ev0.record(gstream)
+    for _ in range(args.steps):
+        eng.run(f1, f2, out=out, stream=gstream, check=False, graph=use_graph)
+    ev1.record(gstream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    ms_total = sharding.max_over_ranks(ev0.elapsed_time(ev1), device=dev)
+    eng.check_status(gstream)  # any non-finite / coverage failure raises here
+    # kernel-breakdown pass (eager, per-class events)
+    L.dis_profile_reset()
+    L.dis_profile_enable(1)
+    barrier()
+    torch.cuda.synchronize(dev)
+    ev2 = torch.cuda.Event(enable_timing=True)
+    ev3 = torch.cuda.Event(enable_timing=True)
+    ev2.record(stream)
     for _ in range(args.steps):
         eng.run(f1, f2, out=out, stream=stream, check=False)
-    ev1.record(stream)
+    ev3.record(stream)
     torch.cuda.synchronize(dev)
     barrier()
     clk = clocks.stop()
     L.dis_profile_enable(0)
-    ms_total = sharding.max_over_ranks(ev0.elapsed_time(ev1), device=dev)
-    eng.check_status(stream)  # any non-finite / coverage failure raises here
+    ms_eager = sharding.max_over_ranks(ev2.elapsed_time(ev3), device=dev) / args.steps
+    eng.check_status(stream)
     nk = len(_lib.KERNEL_CLASSES)
     kms = (ctypes.c_double * nk)()
     kcnt = (ctypes.c_int64 * nk)()
@@ -508,6 +533,11 @@ def run_ours(args, cfg, params):
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk, "kernels": kernels,
+            "timing": {"value": ("CUDA-graph replay of each step (FlowEngine.run(graph=True))"
+                                 if use_graph else "eager launches"),
+                       "kernels": "second timed pass: eager launches, per-class CUDA events "
+                                  "on the launch stream",
+                       "eager_ms_per_step": ms_eager},
             "fp64_peak": {"dadd_TFLOPs": dadd.value / 1e3, "dmul_TFLOPs": dmul.value / 1e3},
         }
         print(json.dumps(line), flush=True)
@@ -525,6 +555,8 @@ def main(argv=None):
     ap.add_argument("--config", default="c1", choices=sorted(synth.CONFIGS))
     ap.add_argument("--batch", type=int, default=0, help="pairs per GPU (default: config)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time eager launches instead of the CUDA-graph replay")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-pairs", type=int, default=64)

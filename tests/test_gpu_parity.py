@@ -256,6 +256,31 @@ def test_host_buffer_path_matches_device_path(torch):
     assert np.array_equal(dev, host)
 
 
+def test_graph_replay_matches_eager_and_reports_errors(torch):
+    from paper_1603_03590_b200 import FlowEngine
+
+    cfg = synth.CONFIGS["c0"]
+    f1, f2 = synth.make_batch(cfg, seed=6, count=2)
+    eng = FlowEngine(2, cfg.height, cfg.width, synth.dis_params(cfg))
+    a, b = torch.from_numpy(f1).cuda(), torch.from_numpy(f2).cuda()
+    eager = eng.run(a, b).cpu().numpy()
+    out = torch.zeros((2, cfg.height, cfg.width, 2), dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    for _ in range(3):  # capture once, replay
+        out.zero_()
+        eng.run(a, b, out=out, stream=s, graph=True)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), eager)
+    # new contents in the captured buffers: the replay recomputes them
+    a.copy_(b)
+    eng.run(a, b, out=out, stream=s, graph=True)
+    assert np.array_equal(out.cpu().numpy(), eng.run(b, b).cpu().numpy())
+    # the status word is reset and checked inside every replay
+    a[0, 5, 5] = float("inf")
+    with pytest.raises(ValueError):
+        eng.run(a, b, out=out, stream=s, graph=True)
+
+
 def test_error_types(torch):
     from paper_1603_03590_b200 import ParameterError, dis_flow
 
