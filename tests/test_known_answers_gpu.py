@@ -197,3 +197,126 @@ def test_constant_patches_are_invalid_and_keep_their_init(torch, st):
                           coarse, coarse)
     assert not out["valid"].any()
     assert (out["u"].cpu().numpy() == 1.5).all() and (out["v"].cpu().numpy() == 1.5).all()
+
+
+# ---- reference test intents on a rendered texture (test_inverse_search.py,
+# test_variational.py), through the grid stage API ---------------------------
+
+def _waves(seed, n=8, lo=6.0, hi=20.0):
+    rng = np.random.default_rng(seed)
+    lam = rng.uniform(lo, hi, n)
+    ang = rng.uniform(0, 2 * np.pi, n)
+    ph = rng.uniform(0, 2 * np.pi, n)
+    amp = rng.uniform(10.0, 30.0, n)
+    return lam, ang, ph, amp
+
+
+def _render(w, width, height, shift=(0.0, 0.0)):
+    """sum of plane waves sampled at (x - sx, y - sy): a continuous texture
+    translated by `shift` (so the flow from the unshifted frame is `shift`)."""
+    lam, ang, ph, amp = w
+    ys, xs = np.mgrid[0:height, 0:width].astype(np.float64)
+    xs = xs - shift[0]
+    ys = ys - shift[1]
+    img = np.full((height, width), 128.0)
+    for L, a, p, A in zip(lam, ang, ph, amp):
+        img += A * np.sin(2 * np.pi * (np.cos(a) * xs + np.sin(a) * ys) / L + p)
+    return img
+
+
+def _search_center(st, ref_img, qry_img, **kw):
+    """The 8px patch centred at (16, 16) of a 32x32 level (grid spacing 4,
+    origin (12, 12), patch index 3 * 7 + 3); returns (u, v, mar)."""
+    ref = st.build_pyramid(ref_img, 0)[0]
+    qry = st.build_pyramid(qry_img, 0)[0]
+    p = DisParams(patch_size=8, overlap=0.5, **kw)
+    out = st.patch_search(ref, qry["img"], p)
+    i = 3 * 7 + 3
+    return (float(out["u"][0, i]), float(out["v"][0, i]), float(out["mar"][0, i]))
+
+
+def test_identity_is_an_exact_fixed_point(torch, st):
+    img = _render(_waves(4), 32, 32)
+    u, v, mar = _search_center(st, img, img, iterations=16)
+    assert u == 0.0 and v == 0.0 and mar == 0.0
+
+
+def test_integer_translation_is_recovered(torch, st):
+    w = _waves(5)
+    u, v, _ = _search_center(st, _render(w, 32, 32), _render(w, 32, 32, (2.0, 1.0)),
+                             iterations=16)
+    assert abs(u - 2.0) < 0.05 and abs(v - 1.0) < 0.05
+
+
+def test_large_translation_is_outside_the_single_level_basin(torch, st):
+    w = _waves(6)
+    ref = st.build_pyramid(_render(w, 64, 32), 0)[0]
+    qry = st.build_pyramid(_render(w, 64, 32, (20.0, 0.0)), 0)[0]
+    out = st.patch_search(ref, qry["img"], DisParams(patch_size=8, overlap=0.5, iterations=16))
+    i = 3 * 15 + 7  # centre (32, 16) of a 15 x 7 grid
+    err = np.hypot(float(out["u"][0, i]) - 20.0, float(out["v"][0, i]))
+    assert err > 1.0
+
+
+def test_mean_normalization_ignores_a_constant_offset(torch, st):
+    w = _waves(8)
+    ref = _render(w, 32, 32)
+    qry = _render(w, 32, 32, (1.3, -0.7))
+    a = _search_center(st, ref, qry, iterations=12)
+    b = _search_center(st, ref, qry + 50.0, iterations=12)
+    assert abs(a[0] - b[0]) <= 1e-9 and abs(a[1] - b[1]) <= 1e-9
+    c = _search_center(st, ref, qry + 50.0, iterations=12, use_mean_normalization=False)
+    assert np.hypot(c[0] - a[0], c[1] - a[1]) > 0.01
+
+
+def test_patch_search_is_deterministic(torch, st):
+    w = _waves(9)
+    ref, qry = _render(w, 32, 32), _render(w, 32, 32, (1.5, 0.5))
+    assert _search_center(st, ref, qry, iterations=12) == _search_center(st, ref, qry,
+                                                                         iterations=12)
+
+
+def test_huber_norm_reduces_outlier_influence(torch, st):
+    w = _waves(10)
+    ref = _render(w, 32, 32)
+    qry = _render(w, 32, 32, (1.0, 0.5))
+    qry[12:16, 12:16] += 200.0  # corrupt part of the window
+    l2 = _search_center(st, ref, qry, iterations=12)
+    hub = _search_center(st, ref, qry, iterations=12, residual_norm="huber", huber_b=1.0)
+    assert np.hypot(hub[0] - 1.0, hub[1] - 0.5) < np.hypot(l2[0] - 1.0, l2[1] - 0.5)
+
+
+def test_refine_reduces_the_error_of_a_noisy_initialisation(torch, st):
+    w = _waves(11, lo=8.0, hi=24.0)
+    H, W = 40, 48
+    ref = st.build_pyramid(_render(w, W, H), 0)[0]
+    qry = st.build_pyramid(_render(w, W, H, (1.0, -0.5)), 0)[0]
+    rng = np.random.default_rng(12)
+    u0 = 1.0 + rng.normal(0, 0.3, (1, H, W))
+    v0 = -0.5 + rng.normal(0, 0.3, (1, H, W))
+    u, v = st.refine(_cu(torch, u0), _cu(torch, v0), ref, qry,
+                     DisParams(variational=VarParams()), 3)
+    inner = (slice(None), slice(4, H - 4), slice(4, W - 4))
+    e0 = np.hypot(u0 - 1.0, v0 + 0.5)[inner].mean()
+    e1 = np.hypot(u.cpu().numpy() - 1.0, v.cpu().numpy() + 0.5)[inner].mean()
+    assert e1 < 0.5 * e0
+
+
+def test_refine_horizontal_only_keeps_v(torch, st):
+    w = _waves(13)
+    ref = st.build_pyramid(_render(w, 40, 24), 0)[0]
+    qry = st.build_pyramid(_render(w, 40, 24, (1.5, 0.0)), 0)[0]
+    rng = np.random.default_rng(14)
+    u0 = _cu(torch, rng.normal(1.5, 0.2, (1, 24, 40)))
+    v0 = torch.zeros_like(u0)
+    u, v = st.refine(u0, v0, ref, qry, DisParams(mode="stereo", variational=VarParams()), 2)
+    assert not v.any()
+    assert not torch.equal(u, u0)
+
+
+def test_refine_rejects_non_finite_flow(torch, st):
+    lv = st.build_pyramid(np.random.default_rng(15).uniform(0, 255, (16, 16)), 0)[0]
+    u0 = torch.zeros((1, 16, 16), dtype=torch.float64, device="cuda")
+    u0[0, 8, 8] = float("nan")
+    with pytest.raises(RuntimeError):
+        st.refine(u0, torch.zeros_like(u0), lv, lv, DisParams(variational=VarParams()), 1)
