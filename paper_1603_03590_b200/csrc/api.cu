@@ -573,6 +573,7 @@ size_t host_chunk_bytes(int Bc, int H, int W, int dtype, const dis_params_t* p) 
 struct HostStreams {
   int dev = -1;
   cudaStream_t s[kHostChunksMax] = {};
+  cudaStream_t cap = nullptr;  // graph capture origin (never the legacy stream)
   cudaEvent_t start = nullptr, done[kHostChunksMax] = {};
 };
 std::mutex g_host_mu;
@@ -716,6 +717,52 @@ int dis_stereo_batch_host(const void* host_left, const void* host_right, int32_t
 }  // extern "C"
 
 namespace {
+// The host path's whole enqueue (copies in, every chunk's kernels, copies
+// out on the chunk streams) is replayed as one CUDA graph when the call
+// repeats with the same pinned host buffers, workspace, stream and problem
+// (captured on the second such call; the first runs eagerly and performs
+// the kernels' one-time set-up).  Saves the per-launch gaps of the
+// latency-bound per-chunk pipelines.
+struct HostGraph {
+  const void* f1 = nullptr;
+  const void* f2 = nullptr;
+  const void* out = nullptr;
+  const void* ws = nullptr;
+  void* stream = nullptr;
+  int32_t dtype = -1, B = 0, H = 0, W = 0;
+  bool stereo = false;
+  int dev = -1;
+  dis_params_t p{};
+  int seen = 0;
+  cudaGraphExec_t exec = nullptr;
+  long long launches = 0;
+};
+constexpr int kHostGraphs = 4;
+HostGraph g_hgraph[kHostGraphs];
+int g_hgraph_next = 0;
+
+bool host_graphs_on() {
+  static const bool on = [] {
+    const char* e = getenv("DIS_HOST_GRAPH");  // experiments only
+    return e ? atoi(e) != 0 : true;
+  }();
+  return on;
+}
+
+bool is_pinned(const void* ptr) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+int host_batch_enqueue(const void* host_frame1, const void* host_frame2, int32_t dtype,
+                       int32_t B, int32_t H, int32_t W, const dis_params_t* p,
+                       double* host_flow_out, void* workspace, cudaStream_t st, bool stereo,
+                       int n, int Bc, size_t per, int* used_out);
+
 int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dtype, int32_t B,
                     int32_t H, int32_t W, const dis_params_t* p, double* host_flow_out,
                     void* workspace, size_t workspace_bytes, void* stream, bool stereo) {
@@ -742,9 +789,95 @@ int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dt
       cudaEventCreateWithFlags(&hs.done[i], cudaEventDisableTiming);
     }
     cudaEventCreateWithFlags(&hs.start, cudaEventDisableTiming);
+    cudaStreamCreateWithFlags(&hs.cap, cudaStreamNonBlocking);
     hs.dev = dev;
   }
   cudaStream_t st = as_stream(stream);
+  // graph cache lookup (pinned host buffers only: pageable copies cannot be
+  // captured)
+  HostGraph* hg = nullptr;
+  if (host_graphs_on()) {
+    for (int i = 0; i < kHostGraphs; ++i) {
+      HostGraph& g = g_hgraph[i];
+      if (g.f1 == host_frame1 && g.f2 == host_frame2 && g.out == host_flow_out &&
+          g.ws == workspace && g.stream == stream && g.dtype == dtype && g.B == B && g.H == H &&
+          g.W == W && g.stereo == stereo && g.dev == dev &&
+          std::memcmp(&g.p, p, sizeof(dis_params_t)) == 0) {
+        hg = &g;
+        break;
+      }
+    }
+    if (!hg && is_pinned(host_frame1) && is_pinned(host_frame2) && is_pinned(host_flow_out)) {
+      hg = &g_hgraph[g_hgraph_next];
+      g_hgraph_next = (g_hgraph_next + 1) % kHostGraphs;
+      if (hg->exec) cudaGraphExecDestroy(hg->exec);
+      *hg = HostGraph{};
+      hg->f1 = host_frame1;
+      hg->f2 = host_frame2;
+      hg->out = host_flow_out;
+      hg->ws = workspace;
+      hg->stream = stream;
+      hg->dtype = dtype;
+      hg->B = B;
+      hg->H = H;
+      hg->W = W;
+      hg->stereo = stereo;
+      hg->dev = dev;
+      hg->p = *p;
+    }
+  }
+  int used = 0;
+  if (hg && hg->exec) {  // replay
+    if (cudaGraphLaunch(hg->exec, st) != cudaSuccess)
+      return fail(DIS_ERR_CUDA, "dis_flow_batch_host: graph launch failed");
+    used = (B + Bc - 1) / Bc;
+    g_launches = hg->launches;
+  } else if (hg && hg->seen >= 1) {  // capture this call, then replay it
+    cudaGraph_t graph = nullptr;
+    if (cudaStreamBeginCapture(hs.cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+      return fail(DIS_ERR_CUDA, "dis_flow_batch_host: stream capture failed");
+    rc = host_batch_enqueue(host_frame1, host_frame2, dtype, B, H, W, p, host_flow_out,
+                            workspace, hs.cap, stereo, n, Bc, per, &used);
+    const cudaError_t ce = cudaStreamEndCapture(hs.cap, &graph);
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (ce != cudaSuccess || cudaGraphInstantiate(&hg->exec, graph, 0) != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      hg->exec = nullptr;
+      return fail(DIS_ERR_CUDA, "dis_flow_batch_host: graph capture failed");
+    }
+    cudaGraphDestroy(graph);
+    hg->launches = g_launches.load();
+    if (cudaGraphLaunch(hg->exec, st) != cudaSuccess)
+      return fail(DIS_ERR_CUDA, "dis_flow_batch_host: graph launch failed");
+  } else {
+    if (hg) ++hg->seen;
+    rc = host_batch_enqueue(host_frame1, host_frame2, dtype, B, H, W, p, host_flow_out,
+                            workspace, st, stereo, n, Bc, per, &used);
+    if (rc) return rc;
+  }
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return fail(DIS_ERR_CUDA, "dis_flow_batch_host: %s", cudaGetErrorString(e));
+  uint32_t any = 0;
+  for (int c = 0; c < used; ++c) {
+    uint32_t status = 0;
+    e = cudaMemcpy(&status, static_cast<char*>(workspace) + (size_t)c * per, sizeof(uint32_t),
+                   cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return fail(DIS_ERR_CUDA, "dis_flow_batch_host: %s", cudaGetErrorString(e));
+    any |= status;
+  }
+  return dis_status_to_error(any);
+}
+int host_batch_enqueue(const void* host_frame1, const void* host_frame2, int32_t dtype,
+                       int32_t B, int32_t H, int32_t W, const dis_params_t* p,
+                       double* host_flow_out, void* workspace, cudaStream_t st, bool stereo,
+                       int n, int Bc, size_t per, int* used_out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  HostStreams& hs = g_host[dev & 15];
+  int rc = DIS_OK;
   cudaEventRecord(hs.start, st);  // chunks start after the caller's prior work
   const size_t esz = dtype_size(dtype);
   const size_t px = (size_t)H * W;
@@ -779,17 +912,8 @@ int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dt
   }
   for (int c = 0; c < used; ++c) cudaStreamWaitEvent(st, hs.done[c], 0);
   g_launches = launches;
-  cudaError_t e = cudaStreamSynchronize(st);
-  if (e != cudaSuccess) return fail(DIS_ERR_CUDA, "dis_flow_batch_host: %s", cudaGetErrorString(e));
-  uint32_t any = 0;
-  for (int c = 0; c < used; ++c) {
-    uint32_t status = 0;
-    e = cudaMemcpy(&status, static_cast<char*>(workspace) + (size_t)c * per, sizeof(uint32_t),
-                   cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) return fail(DIS_ERR_CUDA, "dis_flow_batch_host: %s", cudaGetErrorString(e));
-    any |= status;
-  }
-  return dis_status_to_error(any);
+  *used_out = used;
+  return DIS_OK;
 }
 }  // namespace
 
