@@ -548,13 +548,13 @@ constexpr int kHostChunksMax = 16;
 
 // chunks of the host-buffer pipeline: more chunks overlap more of the copies
 // (the first H2D and the last D2H are exposed) at the cost of smaller kernels
-// (measured on c1/c3: 8 pairs per chunk, 4..16 chunks)
+// (measured on c1 with the graph replay: 4 pairs per chunk, 4..16 chunks)
 int host_chunks(int B) {
   static const int forced = [] {
     const char* e = getenv("DIS_HOST_CHUNKS");  // experiments only
     return e ? atoi(e) : 0;
   }();
-  int want = forced > 0 ? forced : B / 8;
+  int want = forced > 0 ? forced : B / 4;
   want = want < 4 ? 4 : (want > kHostChunksMax ? kHostChunksMax : want);
   return B >= want ? want : (B < 1 ? 1 : B);
 }
