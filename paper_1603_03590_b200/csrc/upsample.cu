@@ -7,18 +7,11 @@
 
 namespace disb200 {
 
-__global__ void __launch_bounds__(256) k_upsample(const double* __restrict__ iu,
-                                                  const double* __restrict__ iv, int W, int H,
-                                                  double* __restrict__ ou,
-                                                  double* __restrict__ ov,
-                                                  double* __restrict__ oi, int Wn, int Hn) {
-  const int b = blockIdx.z;
-  const int x = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
-  if (x >= Wn || y >= Hn) return;
-  const size_t plane = (size_t)W * H;
-  // bilinear_map (core.py:154-170) of u and v at the same coordinate: one
-  // clamp/floor/fraction setup, then the numpy formula for each component
+// bilinear_map (core.py:154-170) of u and v at output pixel (x, y): one
+// clamp/floor/fraction setup, then the numpy formula for each component
+__device__ __forceinline__ void upsample_px(const double* __restrict__ U,
+                                            const double* __restrict__ V, int W, int H, int x,
+                                            int y, double& u, double& v) {
   double xs = (double)x / 2.0;
   double ys = (double)y / 2.0;
   xs = xs > W - 1.0 ? W - 1.0 : xs;
@@ -28,21 +21,57 @@ __global__ void __launch_bounds__(256) k_upsample(const double* __restrict__ iu,
   const int y1 = y0 + 1 < H - 1 ? y0 + 1 : H - 1;
   const double fx = xs - (double)x0, fy = ys - (double)y0;
   const double gx = 1.0 - fx, gy = 1.0 - fy;
-  const double* U = iu + b * plane;
-  const double* V = iv + b * plane;
   const size_t r0 = (size_t)y0 * W, r1 = (size_t)y1 * W;
   const double ut = __ldg(U + r0 + x0) * gx + __ldg(U + r0 + x1) * fx;
   const double ub = __ldg(U + r1 + x0) * gx + __ldg(U + r1 + x1) * fx;
   const double vt = __ldg(V + r0 + x0) * gx + __ldg(V + r0 + x1) * fx;
   const double vb = __ldg(V + r1 + x0) * gx + __ldg(V + r1 + x1) * fx;
-  const double u = (ut * gy + ub * fy) * 2.0;
-  const double v = (vt * gy + vb * fy) * 2.0;
+  u = (ut * gy + ub * fy) * 2.0;
+  v = (vt * gy + vb * fy) * 2.0;
+}
+
+// Two horizontally adjacent output pixels per thread (x = 2i, 2i + 1 share
+// their source columns through L1); the interleaved final field is written
+// as one 32-byte streaming store per thread.
+__global__ void __launch_bounds__(256) k_upsample(const double* __restrict__ iu,
+                                                  const double* __restrict__ iv, int W, int H,
+                                                  double* __restrict__ ou,
+                                                  double* __restrict__ ov,
+                                                  double* __restrict__ oi, int Wn, int Hn) {
+  const int b = blockIdx.z;
+  const int x = 2 * (blockIdx.x * 32 + (threadIdx.x & 31));
+  const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (x >= Wn || y >= Hn) return;
+  const size_t plane = (size_t)W * H;
+  const double* U = iu + b * plane;
+  const double* V = iv + b * plane;
   const size_t g = ((size_t)b * Hn + y) * Wn + x;
-  if (oi) {
-    __stcs(reinterpret_cast<double2*>(oi) + g, make_double2(u, v));  // streamed: not re-read
+  double u0, v0;
+  upsample_px(U, V, W, H, x, y, u0, v0);
+  if (x + 1 < Wn) {
+    double u1, v1;
+    upsample_px(U, V, W, H, x + 1, y, u1, v1);
+    if (oi) {
+      double* d = oi + 2 * g;
+      if ((reinterpret_cast<uintptr_t>(d) & 31) == 0) {  // streamed: not re-read
+        asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(d), "d"(u0), "d"(v0),
+                     "d"(u1), "d"(v1)
+                     : "memory");
+      } else {
+        __stcs(reinterpret_cast<double2*>(oi) + g, make_double2(u0, v0));
+        __stcs(reinterpret_cast<double2*>(oi) + g + 1, make_double2(u1, v1));
+      }
+    } else {
+      ou[g] = u0;
+      ov[g] = v0;
+      ou[g + 1] = u1;
+      ov[g + 1] = v1;
+    }
+  } else if (oi) {
+    __stcs(reinterpret_cast<double2*>(oi) + g, make_double2(u0, v0));
   } else {
-    ou[g] = u;
-    ov[g] = v;
+    ou[g] = u0;
+    ov[g] = v0;
   }
 }
 
@@ -63,7 +92,7 @@ static unsigned blocks_for(size_t n) {
 void launch_upsample(const double* iu, const double* iv, int B, int W, int H, double* ou,
                      double* ov, double* out_interleaved, int Wn, int Hn, cudaStream_t st) {
   prof_begin(KC_UPSAMPLE, st);
-  dim3 g((unsigned)((Wn + 31) / 32), (unsigned)((Hn + 7) / 8), (unsigned)B);
+  dim3 g((unsigned)((Wn + 63) / 64), (unsigned)((Hn + 7) / 8), (unsigned)B);
   k_upsample<<<g, 256, 0, st>>>(iu, iv, W, H, ou, ov, out_interleaved, Wn, Hn);
   prof_end(KC_UPSAMPLE, st);
   note_launch();
