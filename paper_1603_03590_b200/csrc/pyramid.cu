@@ -230,25 +230,39 @@ __global__ void __launch_bounds__(256) k_gradients_tile(const double* __restrict
   }
 }
 
-// gx / gy only (no second derivatives): one thread per pixel, the image_gradients
-// stencil (core.py:75-85) read straight from the level (rows coalesced, the
-// vertical neighbours hit L1/L2), gx and gy written coalesced
+// gx / gy only (no second derivatives): two horizontally adjacent pixels per
+// thread, the image_gradients stencil (core.py:75-85) read straight from the
+// level (rows coalesced, the vertical neighbours hit L1/L2), gx and gy
+// written as 16-byte stores when the pair is 16-byte aligned
 __global__ void __launch_bounds__(256) k_gradients_xy(const double* __restrict__ img_all, int H,
                                                       int W, double* __restrict__ gx_all,
                                                       double* __restrict__ gy_all) {
   const int b = blockIdx.z;
-  const int x = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int x = 2 * (blockIdx.x * 32 + (threadIdx.x & 31));
   const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
   if (x >= W || y >= H) return;
   const size_t plane = (size_t)W * H;
   const double* row = img_all + b * plane + (size_t)y * W;
-  const int xm = x > 0 ? x - 1 : 0, xp = x < W - 1 ? x + 1 : W - 1;
   const double* up = img_all + b * plane + (size_t)(y > 0 ? y - 1 : 0) * W;
   const double* dn = img_all + b * plane + (size_t)(y < H - 1 ? y + 1 : H - 1) * W;
   const size_t o = b * plane + (size_t)y * W + x;
   // clamped indices = the one-sided border forms (x = 0: f[1] - f[0], ...)
-  if (gx_all) gx_all[o] = 0.5 * (__ldg(row + xp) - __ldg(row + xm));
-  if (gy_all) gy_all[o] = 0.5 * (__ldg(dn + x) - __ldg(up + x));
+  auto gxv = [&](int xx) {
+    const int xm = xx > 0 ? xx - 1 : 0, xp = xx < W - 1 ? xx + 1 : W - 1;
+    return 0.5 * (__ldg(row + xp) - __ldg(row + xm));
+  };
+  auto gyv = [&](int xx) { return 0.5 * (__ldg(dn + xx) - __ldg(up + xx)); };
+  if (x + 1 < W && (o & 1) == 0) {
+    if (gx_all)
+      *reinterpret_cast<double2*>(gx_all + o) = make_double2(gxv(x), gxv(x + 1));
+    if (gy_all)
+      *reinterpret_cast<double2*>(gy_all + o) = make_double2(gyv(x), gyv(x + 1));
+  } else {
+    for (int q = 0; q < 2 && x + q < W; ++q) {
+      if (gx_all) gx_all[o + q] = gxv(x + q);
+      if (gy_all) gy_all[o + q] = gyv(x + q);
+    }
+  }
 }
 
 // level 1 straight from the frames + the finiteness check of every input
@@ -324,7 +338,7 @@ static void launch_pyramid_t(const T* frames, int B, int H, int W, int coarsest,
       if (dd && dd[s]) {
         k_gradients_tile<<<g, 256, 0, st>>>(img[s], h, w, gx[s], gy[s], dd[s]);
       } else {
-        dim3 g2((unsigned)((w + 31) / 32), (unsigned)((h + 7) / 8), (unsigned)B);
+        dim3 g2((unsigned)((w + 63) / 64), (unsigned)((h + 7) / 8), (unsigned)B);
         k_gradients_xy<<<g2, 256, 0, st>>>(img[s], h, w, gx[s], gy[s]);
       }
       note_launch();
