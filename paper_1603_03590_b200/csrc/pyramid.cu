@@ -266,32 +266,74 @@ __global__ void __launch_bounds__(256) k_gradients_xy(const double* __restrict__
 }
 
 // level 1 straight from the frames + the finiteness check of every input
-// pixel (as_image, core.py:65-72), one pass over the frames
+// pixel (as_image, core.py:65-72), one pass over the frames; two output
+// pixels (four input columns) per thread, 16-byte output stores
+template <typename T>
+__device__ __forceinline__ void load4(const T* p, double* v) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) v[q] = to_f64(p[q]);
+}
+template <>
+__device__ __forceinline__ void load4<float>(const float* p, double* v) {
+  if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+    const float4 f = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = f.x;
+    v[1] = f.y;
+    v[2] = f.z;
+    v[3] = f.w;
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = (double)p[q];
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_level1_checked(const T* __restrict__ frames, int H,
                                                         int W, double* __restrict__ out,
                                                         uint32_t* status) {
   const int Ho = H / 2, Wo = W / 2;
   const int b = blockIdx.z;
-  const int X = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int X = 2 * (blockIdx.x * 32 + (threadIdx.x & 31));  // first of my two outputs
   const int Y = blockIdx.y * 8 + (threadIdx.x >> 5);
   bool bad = false;
   if (X < Wo && Y < Ho) {
     const T* r0 = frames + ((size_t)b * H + 2 * Y) * W + 2 * X;
     const T* r1 = r0 + W;
-    const double a = to_f64(r0[0]), bb = to_f64(r0[1]), c = to_f64(r1[0]), d = to_f64(r1[1]);
-    bad = !(isfinite(a) && isfinite(bb) && isfinite(c) && isfinite(d));
-    out[((size_t)b * Ho + Y) * Wo + X] = ((a + bb) + (c + d)) / 4.0;
+    const size_t o = ((size_t)b * Ho + Y) * Wo + X;
+    if (X + 1 < Wo) {
+      double t[4], u[4];
+      load4<T>(r0, t);
+      load4<T>(r1, u);
+      bad = !(isfinite(t[0]) && isfinite(t[1]) && isfinite(t[2]) && isfinite(t[3]) &&
+              isfinite(u[0]) && isfinite(u[1]) && isfinite(u[2]) && isfinite(u[3]));
+      const double o0 = ((t[0] + t[1]) + (u[0] + u[1])) / 4.0;
+      const double o1 = ((t[2] + t[3]) + (u[2] + u[3])) / 4.0;
+      if ((o & 1) == 0) {
+        *reinterpret_cast<double2*>(out + o) = make_double2(o0, o1);
+      } else {
+        out[o] = o0;
+        out[o + 1] = o1;
+      }
+    } else {
+      const double a = to_f64(r0[0]), bb = to_f64(r0[1]), c = to_f64(r1[0]), d = to_f64(r1[1]);
+      bad = !(isfinite(a) && isfinite(bb) && isfinite(c) && isfinite(d));
+      out[o] = ((a + bb) + (c + d)) / 4.0;
+    }
   }
   // the pixels no 2x2 block covers (odd last column / row)
-  if ((W & 1) && X == Wo - 1 && Y < H / 2) {
+  const bool last_pair = X <= Wo - 1 && Wo - 1 <= X + 1;  // holds output column Wo - 1
+  if ((W & 1) && last_pair && Y < H / 2) {
     bad |= !isfinite(to_f64(frames[((size_t)b * H + 2 * Y) * W + W - 1]));
     bad |= !isfinite(to_f64(frames[((size_t)b * H + 2 * Y + 1) * W + W - 1]));
   }
-  if ((H & 1) && Y == Ho - 1 && X < W / 2) {
-    bad |= !isfinite(to_f64(frames[((size_t)b * H + H - 1) * W + 2 * X]));
-    bad |= !isfinite(to_f64(frames[((size_t)b * H + H - 1) * W + 2 * X + 1]));
-    if ((W & 1) && X == Wo - 1) bad |= !isfinite(to_f64(frames[((size_t)b * H + H - 1) * W + W - 1]));
+  if ((H & 1) && Y == Ho - 1) {
+    for (int q = 0; q < 2; ++q) {
+      const int Xq = X + q;
+      if (Xq >= W / 2) break;
+      bad |= !isfinite(to_f64(frames[((size_t)b * H + H - 1) * W + 2 * Xq]));
+      bad |= !isfinite(to_f64(frames[((size_t)b * H + H - 1) * W + 2 * Xq + 1]));
+      if ((W & 1) && Xq == Wo - 1) bad |= !isfinite(to_f64(frames[((size_t)b * H + H - 1) * W + W - 1]));
+    }
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) set_status(status, DIS_STATUS_NONFINITE_INPUT);
 }
@@ -321,7 +363,7 @@ static void launch_pyramid_t(const T* frames, int B, int H, int W, int coarsest,
     const int ho = h / 2, wo = w / 2;
     const size_t n = (size_t)B * ho * wo;
     if (s == 1 && img[0] == nullptr) {
-      dim3 g((unsigned)((wo + 31) / 32), (unsigned)((ho + 7) / 8), (unsigned)B);
+      dim3 g((unsigned)((wo + 63) / 64), (unsigned)((ho + 7) / 8), (unsigned)B);
       k_level1_checked<T><<<g, TH, 0, st>>>(frames, H, W, img[1], status);
     } else {
       k_downsample<<<grid_for(n, TH), TH, 0, st>>>(img[s - 1], B, h, w, img[s]);
