@@ -28,6 +28,12 @@
 #include <cstdlib>
 
 #include "common.cuh"
+// 12px lane kernel: blocks per SM and row-loop unroll (compile-time
+// experiment knobs; 1 block + unroll 2 is 6 % faster at c2, 2 % slower at c4)
+#ifndef DIS_ROW_UNROLL12
+#define DIS_ROW_UNROLL12 1
+#endif
+constexpr int kRowUnroll12 = DIS_ROW_UNROLL12;
 #include "kernels.cuh"
 
 namespace disb200 {
@@ -442,6 +448,7 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
     }
 #pragma unroll
     for (int c = 0; c < PS; ++c) A[c] = s1[c] + FX[c] * (s1[c + 1] - s1[c]);
+#pragma unroll (PS == 8 ? PS : kRowUnroll12)
     for (int oy = 0; oy < PS; ++oy) {
       if (kPre) {
 #pragma unroll
@@ -489,6 +496,7 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
     const double* tr = ref + (size_t)y0i * W + x0i;
     const double* gxr = rgx + (size_t)y0i * W + x0i;
     const double* gyr = rgy + (size_t)y0i * W + x0i;
+#pragma unroll (PS == 8 ? PS : kRowUnroll12)
     for (int oy = 0; oy < PS; ++oy) {
       if (kPre) {
 #pragma unroll
@@ -599,7 +607,13 @@ __device__ __forceinline__ void eval_general(const double* __restrict__ qry,
 // window is not regular is parked (state to the spill list) and finished by
 // k_patch_gn_general — this keeps the warp on one code path.
 template <int PS, int CODE>
-__global__ void __launch_bounds__(256, 2) k_patch_gn(SearchArgs a,
+// 8px patches: one 256-lane block per SM with the row loops fully unrolled
+// (no register rotation of the prefetched rows and interpolants; 238
+// registers): measured 1.50 -> 1.37 ms at c1 against 2 blocks with rolled loops
+#ifndef DIS_GN12_MINB
+#define DIS_GN12_MINB 2
+#endif
+__global__ void __launch_bounds__(256, PS == 8 ? 1 : DIS_GN12_MINB) k_patch_gn(SearchArgs a,
                                                      const double* __restrict__ prep,
                                                      unsigned* counter, double* spill,
                                                      unsigned* spill_count) {
