@@ -27,6 +27,8 @@
 #include <cfloat>
 #include <cstdlib>
 
+#include <type_traits>
+
 #include "common.cuh"
 // 12px lane kernel: blocks per SM and row-loop unroll (compile-time
 // experiment knobs; 1 block + unroll 2 is 6 % faster at c2, 2 % slower at c4)
@@ -137,7 +139,39 @@ __global__ void __launch_bounds__(128) k_patch_prep(SearchArgs a, double* __rest
   // rows 32-byte aligned (element offset and pitch multiples of 4, e.g. grid
   // spacing 4): 256-bit loads, one sector per lane per load
   const size_t off0 = (size_t)b * plane + (size_t)y0i * W + x0i;
-  if ((ps & 3) == 0 && ((off0 | (size_t)W) & 3) == 0) {
+  // the common patch sizes with compile-time loops (all rows' loads in
+  // flight ahead of the sequential sums)
+  auto rows_fixed = [&](auto psc) {
+    constexpr int PSc = decltype(psc)::value;
+    if (((off0 | (size_t)W) & 3) == 0) {
+#pragma unroll
+      for (int oy = 0; oy < PSc; ++oy) {
+        const size_t row = (size_t)(y0i + oy) * W + x0i;
+#pragma unroll
+        for (int ox = 0; ox < PSc; ox += 4) {
+          double t[4], gx4[4], gy4[4];
+          ldg256(ref + row + ox, t);
+          ldg256(rgx + row + ox, gx4);
+          ldg256(rgy + row + ox, gy4);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) add(t[q], gx4[q], gy4[q]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int oy = 0; oy < PSc; ++oy) {
+        const size_t row = (size_t)(y0i + oy) * W + x0i;
+#pragma unroll
+        for (int ox = 0; ox < PSc; ++ox)
+          add(__ldg(ref + row + ox), __ldg(rgx + row + ox), __ldg(rgy + row + ox));
+      }
+    }
+  };
+  if (ps == 8) {
+    rows_fixed(std::integral_constant<int, 8>{});
+  } else if (ps == 12) {
+    rows_fixed(std::integral_constant<int, 12>{});
+  } else if ((ps & 3) == 0 && ((off0 | (size_t)W) & 3) == 0) {
     for (int oy = 0; oy < ps; ++oy) {
       const size_t row = (size_t)(y0i + oy) * W + x0i;
       for (int ox = 0; ox < ps; ox += 4) {
