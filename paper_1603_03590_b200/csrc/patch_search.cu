@@ -30,12 +30,6 @@
 #include <type_traits>
 
 #include "common.cuh"
-// 12px lane kernel: blocks per SM and row-loop unroll (compile-time
-// experiment knobs; 1 block + unroll 2 is 6 % faster at c2, 2 % slower at c4)
-#ifndef DIS_ROW_UNROLL12
-#define DIS_ROW_UNROLL12 1
-#endif
-constexpr int kRowUnroll12 = DIS_ROW_UNROLL12;
 #include "kernels.cuh"
 
 namespace disb200 {
@@ -446,7 +440,7 @@ __device__ __forceinline__ bool window_regular(double bx, double by, int W, int 
 // the column alone, b of row oy IS a of row oy+1 (same operands, same
 // operations), so each row's horizontal interpolants are computed once and
 // carried down.  CODE is the residual norm (_transform_residual).
-template <int PS, int CODE>
+template <int PS, int CODE, int UNR>
 __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
                                              const double* __restrict__ ref,
                                              const double* __restrict__ rgx,
@@ -482,7 +476,7 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
     }
 #pragma unroll
     for (int c = 0; c < PS; ++c) A[c] = s1[c] + FX[c] * (s1[c + 1] - s1[c]);
-#pragma unroll (PS == 8 ? PS : kRowUnroll12)
+#pragma unroll (UNR)
     for (int oy = 0; oy < PS; ++oy) {
       if (kPre) {
 #pragma unroll
@@ -530,7 +524,7 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
     const double* tr = ref + (size_t)y0i * W + x0i;
     const double* gxr = rgx + (size_t)y0i * W + x0i;
     const double* gyr = rgy + (size_t)y0i * W + x0i;
-#pragma unroll (PS == 8 ? PS : kRowUnroll12)
+#pragma unroll (UNR)
     for (int oy = 0; oy < PS; ++oy) {
       if (kPre) {
 #pragma unroll
@@ -640,14 +634,15 @@ __device__ __forceinline__ void eval_general(const double* __restrict__ qry,
 // lanes read the same image rows and share L1 lines).  A patch whose next
 // window is not regular is parked (state to the spill list) and finished by
 // k_patch_gn_general — this keeps the warp on one code path.
-template <int PS, int CODE>
-// 8px patches: one 256-lane block per SM with the row loops fully unrolled
-// (no register rotation of the prefetched rows and interpolants; 238
-// registers): measured 1.50 -> 1.37 ms at c1 against 2 blocks with rolled loops
-#ifndef DIS_GN12_MINB
-#define DIS_GN12_MINB 2
-#endif
-__global__ void __launch_bounds__(256, PS == 8 ? 1 : DIS_GN12_MINB) k_patch_gn(SearchArgs a,
+// Blocks per SM (MINB) and the row loops' unroll: 8px patches run one
+// 256-lane block per SM with the rows fully unrolled (no register rotation
+// of the prefetched rows and interpolants; 238 registers; c1 1.50 -> 1.37
+// ms against 2 blocks with rolled loops).  12px patches: one block with the
+// rows unrolled by 2 on levels up to 1 Mpixel (c2 8.1 -> 7.5 ms), two blocks
+// with rolled rows on larger ones (better at c4's 1920x1080 level, whose
+// gathers miss L1 more often).
+template <int PS, int CODE, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_patch_gn(SearchArgs a,
                                                      const double* __restrict__ prep,
                                                      unsigned* counter, double* spill,
                                                      unsigned* spill_count) {
@@ -713,7 +708,7 @@ __global__ void __launch_bounds__(256, PS == 8 ? 1 : DIS_GN12_MINB) k_patch_gn(S
     const bool tmpl128 = (PS & 1) == 0 && __all_sync(am, ((toff | (size_t)W) & 1) == 0);
     const bool tmpl256 = (PS & 3) == 0 && __all_sync(am, ((toff | (size_t)W) & 3) == 0);
     double off, ssd, b0, b1, mar;
-    eval_regular<PS, CODE>(a.qry + po, a.ref + po, a.rgx + po, a.rgy + po, W, H, L.x0i, L.y0i,
+    eval_regular<PS, CODE, (PS == 8 ? PS : (MINB == 1 ? 2 : 1))>(a.qry + po, a.ref + po, a.rgx + po, a.rgy + po, W, H, L.x0i, L.y0i,
                            by, FX, xbase, ybase, L.mean_t, mean_norm, a.hb, tmpl128, tmpl256, off,
                            ssd, b0, b1, mar);
     gn_update(L, a, PS, off, ssd, b0, b1, mar);
@@ -959,19 +954,33 @@ static void launch_gn_group(const SearchArgs& a, const double* prep, unsigned* c
                                              from_spill);
 }
 
-template <int PS, int CODE>
-static void launch_gn_lane_code(const SearchArgs& a, const double* prep, unsigned* counter,
+template <int PS, int CODE, int MINB>
+static void launch_gn_lane_minb(const SearchArgs& a, const double* prep, unsigned* counter,
                                 double* spill, unsigned* spill_count, size_t n, int sms,
                                 cudaStream_t st) {
   static int per_sm = 0;
   if (!per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_patch_gn<PS, CODE>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_patch_gn<PS, CODE, MINB>, 256, 0);
     if (per_sm < 1) per_sm = 1;
   }
   size_t blocks = (size_t)per_sm * sms;
   const size_t need = (n + 255) / 256;
   if (blocks > need) blocks = need;
-  k_patch_gn<PS, CODE><<<(unsigned)blocks, 256, 0, st>>>(a, prep, counter, spill, spill_count);
+  k_patch_gn<PS, CODE, MINB>
+      <<<(unsigned)blocks, 256, 0, st>>>(a, prep, counter, spill, spill_count);
+}
+
+template <int PS, int CODE>
+static void launch_gn_lane_code(const SearchArgs& a, const double* prep, unsigned* counter,
+                                double* spill, unsigned* spill_count, size_t n, int sms,
+                                cudaStream_t st) {
+  if constexpr (PS == 12) {
+    if ((size_t)a.W * a.H > ((size_t)1 << 20)) {
+      launch_gn_lane_minb<PS, CODE, 2>(a, prep, counter, spill, spill_count, n, sms, st);
+      return;
+    }
+  }
+  launch_gn_lane_minb<PS, CODE, 1>(a, prep, counter, spill, spill_count, n, sms, st);
 }
 
 static int sm_count();
