@@ -103,6 +103,22 @@ def test_nonfinite_input_raises(torch, st):
         st.build_pyramid(img, 1)
 
 
+@pytest.mark.parametrize("h,w", [(17, 23), (16, 23), (17, 24), (9, 2047)])
+def test_nonfinite_input_found_at_every_position(torch, st, h, w):
+    # the level-1 pass reads the frames two output pixels at a time and checks
+    # the odd last column / row separately: a non-finite value anywhere raises
+    rng = np.random.default_rng(h * w)
+    spots = [(0, 0), (h - 1, w - 1), (h - 1, 0), (0, w - 1), (h // 2, w // 2)]
+    spots += [(int(rng.integers(h)), int(rng.integers(w))) for _ in range(3)]
+    for dtype in (np.float32, np.float64):
+        for y, x in spots:
+            img = rng.uniform(0, 255, (2, h, w)).astype(dtype)
+            img[1, y, x] = np.inf
+            with pytest.raises(ValueError):
+                st.build_pyramid(img, 1)
+        st.build_pyramid(rng.uniform(0, 255, (2, h, w)).astype(dtype), 1)  # finite: fine
+
+
 def test_upsample_bit_exact(torch, st):
     g = golden("samplers.npz")
     f = torch.tensor(g["flow"], device="cuda")
