@@ -63,20 +63,49 @@ __global__ void k_level1_from_frames(const T* __restrict__ frames, int B, int H,
 }
 
 // level s from level s-1 (both float64 row-major)
+// two output pixels per thread: each input row pair read as one 32-byte
+// load per row when aligned, the outputs as one 16-byte store
 __global__ void k_downsample(const double* __restrict__ in, int B, int H, int W,
                              double* __restrict__ out) {
-  int Ho = H / 2, Wo = W / 2;
-  size_t n = (size_t)B * Ho * Wo;
+  const int Ho = H / 2, Wo = W / 2;
+  const int Wp = (Wo + 1) / 2;  // output pairs per row
+  const size_t n = (size_t)B * Ho * Wp;
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (size_t)gridDim.x * blockDim.x) {
-    int X = (int)(i % Wo);
-    size_t t = i / Wo;
-    int Y = (int)(t % Ho);
-    int b = (int)(t / Ho);
+    const int Xp = (int)(i % Wp);
+    const size_t t = i / Wp;
+    const int Y = (int)(t % Ho);
+    const int b = (int)(t / Ho);
+    const int X = 2 * Xp;
     const double* r0 = in + ((size_t)b * H + 2 * Y) * W + 2 * X;
     const double* r1 = r0 + W;
-    double a = r0[0], bb = r0[1], c = r1[0], d = r1[1];
-    out[i] = ((a + bb) + (c + d)) / 4.0;
+    const size_t o = ((size_t)b * Ho + Y) * Wo + X;
+    if (X + 1 < Wo) {
+      double a[4], c[4];
+      if (((reinterpret_cast<uintptr_t>(r0) | reinterpret_cast<uintptr_t>(r1)) & 31) == 0) {
+        asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+            : "=d"(a[0]), "=d"(a[1]), "=d"(a[2]), "=d"(a[3]) : "l"(r0));
+        asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+            : "=d"(c[0]), "=d"(c[1]), "=d"(c[2]), "=d"(c[3]) : "l"(r1));
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          a[q] = r0[q];
+          c[q] = r1[q];
+        }
+      }
+      const double o0 = ((a[0] + a[1]) + (c[0] + c[1])) / 4.0;
+      const double o1 = ((a[2] + a[3]) + (c[2] + c[3])) / 4.0;
+      if ((o & 1) == 0) {
+        *reinterpret_cast<double2*>(out + o) = make_double2(o0, o1);
+      } else {
+        out[o] = o0;
+        out[o + 1] = o1;
+      }
+    } else {
+      const double a = r0[0], bb = r0[1], c = r1[0], d = r1[1];
+      out[o] = ((a + bb) + (c + d)) / 4.0;
+    }
   }
 }
 
@@ -361,12 +390,12 @@ static void launch_pyramid_t(const T* frames, int B, int H, int W, int coarsest,
   }
   for (int s = 1; s <= coarsest; ++s) {
     const int ho = h / 2, wo = w / 2;
-    const size_t n = (size_t)B * ho * wo;
     if (s == 1 && img[0] == nullptr) {
       dim3 g((unsigned)((wo + 63) / 64), (unsigned)((ho + 7) / 8), (unsigned)B);
       k_level1_checked<T><<<g, TH, 0, st>>>(frames, H, W, img[1], status);
     } else {
-      k_downsample<<<grid_for(n, TH), TH, 0, st>>>(img[s - 1], B, h, w, img[s]);
+      k_downsample<<<grid_for((size_t)B * ho * ((wo + 1) / 2), TH), TH, 0, st>>>(img[s - 1], B,
+                                                                                 h, w, img[s]);
     }
     note_launch();
     h = ho;
