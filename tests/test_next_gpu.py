@@ -83,6 +83,37 @@ def test_stereo_batch_vs_oracle_and_host_path(torch, orc):
     assert np.array_equal(eng.run_host(f1, f2), got)
 
 
+def test_stereo_graph_replays_and_pinned_host_dtypes(torch):
+    # the graph-replayed device path and the captured host path, stereo
+    # engines and every frame dtype, against the eager device result
+    from paper_1603_03590_b200 import FlowEngine, DisParams
+    from tools import synth
+
+    p = DisParams.preset(3, stereo=True, coarsest_scale=3)
+    pairs = [synth.make_stereo_pair(40 + i, 109, 256, 8.0) for i in range(2)]
+    f1 = np.stack([a for a, _, _ in pairs])
+    f2 = np.stack([b for _, b, _ in pairs])
+    eng = FlowEngine(2, 109, 256, p, stereo=True)
+    for dt in (np.float32, np.float64, np.uint8):
+        a = np.clip(f1, 0, 255).astype(dt)
+        b = np.clip(f2, 0, 255).astype(dt)
+        ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+        want = eng.run(ta, tb).cpu().numpy()
+        out = torch.empty((2, 109, 256, 2), dtype=torch.float64, device="cuda")
+        s = torch.cuda.Stream()
+        for _ in range(2):
+            eng.run(ta, tb, out=out, stream=s, graph=True)
+            torch.cuda.synchronize()
+            assert np.array_equal(out.cpu().numpy(), want), dt
+        pa = torch.from_numpy(a).pin_memory()
+        pb = torch.from_numpy(b).pin_memory()
+        po = torch.empty((2, 109, 256, 2), dtype=torch.float64).pin_memory()
+        for _ in range(3):  # eager, capture, replay
+            po.zero_()
+            eng.run_host(pa.numpy(), pb.numpy(), out=po.numpy())
+            assert np.array_equal(po.numpy(), want), dt
+
+
 def test_stereo_mode_params_rejected_by_dis_flow(torch):
     from paper_1603_03590_b200 import DisParams, dis_flow
 
