@@ -167,9 +167,13 @@ DIS_API size_t dis_host_workspace_bytes(int32_t B, int32_t H, int32_t W, int32_t
                                 const dis_params_t* p);
 
 /* Synchronous host-buffer variant (the e2e boundary): host frames in, host
- * flow out; copies are enqueued on `stream` around dis_flow_batch and the
- * call returns after the stream has drained, with the status word already
- * converted to a return code. Host buffers should be pinned for speed. */
+ * flow out; the batch runs as up to 16 chunks on internal streams (copies
+ * in, kernels, copies out overlapping across chunks), ordered after prior
+ * work on `stream`, and the call returns once they have drained, with the
+ * status word already converted to a return code.  Host buffers should be
+ * pinned: a call repeating the same pinned buffers, workspace, stream and
+ * problem is captured once (its second occurrence) and then replayed as one
+ * CUDA graph (same kernels and arguments, so the same results). */
 DIS_API int dis_flow_batch_host(const void* host_frame1, const void* host_frame2,
                         int32_t dtype, int32_t B, int32_t H, int32_t W,
                         const dis_params_t* p, double* host_flow_out,
