@@ -134,3 +134,29 @@ def test_no_cuda_means_loud_failure():
 
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         dis_flow(np.zeros((64, 64)), np.zeros((64, 64)))
+
+
+def test_grid_covers_every_pixel_for_random_layouts():
+    # test_densification.py:58-66 intent: every pixel of the level is covered
+    # by at least one patch window, for 200 random (dim, ps, overlap) layouts
+    from paper_1603_03590_b200 import stages
+
+    rng = np.random.default_rng(58)
+    for _ in range(200):
+        ps = int(rng.integers(2, 17))
+        dim = int(rng.integers(ps, 300))
+        ov = float(rng.uniform(0.0, 0.95))
+        xo = stages.grid_axis(dim, ps, ov)
+        covered = np.zeros(dim, dtype=bool)
+        for o in xo:
+            covered[o:o + ps] = True
+        assert covered.all(), (dim, ps, ov)
+        assert xo[0] == 0 and xo[-1] == dim - ps and np.all(np.diff(xo) > 0)
+
+
+def test_grid_dense_limit_is_one_patch_per_pixel():
+    # test_densification.py:45-48: the densest overlap gives spacing 1
+    from paper_1603_03590_b200 import stages
+
+    xo = stages.grid_axis(40, 8, 7.0 / 8.0)
+    assert np.array_equal(xo, np.arange(33))

@@ -320,3 +320,50 @@ def test_refine_rejects_non_finite_flow(torch, st):
     u0[0, 8, 8] = float("nan")
     with pytest.raises(RuntimeError):
         st.refine(u0, torch.zeros_like(u0), lv, lv, DisParams(variational=VarParams()), 1)
+
+
+def test_ramp_patch_is_invalid_and_checkerboard_valid(torch, st):
+    # test_inverse_search.py:36-55 intent, through the grid stage: a unit
+    # horizontal ramp gives a singular Hessian (invalid, keeps its init), a
+    # checkerboard a well-conditioned one (valid)
+    ys, xs = np.mgrid[0:24, 0:24].astype(np.float64)
+    ramp = st.build_pyramid(xs * 1.0, 0)[0]
+    out = st.patch_search(ramp, ramp["img"], DisParams(patch_size=8, overlap=0.0, iterations=4))
+    assert not out["valid"].any()
+    checker = 100.0 * (((xs // 2) + (ys // 2)) % 2) + 20.0
+    lv = st.build_pyramid(checker, 0)[0]
+    out = st.patch_search(lv, lv["img"], DisParams(patch_size=8, overlap=0.0, iterations=4))
+    assert out["valid"].all()
+
+
+def test_refine_barely_moves_the_exact_solution(torch, st):
+    # test_variational.py:74-81 intent: at the true translation the update
+    # stays small
+    w = _waves(16, lo=8.0, hi=24.0)
+    H, W = 40, 48
+    ref = st.build_pyramid(_render(w, W, H), 0)[0]
+    qry = st.build_pyramid(_render(w, W, H, (0.75, -0.5)), 0)[0]
+    u0 = np.full((1, H, W), 0.75)
+    v0 = np.full((1, H, W), -0.5)
+    u, v = st.refine(_cu(torch, u0), _cu(torch, v0), ref, qry,
+                     DisParams(variational=VarParams()), 1)
+    inner = (slice(None), slice(4, H - 4), slice(4, W - 4))
+    drift = np.hypot(u.cpu().numpy() - 0.75, v.cpu().numpy() + 0.5)[inner].mean()
+    assert drift < 0.05
+
+
+def test_more_outer_iterations_lower_the_error(torch, st):
+    # test_variational.py:120-131 intent
+    w = _waves(17, lo=8.0, hi=24.0)
+    H, W = 40, 48
+    ref = st.build_pyramid(_render(w, W, H), 0)[0]
+    qry = st.build_pyramid(_render(w, W, H, (1.0, 0.5)), 0)[0]
+    rng = np.random.default_rng(18)
+    u0 = _cu(torch, 1.0 + rng.normal(0, 0.4, (1, H, W)))
+    v0 = _cu(torch, 0.5 + rng.normal(0, 0.4, (1, H, W)))
+    inner = (slice(None), slice(4, H - 4), slice(4, W - 4))
+    errs = []
+    for outer in (1, 4):
+        u, v = st.refine(u0, v0, ref, qry, DisParams(variational=VarParams()), outer)
+        errs.append(np.hypot(u.cpu().numpy() - 1.0, v.cpu().numpy() - 0.5)[inner].mean())
+    assert errs[1] < errs[0]
