@@ -367,3 +367,55 @@ def test_more_outer_iterations_lower_the_error(torch, st):
         u, v = st.refine(u0, v0, ref, qry, DisParams(variational=VarParams()), outer)
         errs.append(np.hypot(u.cpu().numpy() - 1.0, v.cpu().numpy() - 0.5)[inner].mean())
     assert errs[1] < errs[0]
+
+
+def _ssd_meannorm(ref, qry, x0, y0, ps, u, v):
+    """mean-normalised SSD of the ps x ps window at (x0, y0) against the query
+    sampled at +(u, v) (clamped bilinear, an independent restatement)."""
+    h, w = qry.shape
+    ys, xs = np.mgrid[0:ps, 0:ps].astype(np.float64)
+    x = np.clip(x0 + xs + u, 0.0, w - 1.0)
+    y = np.clip(y0 + ys + v, 0.0, h - 1.0)
+    xi = np.floor(x).astype(int)
+    yi = np.floor(y).astype(int)
+    x1 = np.minimum(xi + 1, w - 1)
+    y1 = np.minimum(yi + 1, h - 1)
+    fx, fy = x - xi, y - yi
+    a = qry[yi, xi] + fx * (qry[yi, x1] - qry[yi, xi])
+    b = qry[y1, xi] + fx * (qry[y1, x1] - qry[y1, xi])
+    warped = a + fy * (b - a)
+    t = ref[y0:y0 + ps, x0:x0 + ps]
+    d = (warped - warped.mean()) - (t - t.mean())
+    return float((d * d).sum())
+
+
+def test_first_gauss_newton_step_reduces_the_ssd(torch, st):
+    # test_inverse_search.py:106-125 intent: one iteration from zero lowers the
+    # (mean-normalised) SSD for >= 99 % of valid patches under small shifts
+    rng = np.random.default_rng(7)
+    n = 300
+    refs, qrys = [], []
+    for _ in range(n):
+        w = _waves(int(rng.integers(1 << 30)), n=6, lo=16.0, hi=48.0)
+        a = rng.uniform(0, 2 * np.pi)
+        r = rng.uniform(0.25, 1.0)
+        refs.append(_render(w, 24, 24))
+        qrys.append(_render(w, 24, 24, (r * np.cos(a), r * np.sin(a))))
+    ref_b, qry_b = np.stack(refs), np.stack(qrys)
+    lr = st.build_pyramid(ref_b, 0)[0]
+    lq = st.build_pyramid(qry_b, 0)[0]
+    out = st.patch_search(lr, lq["img"], DisParams(patch_size=8, overlap=0.5, iterations=1))
+    i = 2 * 5 + 2  # the patch at origin (8, 8) of a 5 x 5 grid
+    u = out["u"][:, i].cpu().numpy()
+    v = out["v"][:, i].cpu().numpy()
+    valid = out["valid"][:, i].cpu().numpy().astype(bool)
+    reduced = checked = 0
+    for k in range(n):
+        if not valid[k]:
+            continue
+        checked += 1
+        if _ssd_meannorm(ref_b[k], qry_b[k], 8, 8, 8, u[k], v[k]) < \
+                _ssd_meannorm(ref_b[k], qry_b[k], 8, 8, 8, 0.0, 0.0):
+            reduced += 1
+    assert checked >= 0.8 * n
+    assert reduced >= 0.99 * checked
