@@ -1,5 +1,5 @@
 """Per-source-line instruction/stall view of an `ncu --page source --print-source
-cuda,sass` CSV (tools/_exp_prof.sh): python tools/src_top.py file.csv [n] [warp_steps]"""
+cuda,sass` CSV (tools/gpu_round.sh): python tools/src_top.py file.csv [n] [warp_steps]"""
 import csv
 import sys
 
