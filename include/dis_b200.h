@@ -316,6 +316,12 @@ DIS_API void dis_profile_enable(int32_t on);
 DIS_API void dis_profile_reset(void);
 /* Blocks on the recorded events; writes total ms and launch counts. */
 DIS_API int dis_profile_read(double* ms_out, int64_t* count_out, int32_t n_classes);
+/* Every timed launch since dis_profile_reset, in enqueue order: its class,
+ * its pyramid level (-1 outside the coarse-to-fine loop) and its ms (up to
+ * `max` entries).  Blocks like dis_profile_read; returns the entry count or
+ * a negative status. */
+DIS_API int32_t dis_profile_log(int32_t* cls_out, int32_t* level_out, double* ms_out,
+                                int32_t max);
 
 /* Evaluation census (bench roofline): while on, the patch-search kernels
  * count window evaluations and finished patches on the device; read with

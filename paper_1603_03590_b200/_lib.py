@@ -37,7 +37,7 @@ EXPORTED = (
     "dis_census_read", "dis_selftest_fp64_peak", "dis_compose_flows", "dis_stereo_batch",
     "dis_stereo_batch_host", "dis_densify_bidirectional",
     "dis_densify_bidirectional_workspace_bytes", "dis_sparse_workspace_bytes",
-    "dis_sparse_correspondences", "dis_flow_batch_levels",
+    "dis_sparse_correspondences", "dis_flow_batch_levels", "dis_profile_log",
 )
 
 KERNEL_CLASSES = ("pyramid", "patch_search", "densify", "tensor_assemble", "sor", "upsample")
@@ -125,6 +125,9 @@ def lib() -> ctypes.CDLL:
     L.dis_profile_read.argtypes = [ctypes.POINTER(ctypes.c_double),
                                    ctypes.POINTER(ctypes.c_int64), _i32]
     L.dis_profile_read.restype = ctypes.c_int
+    L.dis_profile_log.argtypes = [ctypes.POINTER(_i32), ctypes.POINTER(_i32),
+                                  ctypes.POINTER(ctypes.c_double), _i32]
+    L.dis_profile_log.restype = _i32
     L.dis_selftest_div.argtypes = [_vp, _vp, _vp, _vp, _sz, _vp]
     L.dis_selftest_div.restype = ctypes.c_int
     L.dis_census_enable.argtypes = [_i32]

@@ -32,9 +32,15 @@ std::mutex g_prof_mu;
 bool g_prof_on = false;
 struct EvPair {
   cudaEvent_t a, b;
-  int cls;
+  int cls, level;
+};
+struct LogEntry {
+  int cls, level;
+  double ms;
 };
 std::vector<EvPair> g_prof_pending;
+std::vector<LogEntry> g_prof_log;  // every resolved launch since the last reset, in order
+int g_prof_level = -1;              // pyramid level of the launches being enqueued
 std::vector<cudaEvent_t> g_prof_free;
 cudaEvent_t g_prof_open[KC_COUNT];
 double g_prof_ms[KC_COUNT];
@@ -55,6 +61,24 @@ cudaEvent_t prof_event() {
 namespace disb200 {
 void note_launch(int n) { g_launches += n; }
 
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < 0 ? 0 : d % kMaxDevices;
+}
+
+int device_sm_count() {
+  static std::atomic<int> sms[kMaxDevices];
+  const int d = current_device();
+  int n = sms[d].load(std::memory_order_relaxed);
+  if (n <= 0) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    if (n <= 0) n = 148;
+    sms[d].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
+
 // evaluation census: while enabled, the Gauss-Newton kernels add each
 // finished patch's window-evaluation count to census[0] and 1 to census[1]
 // (bench.py's FP64 roofline of the patch search; not used when timing)
@@ -68,12 +92,16 @@ void prof_begin(int cls, cudaStream_t st) {
   cudaEventRecord(e, st);
   g_prof_open[cls] = e;
 }
+void prof_level(int level) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof_level = level;
+}
 void prof_end(int cls, cudaStream_t st) {
   std::lock_guard<std::mutex> g(g_prof_mu);
   if (!g_prof_on || !g_prof_open[cls]) return;
   cudaEvent_t e = prof_event();
   cudaEventRecord(e, st);
-  g_prof_pending.push_back({g_prof_open[cls], e, cls});
+  g_prof_pending.push_back({g_prof_open[cls], e, cls, g_prof_level});
   g_prof_open[cls] = nullptr;
 }
 }  // namespace disb200
@@ -319,6 +347,7 @@ int run_pipeline(const Plan& pl, const dis_params_t* p, double* out, void* ws, c
   double* bprev_v = nullptr;
   int prev_w = 0, prev_h = 0;
   for (int s = pl.ss; s >= pl.sf; --s) {
+    prof_level(s);
     const int h = pl.hs[s], w = pl.ws[s];
     double* ref = at<double>(ws, pl.off_img[0][s]);
     double* qry = at<double>(ws, pl.off_img[1][s]);
@@ -363,6 +392,7 @@ int run_pipeline(const Plan& pl, const dis_params_t* p, double* out, void* ws, c
     prev_w = w;
     prev_h = h;
   }
+  prof_level(-1);
   if (!upscale) return check_cuda("dense_scales");  // the finest scale's field stays in ws
   // _upscale_to_full (pipeline.py:129-133)
   if (pl.sf == 0) {
@@ -429,6 +459,7 @@ void dis_profile_reset(void) {
     g_prof_free.push_back(p.b);
   }
   g_prof_pending.clear();
+  g_prof_log.clear();
   for (int c = 0; c < KC_COUNT; ++c) {
     g_prof_ms[c] = 0.0;
     g_prof_n[c] = 0;
@@ -465,6 +496,7 @@ int dis_profile_read(double* ms_out, int64_t* count_out, int32_t n_classes) {
     cudaEventElapsedTime(&ms, p.a, p.b);
     g_prof_ms[p.cls] += ms;
     g_prof_n[p.cls] += 1;
+    g_prof_log.push_back({p.cls, p.level, (double)ms});
     g_prof_free.push_back(p.a);
     g_prof_free.push_back(p.b);
   }
@@ -475,6 +507,21 @@ int dis_profile_read(double* ms_out, int64_t* count_out, int32_t n_classes) {
   }
   return DIS_OK;
 }
+int32_t dis_profile_log(int32_t* cls_out, int32_t* level_out, double* ms_out, int32_t max) {
+  double ms[KC_COUNT];
+  int64_t n[KC_COUNT];
+  int rc = dis_profile_read(ms, n, KC_COUNT);  // resolves the pending events
+  if (rc) return rc;
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  const int32_t cnt = (int32_t)g_prof_log.size();
+  for (int32_t i = 0; i < cnt && i < max; ++i) {
+    if (cls_out) cls_out[i] = g_prof_log[i].cls;
+    if (level_out) level_out[i] = g_prof_log[i].level;
+    if (ms_out) ms_out[i] = g_prof_log[i].ms;
+  }
+  return cnt;
+}
+
 int32_t dis_abi_version(void) { return DIS_B200_ABI_VERSION; }
 
 void dis_params_default(dis_params_t* p) {

@@ -23,9 +23,16 @@ enum KernelClass {
 };
 void prof_begin(int cls, cudaStream_t st);
 void prof_end(int cls, cudaStream_t st);
+void prof_level(int level);  // tags the following launches with their pyramid level
 void note_launch(int n = 1);
 // evaluation census (bench roofline): device counters or null when off
 unsigned long long* census_counters();
+// the current CUDA device and its SM count; per-device launch settings
+// (kernel attributes, occupancy-derived grid caps) are cached per device
+// index, so one process may drive several GPUs
+constexpr int kMaxDevices = 64;
+int current_device();
+int device_sm_count();
 
 // pyramid.cu
 void launch_pyramid(const void* frames, int dtype, int B, int H, int W, int coarsest,

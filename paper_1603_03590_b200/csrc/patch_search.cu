@@ -922,15 +922,13 @@ template <int PS, int G, int CODE>
 static void launch_gn_group_code(const SearchArgs& a, const double* prep, unsigned* counter,
                                  size_t n, cudaStream_t st, const double* spill,
                                  const unsigned* spill_count, bool from_spill) {
-  static int cap = 0;
+  static int caps[kMaxDevices];
+  int& cap = caps[current_device()];
   if (!cap) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_patch_gn_group<PS, G, CODE>, 128,
                                                   0);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cap = (per_sm > 0 ? per_sm : 1) * sms;
+    cap = (per_sm > 0 ? per_sm : 1) * device_sm_count();
   }
   const size_t need = (n * G + 127) / 128;
   int blocks = (int)(need < (size_t)cap ? need : (size_t)cap);
@@ -958,7 +956,8 @@ template <int PS, int CODE, int MINB>
 static void launch_gn_lane_minb(const SearchArgs& a, const double* prep, unsigned* counter,
                                 double* spill, unsigned* spill_count, size_t n, int sms,
                                 cudaStream_t st) {
-  static int per_sm = 0;
+  static int per_sms[kMaxDevices];
+  int& per_sm = per_sms[current_device()];
   if (!per_sm) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_patch_gn<PS, CODE, MINB>, 256, 0);
     if (per_sm < 1) per_sm = 1;
@@ -983,29 +982,16 @@ static void launch_gn_lane_code(const SearchArgs& a, const double* prep, unsigne
   launch_gn_lane_minb<PS, CODE, 1>(a, prep, counter, spill, spill_count, n, sms, st);
 }
 
-static int sm_count();
-
 template <int PS>
 static void launch_gn_lane(const SearchArgs& a, const double* prep, unsigned* counter,
                            double* spill, unsigned* spill_count, size_t n, cudaStream_t st) {
-  const int sms = sm_count();
+  const int sms = device_sm_count();
   if (a.code == DIS_NORM_L1)
     launch_gn_lane_code<PS, DIS_NORM_L1>(a, prep, counter, spill, spill_count, n, sms, st);
   else if (a.code == DIS_NORM_HUBER)
     launch_gn_lane_code<PS, DIS_NORM_HUBER>(a, prep, counter, spill, spill_count, n, sms, st);
   else
     launch_gn_lane_code<PS, DIS_NORM_L2>(a, prep, counter, spill, spill_count, n, sms, st);
-}
-
-static int sm_count() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  return sms;
 }
 
 constexpr size_t kGroupLanes = (size_t)148 * 2048 * 4;  // group kernel up to ~4 waves

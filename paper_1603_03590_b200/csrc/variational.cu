@@ -793,12 +793,7 @@ static int choose_cluster(int B, int H) {
   auto hp = [&](int C) { return ((H + C - 1) / C + 31) / 32 * 32; };
   int C = 1;
   while (C < 16 && (hp(C) > kMaxBandRows || sor_rows_smem_bytes<S>(hp(C)) > kMaxSmem)) ++C;
-  static const int sms = [] {
-    int dev = 0, n = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n > 0 ? n : 148;
-  }();
+  const int sms = device_sm_count();
   // while the batch leaves SMs idle, split the rows further (bands of >= 32
   // rows; the st.async halo exchange costs ~0.15 us per step)
   while (C < 16 && B * (C + 1) <= sms && (H + C) / (C + 1) >= 32) ++C;
@@ -832,11 +827,13 @@ static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const
     kfn = k_sor<S, HZ, 1>;
   else if (P == 2)
     kfn = k_sor<S, HZ, (S >= 2 ? 2 : 1)>;
-  static bool attr = false;
-  if (!attr) {
+  // function attributes are per device: set them once on each device used
+  static bool attr[kMaxDevices];
+  const int dev = current_device();
+  if (!attr[dev]) {
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
     cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr = true;
+    attr[dev] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(a.B * C));

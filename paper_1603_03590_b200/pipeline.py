@@ -65,6 +65,26 @@ def _to_device_frames(x, device):
     return t.to(device=device, non_blocking=True).contiguous()
 
 
+def _promote_pair(f1, f2):
+    """as_image converts BOTH frames to float64 (core.py:65-72): a pair of
+    different dtypes is promoted to float64 together (exact for u8/f32), never
+    narrowed to the first frame's dtype."""
+    if f1.dtype == f2.dtype:
+        return f1, f2
+    torch = _torch()
+    return f1.to(torch.float64), f2.to(torch.float64)
+
+
+def _promote_pair_np(a, b):
+    if a.dtype not in (np.float32, np.float64, np.uint8):
+        a = a.astype(np.float64)
+    if b.dtype not in (np.float32, np.float64, np.uint8):
+        b = b.astype(np.float64)
+    if a.dtype != b.dtype:
+        a, b = a.astype(np.float64), b.astype(np.float64)
+    return np.ascontiguousarray(a), np.ascontiguousarray(b)
+
+
 class FlowEngine:
     """A reusable device workspace for batches of ``B`` pairs of ``H x W``
     frames at one parameter set (the workspace layout is fixed by
@@ -81,7 +101,11 @@ class FlowEngine:
         if self.params.mode == "stereo" and not self.stereo:
             raise ValueError("use dis_stereo for stereo-mode parameters")
         self.B, self.H, self.W = int(batch), int(height), int(width)
-        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        if dev.type != "cuda":
+            raise ValueError(f"FlowEngine needs a CUDA device, got {dev}")
+        self.device = torch.device("cuda", dev.index if dev.index is not None
+                                   else torch.cuda.current_device())
         self.cparams = to_c(self.params)
         L = _lib.lib()
         _lib.check(L.dis_params_validate(ctypes.byref(self.cparams)))
@@ -111,35 +135,56 @@ class FlowEngine:
         if graph:
             return self._run_graph(frames1, frames2, out, stream, check)
         torch = _torch()
-        f1 = _to_device_frames(frames1, self.device)
-        f2 = _to_device_frames(frames2, self.device)
-        if f1.dim() == 2:
-            f1 = f1.unsqueeze(0)
-            f2 = f2.unsqueeze(0)
-        if tuple(f1.shape) != (self.B, self.H, self.W) or tuple(f2.shape) != tuple(f1.shape):
-            raise ValueError(
-                f"frame batch {tuple(f1.shape)} / {tuple(f2.shape)} does not match the engine "
-                f"({self.B}, {self.H}, {self.W})")
-        if f2.dtype != f1.dtype:
-            f2 = f2.to(f1.dtype)
-        if out is None:
-            out = torch.empty((self.B, self.H, self.W, 2), dtype=torch.float64,
-                              device=self.device)
-        L = _lib.lib()
-        fn = L.dis_stereo_batch if self.stereo else L.dis_flow_batch
-        rc = fn(
-            f1.data_ptr(), f2.data_ptr(), _dtype_code(f1), self.B, self.H, self.W,
-            ctypes.byref(self.cparams), out.data_ptr(), self.workspace.data_ptr(),
-            self.workspace_bytes, _lib.stream_handle(stream))
-        _lib.check(rc)
-        if check:
-            self.check_status(stream)
+        with torch.cuda.device(self.device):
+            if stream is None:
+                stream = torch.cuda.current_stream(self.device)
+            f1 = _to_device_frames(frames1, self.device)
+            f2 = _to_device_frames(frames2, self.device)
+            if f1.dim() == 2:
+                f1 = f1.unsqueeze(0)
+            if f2.dim() == 2:
+                f2 = f2.unsqueeze(0)
+            if tuple(f1.shape) != (self.B, self.H, self.W) or tuple(f2.shape) != tuple(f1.shape):
+                raise ValueError(
+                    f"frame batch {tuple(f1.shape)} / {tuple(f2.shape)} does not match the "
+                    f"engine ({self.B}, {self.H}, {self.W})")
+            f1, f2 = _promote_pair(f1, f2)
+            if out is None:
+                out = torch.empty((self.B, self.H, self.W, 2), dtype=torch.float64,
+                                  device=self.device)
+            else:
+                self._check_out_tensor(out)
+            L = _lib.lib()
+            fn = L.dis_stereo_batch if self.stereo else L.dis_flow_batch
+            rc = fn(
+                f1.data_ptr(), f2.data_ptr(), _dtype_code(f1), self.B, self.H, self.W,
+                ctypes.byref(self.cparams), out.data_ptr(), self.workspace.data_ptr(),
+                self.workspace_bytes, _lib.stream_handle(stream))
+            _lib.check(rc)
+            if check:
+                self.check_status(stream)
         return out
+
+    def _check_out_tensor(self, out):
+        torch = _torch()
+        want = (self.B, self.H, self.W, 2)
+        if not isinstance(out, torch.Tensor):
+            raise ValueError("out must be a CUDA tensor (use run_host for numpy buffers)")
+        if (tuple(out.shape) != want or out.dtype != torch.float64 or not out.is_contiguous()
+                or out.device != self._dev_index()):
+            raise ValueError(
+                f"out must be a contiguous float64 tensor of shape {want} on {self.device}, "
+                f"got {tuple(out.shape)} {out.dtype} on {out.device}"
+                f"{'' if out.is_contiguous() else ' (non-contiguous)'}")
+
+    def _dev_index(self):
+        return self.device
 
     def _run_graph(self, frames1, frames2, out, stream, check):
         torch = _torch()
         if out is None:
             raise ValueError("graph replay needs a persistent output tensor (out=...)")
+        self._check_out_tensor(out)
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
         key = (frames1.data_ptr(), frames2.data_ptr(), out.data_ptr(), frames1.dtype,
@@ -150,17 +195,21 @@ class FlowEngine:
             with torch.cuda.graph(g, stream=stream):
                 self.run(frames1, frames2, out=out, stream=stream, check=False)
             self._graph, self._graph_key = g, key
-        with torch.cuda.stream(stream):
+        with torch.cuda.device(self.device), torch.cuda.stream(stream):
             self._graph.replay()
         if check:
             self.check_status(stream)
         return out
 
     def check_status(self, stream=None) -> None:
+        torch = _torch()
         status = ctypes.c_uint32(0)
         L = _lib.lib()
-        _lib.check(L.dis_read_status(self.workspace.data_ptr(), ctypes.byref(status),
-                                     _lib.stream_handle(stream)))
+        with torch.cuda.device(self.device):
+            if stream is None:
+                stream = torch.cuda.current_stream(self.device)
+            _lib.check(L.dis_read_status(self.workspace.data_ptr(), ctypes.byref(status),
+                                         _lib.stream_handle(stream)))
         _lib.check(L.dis_status_to_error(status.value))
 
     # -- host-buffer path (the e2e boundary) ---------------------------------
@@ -169,23 +218,34 @@ class FlowEngine:
         """dis_flow_batch_host: host frames in, host flow out (copies
         included).  Pinned host buffers (torch ``pin_memory``) are fastest."""
         torch = _torch()
-        a = np.ascontiguousarray(frames1)
-        b = np.ascontiguousarray(frames2)
-        if a.dtype not in (np.float32, np.float64, np.uint8):
-            a = a.astype(np.float64)
-            b = b.astype(np.float64)
-        b = b.astype(a.dtype, copy=False)
-        code = {np.dtype(np.float32): 0, np.dtype(np.float64): 1, np.dtype(np.uint8): 2}[a.dtype]
-        L = _lib.lib()
-        n = L.dis_host_workspace_bytes(self.B, self.H, self.W, code, ctypes.byref(self.cparams))
-        if self._host_ws is None or self._host_ws.numel() < n:
-            self._host_ws = torch.empty(int(n), dtype=torch.uint8, device=self.device)
+        a, b = _promote_pair_np(np.asarray(frames1), np.asarray(frames2))
+        if a.ndim == 2:
+            a = a[None]
+        if b.ndim == 2:
+            b = b[None]
+        want = (self.B, self.H, self.W)
+        if tuple(a.shape) != want or tuple(b.shape) != want:
+            raise ValueError(f"frame batch {tuple(a.shape)} / {tuple(b.shape)} does not match "
+                             f"the engine {want}")
         if out is None:
             out = np.empty((self.B, self.H, self.W, 2), dtype=np.float64)
-        fn = L.dis_stereo_batch_host if self.stereo else L.dis_flow_batch_host
-        rc = fn(a.ctypes.data, b.ctypes.data, code, self.B, self.H, self.W,
-                ctypes.byref(self.cparams), out.ctypes.data, self._host_ws.data_ptr(), int(n),
-                _lib.stream_handle(stream))
+        elif (not isinstance(out, np.ndarray) or out.shape != want + (2,)
+              or out.dtype != np.float64 or not out.flags.c_contiguous or not out.flags.writeable):
+            raise ValueError(f"out must be a writeable C-contiguous float64 array of shape "
+                             f"{want + (2,)}")
+        code = {np.dtype(np.float32): 0, np.dtype(np.float64): 1, np.dtype(np.uint8): 2}[a.dtype]
+        L = _lib.lib()
+        with torch.cuda.device(self.device):
+            if stream is None:
+                stream = torch.cuda.current_stream(self.device)
+            n = L.dis_host_workspace_bytes(self.B, self.H, self.W, code,
+                                           ctypes.byref(self.cparams))
+            if self._host_ws is None or self._host_ws.numel() < n:
+                self._host_ws = torch.empty(int(n), dtype=torch.uint8, device=self.device)
+            fn = L.dis_stereo_batch_host if self.stereo else L.dis_flow_batch_host
+            rc = fn(a.ctypes.data, b.ctypes.data, code, self.B, self.H, self.W,
+                    ctypes.byref(self.cparams), out.ctypes.data, self._host_ws.data_ptr(),
+                    int(n), _lib.stream_handle(stream))
         _lib.check(rc)
         return out
 
@@ -193,15 +253,27 @@ class FlowEngine:
 _ENGINES: dict = {}
 
 
-def _engine(B, H, W, params, stereo=False):
-    key = (B, H, W, params, stereo)
+def _engine(B, H, W, params, stereo=False, device=None):
+    """Cached engine per (problem, parameters, device): the workspace lives on
+    one device, so the current device is part of the key."""
+    torch = _torch()
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    key = (B, H, W, params, stereo, str(device))
     eng = _ENGINES.get(key)
     if eng is None:
         if len(_ENGINES) > 8:
             _ENGINES.clear()
-        eng = FlowEngine(B, H, W, params, stereo=stereo)
+        eng = FlowEngine(B, H, W, params, device=device, stereo=stereo)
         _ENGINES[key] = eng
     return eng
+
+
+def _device_of(x):
+    torch = _torch()
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        return x.device
+    return None
 
 
 def _check_frame(a):
@@ -224,7 +296,7 @@ def dis_flow_batch(frames1, frames2, params: DisParams | None = None):
         raise ValueError(f"frame batch must be (B, H, W), got {s1}")
     if s1 != s2:
         raise ValueError(f"frame dimensions differ: {s1[:0:-1]} vs {s2[:0:-1]}")
-    eng = _engine(s1[0], s1[1], s1[2], params)
+    eng = _engine(s1[0], s1[1], s1[2], params, device=_device_of(frames1))
     return eng.run(frames1, frames2)
 
 
@@ -244,7 +316,7 @@ def dis_flow(frame1, frame2, params: DisParams | None = None, threads: int = 1):
     if params.coarsest_scale < 0:
         raise ParameterError("coarsest_scale must be >= 0")
     h, w = frame1.shape
-    eng = _engine(1, int(h), int(w), params)
+    eng = _engine(1, int(h), int(w), params, device=_device_of(frame1))
     out = eng.run(frame1, frame2)[0]
     if isinstance(frame1, torch.Tensor):
         return out
@@ -266,7 +338,8 @@ def dis_stereo(left, right, params: DisParams | None = None, threads: int = 1):
             f"frame dimensions differ: {tuple(left.shape)[::-1]} vs "
             f"{tuple(right.shape)[::-1]}")
     h, w = left.shape
-    out = _engine(1, int(h), int(w), params, stereo=True).run(left, right)[0]
+    out = _engine(1, int(h), int(w), params, stereo=True,
+                  device=_device_of(left)).run(left, right)[0]
     if isinstance(left, torch.Tensor):
         return out
     return out.cpu().numpy()
@@ -282,7 +355,8 @@ def dis_stereo_batch(left, right, params: DisParams | None = None):
         raise ValueError(f"frame batch must be (B, H, W), got {s1}")
     if s1 != s2:
         raise ValueError(f"frame dimensions differ: {s1[:0:-1]} vs {s2[:0:-1]}")
-    return _engine(s1[0], s1[1], s1[2], params, stereo=True).run(left, right)
+    return _engine(s1[0], s1[1], s1[2], params, stereo=True,
+                   device=_device_of(left)).run(left, right)
 
 
 class SparseMatch(NamedTuple):
@@ -314,11 +388,10 @@ def sparse_correspondences(frame1, frame2, seeds, params: DisParams | None = Non
         raise ValueError(f"seeds must be (n, 2) x, y pairs, got shape {seed_arr.shape}")
     n = seed_arr.shape[0]
     h, w = (int(d) for d in frame1.shape)
-    dev = torch.device("cuda")
+    dev = _device_of(frame1) or torch.device("cuda", torch.cuda.current_device())
     f1 = _to_device_frames(frame1, dev)
     f2 = _to_device_frames(frame2, dev)
-    if f2.dtype != f1.dtype:
-        f2 = f2.to(f1.dtype)
+    f1, f2 = _promote_pair(f1, f2)
     cp = to_c(params)
     L = _lib.lib()
     nbytes = int(L.dis_sparse_workspace_bytes(h, w, n, ctypes.byref(cp)))
@@ -330,10 +403,11 @@ def sparse_correspondences(frame1, frame2, seeds, params: DisParams | None = Non
     ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     disp = np.zeros((n, 2), dtype=np.float64)
     valid = np.zeros(n, dtype=np.uint8)
-    _lib.check(L.dis_sparse_correspondences(
-        f1.data_ptr(), f2.data_ptr(), _dtype_code(f1), h, w, ctypes.byref(cp),
-        seed_arr.ctypes.data, n, disp.ctypes.data, valid.ctypes.data, ws.data_ptr(), nbytes,
-        _lib.stream_handle(torch.cuda.current_stream(dev))))
+    with torch.cuda.device(dev):
+        _lib.check(L.dis_sparse_correspondences(
+            f1.data_ptr(), f2.data_ptr(), _dtype_code(f1), h, w, ctypes.byref(cp),
+            seed_arr.ctypes.data, n, disp.ctypes.data, valid.ctypes.data, ws.data_ptr(), nbytes,
+            _lib.stream_handle(torch.cuda.current_stream(dev))))
     return [SparseMatch((float(seed_arr[i, 0]), float(seed_arr[i, 1])),
                         (float(disp[i, 0]), float(disp[i, 1])), bool(valid[i]))
             for i in range(n)]
@@ -364,9 +438,10 @@ def compose_flows(flow_ab, flow_bc):
     B, H, W = ab.shape[:3]
     out = torch.empty_like(ab)
     if B * H * W:
-        _lib.check(_lib.lib().dis_compose_flows(
-            ab.data_ptr(), bc.data_ptr(), B, H, W, out.data_ptr(),
-            _lib.stream_handle(torch.cuda.current_stream(dev))))
+        with torch.cuda.device(dev):
+            _lib.check(_lib.lib().dis_compose_flows(
+                ab.data_ptr(), bc.data_ptr(), B, H, W, out.data_ptr(),
+                _lib.stream_handle(torch.cuda.current_stream(dev))))
     if not batched:
         out = out[0]
     return out if as_torch else out.cpu().numpy()

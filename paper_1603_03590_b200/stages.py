@@ -18,6 +18,14 @@ from .params import DisParams, to_c
 from .pipeline import _dtype_code, _require_cuda, _to_device_frames
 
 
+def _cur(t) -> int:
+    """cudaStream_t of torch's current stream on tensor ``t``'s device (the
+    stage launches are ordered after the work that produced their inputs)."""
+    import torch
+
+    return _lib.stream_handle(torch.cuda.current_stream(t.device))
+
+
 def grid_axis(dim: int, patch_size: int, overlap: float) -> np.ndarray:
     """_axis_origins of create_grid (densification.py:50-79)."""
     L = _lib.lib()
@@ -54,7 +62,7 @@ def build_pyramid(frames, coarsest: int, finest: int = 0, second_derivatives: bo
     dd = arr(*[lv["dd"].data_ptr() if "dd" in lv else None for lv in levels])
     status = torch.zeros(1, dtype=torch.int32, device=f.device)
     _lib.check(_lib.lib().dis_build_pyramid(f.data_ptr(), _dtype_code(f), B, H, W, coarsest,
-                                            img, gx, gy, dd, status.data_ptr(), None))
+                                            img, gx, gy, dd, status.data_ptr(), _cur(f)))
     if int(status.item()) != 0:
         raise ValueError("image contains non-finite values")
     return levels
@@ -83,7 +91,7 @@ def patch_search(ref: dict, qry_img, params: DisParams, coarse_u=None, coarse_v=
         B, W, H, _lib.ptr(coarse_u), _lib.ptr(coarse_v), Wc, Hc, ctypes.byref(cp),
         out["u"].data_ptr(), out["v"].data_ptr(), out["off"].data_ptr(), out["mar"].data_ptr(),
         out["init_u"].data_ptr(), out["init_v"].data_ptr(), out["valid"].data_ptr(),
-        ws.data_ptr(), nbytes, None)
+        ws.data_ptr(), nbytes, _cur(ref["img"]))
     _lib.check(rc)
     out["x_origins"] = xo
     out["y_origins"] = yo
@@ -101,7 +109,7 @@ def densify(ref_img, qry_img, params: DisParams, pu, pv, poff):
     _lib.check(_lib.lib().dis_densify(ref_img.data_ptr(), qry_img.data_ptr(), B, W, H,
                                       ctypes.byref(cp), pu.data_ptr(), pv.data_ptr(),
                                       poff.data_ptr(), fu.data_ptr(), fv.data_ptr(),
-                                      status.data_ptr(), None))
+                                      status.data_ptr(), _cur(ref_img)))
     if int(status.item()) != 0:
         raise AssertionError("pixel without a contributing patch; grid coverage broken")
     return fu, fv
@@ -123,7 +131,7 @@ def refine(fu, fv, ref: dict, qry: dict, params: DisParams, outer: int):
                             ref["dd"].data_ptr(), qry["img"].data_ptr(), qry["gx"].data_ptr(),
                             qry["gy"].data_ptr(), qry["dd"].data_ptr(), B, W, H,
                             ctypes.byref(cp), int(outer), u.data_ptr(), v.data_ptr(),
-                            ws.data_ptr(), int(nbytes), status.data_ptr(), None))
+                            ws.data_ptr(), int(nbytes), status.data_ptr(), _cur(fu)))
     if int(status.item()) != 0:
         raise RuntimeError("variational refinement produced a non-finite value")
     return u, v
@@ -137,7 +145,7 @@ def upsample_flow(fu, fv, new_width: int, new_height: int):
     ov = torch.empty_like(ou)
     _lib.check(_lib.lib().dis_upsample_flow(fu.data_ptr(), fv.data_ptr(), B, W, H,
                                             ou.data_ptr(), ov.data_ptr(), new_width,
-                                            new_height, None))
+                                            new_height, _cur(fu)))
     return ou, ov
 
 
@@ -160,7 +168,7 @@ def densify_bidirectional(ref_img, qry_img, params: DisParams, fu_p, fv_p, foff,
     _lib.check(L.dis_densify_bidirectional(
         ref_img.data_ptr(), qry_img.data_ptr(), B, W, H, ctypes.byref(cp),
         *[t.data_ptr() for t in args], fu.data_ptr(), fv.data_ptr(), ws.data_ptr(), nbytes,
-        status.data_ptr(), None))
+        status.data_ptr(), _cur(ref_img)))
     if int(status.item()) != 0:
         raise AssertionError("pixel without a contributing patch; grid coverage broken")
     return fu, fv

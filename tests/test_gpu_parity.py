@@ -2,6 +2,7 @@
 reference's operation order; the tolerance for every comparison here is
 zero: np.array_equal).  All calls go through the C ABI (libdis_b200.so)."""
 
+import dataclasses
 import hashlib
 
 import numpy as np
@@ -337,3 +338,72 @@ def test_error_types(torch):
     bad[3, 3] = np.inf
     with pytest.raises(ValueError):
         dis_flow(bad, a, DisParams(coarsest_scale=2, finest_scale=1))
+
+
+def test_mixed_dtype_pair_promotes_to_float64(torch, orc):
+    """as_image converts both frames to float64 (core.py:65-72): a uint8
+    frame1 with a float64 frame2 (fractional values) gives the oracle's flow
+    on the float64 pair — frame2 is never narrowed to frame1's dtype."""
+    from paper_1603_03590_b200 import FlowEngine, dis_flow
+
+    cfg = synth.CONFIGS["c0"]
+    f1, f2 = synth.make_batch(cfg, seed=21, count=1, h=109, w=256)
+    a = np.clip(np.rint(f1[0]), 0, 255).astype(np.uint8)
+    b = f2[0].astype(np.float64) + 0.25
+    params = synth.dis_params(cfg, coarsest=3)
+    params = dataclasses.replace(params, finest_scale=1)
+    want = orc.dis_flow(a.astype(np.float64), b, params)
+    assert np.array_equal(dis_flow(a, b, params), want)
+    got_t = dis_flow(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), params)
+    assert np.array_equal(got_t.cpu().numpy(), want)
+    eng = FlowEngine(1, 109, 256, params)
+    assert np.array_equal(eng.run_host(a[None], b[None])[0], want)
+    # a NaN in the float64 frame2 is caught even though frame1 is uint8
+    bad = b.copy()
+    bad[7, 9] = np.nan
+    with pytest.raises(ValueError):
+        dis_flow(a, bad, params)
+
+
+def test_engine_rejects_mismatched_buffers(torch):
+    from paper_1603_03590_b200 import FlowEngine
+
+    cfg = synth.CONFIGS["c0"]
+    eng = FlowEngine(2, 64, 96, synth.dis_params(cfg, coarsest=2))
+    f = np.zeros((2, 64, 96), dtype=np.float32)
+    with pytest.raises(ValueError):
+        eng.run_host(f[:1], f[:1])
+    with pytest.raises(ValueError):
+        eng.run_host(f, f, out=np.empty((2, 64, 96, 2), dtype=np.float32))
+    with pytest.raises(ValueError):
+        eng.run_host(f, f, out=np.empty((1, 64, 96, 2)))
+    d = torch.zeros((2, 64, 96), device="cuda")
+    with pytest.raises(ValueError):
+        eng.run(d, d, out=torch.empty((2, 64, 96, 2), dtype=torch.float32, device="cuda"))
+    with pytest.raises(ValueError):
+        eng.run(d, d, out=torch.empty((2, 96, 64, 2), dtype=torch.float64,
+                                      device="cuda").transpose(1, 2))
+    with pytest.raises(ValueError):
+        eng.run(d, d, out=torch.empty((2, 64, 96, 2), dtype=torch.float64))  # host tensor
+
+
+def test_default_stream_is_torch_current_stream(torch):
+    """With no explicit stream the engine launches on torch's current stream,
+    so work queued there before the call (the frames' producer) is ordered
+    before the kernels."""
+    from paper_1603_03590_b200 import FlowEngine
+
+    cfg = synth.CONFIGS["c0"]
+    f1, f2 = synth.make_batch(cfg, seed=8, count=1)
+    eng = FlowEngine(1, cfg.height, cfg.width, synth.dis_params(cfg))
+    want = eng.run(torch.from_numpy(f1).cuda(), torch.from_numpy(f2).cuda()).cpu().numpy()
+    s = torch.cuda.Stream()
+    h1 = torch.from_numpy(f1).pin_memory()
+    with torch.cuda.stream(s):
+        a = torch.empty_like(h1, device="cuda")
+        torch.cuda._sleep(50_000_000)  # keep the side stream busy before the copy
+        a.copy_(h1, non_blocking=True)
+        b = torch.from_numpy(f2).cuda()
+        got = eng.run(a, b)
+        res = got.cpu().numpy()
+    assert np.array_equal(res, want)

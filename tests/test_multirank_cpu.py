@@ -111,3 +111,43 @@ def test_reference_arm_nonzero_rank_exits_quietly(monkeypatch, capsys):
     monkeypatch.setenv("WORLD_SIZE", "2")
     assert bench.main(["--impl", "reference", "--gpus", "2", "--steps", "1"]) == 0
     assert capsys.readouterr().out == ""
+
+
+@pytest.mark.parametrize("cfg,total,scaling", [("c3", 256, "strong"), ("c1", 128, "weak"),
+                                               ("c4", 31, "strong")])
+def test_bench_launcher_spawns_ranks(cfg, total, scaling):
+    """`bench.py --gpus 2` without torchrun re-launches itself as two ranks
+    under torch.distributed.run (127.0.0.1 rendezvous); the launch self-test
+    joins a gloo group, splits the config's pairs and reduces over ranks."""
+    import json
+    import subprocess
+    import sys
+
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    r = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--gpus", "2",
+                        "--config", cfg, "--launch-selftest"], capture_output=True, text=True,
+                       timeout=240, env=env, cwd=repo)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["world"] == 2 and d["scaling"] == scaling
+    assert d["pairs_total"] == total and d["pairs_sum_over_ranks"] == total
+    assert d["max_over_ranks"] == 2.0
+
+
+def test_rank_pairs_plan():
+    import bench
+    from tools import synth
+
+    c3 = synth.CONFIGS["c3"]
+    spans = [bench.rank_pairs(c3, r, 8) for r in range(8)]
+    assert [s[1] for s in spans] == [32] * 8 and spans[-1][0] + 32 == 256
+    c1 = synth.CONFIGS["c1"]
+    assert [bench.rank_pairs(c1, r, 4)[:2] for r in range(4)] == [(0, 64), (64, 64),
+                                                                   (128, 64), (192, 64)]
+    c4 = synth.CONFIGS["c4"]
+    assert sum(bench.rank_pairs(c4, r, 8)[1] for r in range(8)) == 31
