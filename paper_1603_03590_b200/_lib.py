@@ -14,6 +14,10 @@ from functools import lru_cache
 from .params import DisParamsC, ParameterError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdis_b200.so")
+# kernel experiments only (tools/build_variant.sh): an alternative in-tree build
+# of the same library, e.g. exp_so/libdis_<tag>.so
+if os.environ.get("DIS_B200_LIB"):
+    LIB_PATH = os.path.abspath(os.environ["DIS_B200_LIB"])
 
 DIS_OK = 0
 DIS_ERR_PARAMETER = -1
@@ -102,7 +106,7 @@ def lib() -> ctypes.CDLL:
     L.dis_stereo_batch_host.restype = ctypes.c_int
     L.dis_densify_bidirectional_workspace_bytes.argtypes = [_i32, _i32, _i32, _pp]
     L.dis_densify_bidirectional_workspace_bytes.restype = _sz
-    L.dis_densify_bidirectional.argtypes = [_vp, _vp, _i32, _i32, _i32, _pp] + [_vp] * 8 + [
+    L.dis_densify_bidirectional.argtypes = [_vp, _vp, _i32, _i32, _i32, _pp] + [_vp] * 9 + [
         _sz, _vp, _vp]
     L.dis_densify_bidirectional.restype = ctypes.c_int
     L.dis_sparse_workspace_bytes.argtypes = [_i32, _i32, _i32, _pp]

@@ -31,6 +31,50 @@ def test_library_exports_every_header_symbol():
     assert sorted(_lib.EXPORTED) == syms
 
 
+def _header_prototypes():
+    """{name: [C parameter types]} of every DIS_API function in the header."""
+    src = open(os.path.join(REPO, "include", "dis_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", " ", src, flags=re.S)
+    out = {}
+    for m in re.finditer(r"DIS_API\s+([^;]*?)\b(dis_\w+)\s*\(([^)]*)\)\s*;", src):
+        params = [p.strip() for p in m.group(3).split(",") if p.strip() and p.strip() != "void"]
+        types = []
+        for p in params:
+            p = " ".join(p.split())
+            ptr = p.count("*")
+            base = re.sub(r"\bconst\b|\*", " ", p).split()[0]
+            types.append("ptr" if ptr else base)
+        out[m.group(2)] = types
+    return out
+
+
+_CTYPE_OF = {"int32_t": ctypes.c_int32, "int": ctypes.c_int, "size_t": ctypes.c_size_t,
+             "double": ctypes.c_double, "uint32_t": ctypes.c_uint32}
+
+
+def test_ctypes_argtypes_match_header_prototypes():
+    """Every binding in _lib declares exactly the header's parameter list
+    (count, and pointer vs integer/float width), so no argument is
+    truncated or shifted (a missing slot once shifted a stream handle into
+    ctypes' default int conversion)."""
+    L = _lib.lib()
+    protos = _header_prototypes()
+    assert set(protos) == set(_lib.EXPORTED)
+    for name, types in protos.items():
+        fn = getattr(L, name)
+        at = fn.argtypes
+        assert at is not None, f"{name}: argtypes not declared"
+        assert len(at) == len(types), (name, len(at), len(types))
+        for i, (t, a) in enumerate(zip(types, at)):
+            if t == "ptr":
+                assert a is ctypes.c_void_p or a is ctypes.c_char_p or hasattr(a, "contents") \
+                    or issubclass(a, ctypes._Pointer), (name, i, a)
+            else:
+                want = _CTYPE_OF[t]
+                assert ctypes.sizeof(a) == ctypes.sizeof(want), (name, i, t, a)
+                assert (a in (ctypes.c_double, ctypes.c_float)) == (t == "double"), (name, i)
+
+
 def test_params_struct_layout_matches_header():
     # dis_params_default fills the C struct; compare with DisParams() defaults
     c = DisParamsC()
