@@ -1,5 +1,7 @@
 """Micro-benchmark of the refinement stage alone (dis_refine, outer=1) on
-synthetic levels: python tools/sor_bench.py B H W [reps]."""
+synthetic levels:  python tools/sor_bench.py B:H:W [B:H:W ...] [--reps N]
+Prints tensor+assemble and SOR ms and the SOR's us per anti-diagonal step."""
+import argparse
 import ctypes
 import os
 import sys
@@ -12,9 +14,7 @@ from paper_1603_03590_b200 import _lib, stages
 from paper_1603_03590_b200.params import DisParams, VarParams, to_c
 
 
-def main():
-    B, H, W = (int(a) for a in sys.argv[1:4])
-    reps = int(sys.argv[4]) if len(sys.argv) > 4 else 5
+def run(B, H, W, reps):
     rng = np.random.default_rng(0)
     f = rng.uniform(0, 255, size=(2, B, H, W)).astype(np.float32)
     l1 = stages.build_pyramid(f[0], 0)[0]
@@ -48,8 +48,19 @@ def main():
     same = torch.equal(uu, ref[0]) and torch.equal(vv, ref[1])
     steps = W + H - 1 + 8
     sor_ms = ms[4] / reps
-    print(f"B={B} H={H} W={W} C={os.environ.get('DIS_SOR_CLUSTER', 'auto')} tensor {ms[3]/reps:.3f} ms "
-          f"sor {sor_ms:.3f} ms  ({sor_ms * 1e3 / steps:.2f} us/step) deterministic={same}")
+    print(f"{os.path.basename(_lib.LIB_PATH)} B={B} H={H} W={W} tensor {ms[3]/reps:.3f} ms "
+          f"sor {sor_ms:.3f} ms ({sor_ms * 1e3 / steps:.3f} us/step) deterministic={same}",
+          flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("shapes", nargs="+")
+    ap.add_argument("--reps", type=int, default=10)
+    a = ap.parse_args()
+    for s in a.shapes:
+        B, H, W = (int(x) for x in s.split(":"))
+        run(B, H, W, a.reps)
 
 
 if __name__ == "__main__":
