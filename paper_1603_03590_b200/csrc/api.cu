@@ -420,19 +420,16 @@ int run_pipeline(const Plan& pl, const dis_params_t* p, double* out, void* ws, c
 void build_pyramids(const Plan& pl, const void* f1, const void* f2, int dtype, void* ws,
                     cudaStream_t st) {
   uint32_t* status = at<uint32_t>(ws, pl.off_status);
-  for (int f = 0; f < 2; ++f) {
-    double* img[32];
-    double* gx[32];
-    double* gy[32];
-    double* dd[32];
+  double* img[2][32] = {};
+  double* gx[2][32] = {};
+  double* gy[2][32] = {};
+  for (int f = 0; f < 2; ++f)
     for (int s = 0; s <= pl.ss; ++s) {
-      img[s] = at<double>(ws, pl.off_img[f][s]);
-      gx[s] = at<double>(ws, pl.off_gx[f][s]);
-      gy[s] = at<double>(ws, pl.off_gy[f][s]);
-      dd[s] = at<double>(ws, pl.off_dd[f][s]);
+      img[f][s] = at<double>(ws, pl.off_img[f][s]);
+      gx[f][s] = at<double>(ws, pl.off_gx[f][s]);
+      gy[f][s] = at<double>(ws, pl.off_gy[f][s]);
     }
-    launch_pyramid(f ? f2 : f1, dtype, pl.B, pl.H, pl.W, pl.ss, img, gx, gy, dd, status, st);
-  }
+  launch_pyramid_pair(f1, f2, dtype, pl.B, pl.H, pl.W, pl.ss, img, gx, gy, status, st);
 }
 
 size_t dtype_size(int dtype) {

@@ -39,6 +39,12 @@ void launch_pyramid(const void* frames, int dtype, int B, int H, int W, int coar
                     double* const* img, double* const* gx, double* const* gy,
                     double* const* dd, uint32_t* status, cudaStream_t st);
 
+// both frames of a batch at once (the flow path): img[f][s] / gx / gy per
+// frame f and level s (null = not needed); no second derivatives
+void launch_pyramid_pair(const void* f1, const void* f2, int dtype, int B, int H, int W,
+                         int coarsest, double* const (*img)[32], double* const (*gx)[32],
+                         double* const (*gy)[32], uint32_t* status, cudaStream_t st);
+
 // patch_search.cu — init + precompute + condition + GN + reset + refresh
 struct SearchArgs {
   const double* ref;

@@ -375,6 +375,265 @@ static inline int grid_for(size_t n, int threads) {
   return (int)blocks;
 }
 
+// ---------------------------------------------------------------------------
+// Fused pyramid (the flow path; no second derivatives): two launches for both
+// frames of a batch instead of a convert / downsample / gradient chain per
+// level and frame.
+//
+// k_pyr_tile: one block per kPTX x kPTY tile of the BASE level L0 (level 1
+// built straight from the frames when the finest scale is >= 1, else level
+// 0): the tile plus a one-pixel halo (clamped coordinates = the reference's
+// one-sided borders) is formed in shared memory, the base image and its
+// gradients are written, and every coarser level whose 2^k-aligned pixels
+// fall inside the tile (box means are local to the tile) is reduced in
+// shared memory and written — levels L0+1 .. L0+5 from one read of the
+// frames.  The finiteness check of as_image covers every frame pixel.
+// k_pyr_grad: the gradients of the coarser levels, all levels and both
+// frames in one launch (their images are L2-resident by then).
+// ---------------------------------------------------------------------------
+constexpr int kPTX = 64, kPTY = 32;
+constexpr int kPTLevels = 5;  // halvings inside one tile (kPTY = 2^5)
+
+struct PyrArgs {
+  const void* frames[2];
+  int B, H, W;    // frames
+  int L0;         // base level: 0 or 1
+  int smax;       // deepest level reduced in the tile kernel
+  int g0, g1;     // gradient levels handled by k_pyr_grad: [g0, g1]
+  int Ws[32], Hs[32];
+  double* img[2][32];
+  double* gx[2][32];
+  double* gy[2][32];
+  uint32_t* status;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_pyr_tile(PyrArgs a) {
+  __shared__ double base[kPTY + 2][kPTX + 2];
+  __shared__ double lv[2][kPTY / 2][kPTX / 2];
+  const int z = blockIdx.z;
+  const int f = z / a.B, b = z - f * a.B;
+  const int W = a.W, H = a.H;
+  const T* __restrict__ fr = static_cast<const T*>(a.frames[f]) + (size_t)b * H * W;
+  const int L0 = a.L0;
+  const int Wb = a.Ws[L0], Hb = a.Hs[L0];
+  const int X0 = blockIdx.x * kPTX, Y0 = blockIdx.y * kPTY;
+  bool bad = false;
+  // ---- 1. base tile + halo (clamped coordinates) ----
+  for (int i = threadIdx.x; i < (kPTY + 2) * (kPTX + 2); i += 256) {
+    const int ly = i / (kPTX + 2), lx = i - ly * (kPTX + 2);
+    const int uy = Y0 - 1 + ly, ux = X0 - 1 + lx;
+    const int by = uy < 0 ? 0 : (uy > Hb - 1 ? Hb - 1 : uy);
+    const int bx = ux < 0 ? 0 : (ux > Wb - 1 ? Wb - 1 : ux);
+    const bool core = uy == by && ux == bx && ly >= 1 && ly <= kPTY && lx >= 1 && lx <= kPTX;
+    double v;
+    if (L0 == 0) {
+      v = to_f64(fr[(size_t)by * W + bx]);
+      if (core) bad |= !isfinite(v);
+    } else {  // _box_downsample of the converted frame: ((a+b)+(c+d))/4
+      const T* r0 = fr + (size_t)(2 * by) * W + 2 * bx;
+      const T* r1 = r0 + W;
+      const double p00 = to_f64(r0[0]), p01 = to_f64(r0[1]);
+      const double p10 = to_f64(r1[0]), p11 = to_f64(r1[1]);
+      if (core) bad |= !(isfinite(p00) && isfinite(p01) && isfinite(p10) && isfinite(p11));
+      v = ((p00 + p01) + (p10 + p11)) / 4.0;
+    }
+    base[ly][lx] = v;
+  }
+  if (L0 == 1) {  // frame pixels no 2x2 block covers: the odd last column / row
+    const bool right = X0 + kPTX >= Wb, bottom = Y0 + kPTY >= Hb;
+    if ((W & 1) && right)
+      for (int r = threadIdx.x; r < 2 * kPTY; r += 256) {
+        const int yy = 2 * Y0 + r;
+        if (yy < 2 * Hb) bad |= !isfinite(to_f64(fr[(size_t)yy * W + W - 1]));
+      }
+    if ((H & 1) && bottom) {
+      for (int c = threadIdx.x; c < 2 * kPTX; c += 256) {
+        const int xx = 2 * X0 + c;
+        if (xx < 2 * Wb) bad |= !isfinite(to_f64(fr[(size_t)(H - 1) * W + xx]));
+      }
+      if ((W & 1) && right && threadIdx.x == 0)
+        bad |= !isfinite(to_f64(fr[(size_t)(H - 1) * W + W - 1]));
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
+    set_status(a.status, DIS_STATUS_NONFINITE_INPUT);
+  __syncthreads();
+  // ---- 2. base image + gradients (image_gradients, clamped = one-sided) ----
+  {
+    double* __restrict__ oimg = a.img[f][L0];
+    double* __restrict__ ogx = a.gx[f][L0];
+    double* __restrict__ ogy = a.gy[f][L0];
+    const size_t plane = (size_t)Wb * Hb;
+    for (int i = threadIdx.x; i < kPTY * (kPTX / 2); i += 256) {
+      const int ly = i / (kPTX / 2), lx = 2 * (i - ly * (kPTX / 2));
+      const int y = Y0 + ly, x = X0 + lx;
+      if (y >= Hb || x >= Wb) continue;
+      const size_t o = (size_t)b * plane + (size_t)y * Wb + x;
+      const int cy = ly + 1, cx = lx + 1;
+      const double i0 = base[cy][cx], i1 = base[cy][cx + 1];
+      const double gx0 = 0.5 * (base[cy][cx + 1] - base[cy][cx - 1]);
+      const double gx1 = 0.5 * (base[cy][cx + 2] - base[cy][cx]);
+      const double gy0 = 0.5 * (base[cy + 1][cx] - base[cy - 1][cx]);
+      const double gy1 = 0.5 * (base[cy + 1][cx + 1] - base[cy - 1][cx + 1]);
+      if (x + 1 < Wb && (o & 1) == 0) {
+        if (oimg) *reinterpret_cast<double2*>(oimg + o) = make_double2(i0, i1);
+        if (ogx) *reinterpret_cast<double2*>(ogx + o) = make_double2(gx0, gx1);
+        if (ogy) *reinterpret_cast<double2*>(ogy + o) = make_double2(gy0, gy1);
+      } else {
+        if (oimg) oimg[o] = i0;
+        if (ogx) ogx[o] = gx0;
+        if (ogy) ogy[o] = gy0;
+        if (x + 1 < Wb) {
+          if (oimg) oimg[o + 1] = i1;
+          if (ogx) ogx[o + 1] = gx1;
+          if (ogy) ogy[o + 1] = gy1;
+        }
+      }
+    }
+  }
+  // ---- 3. coarser levels reduced in shared memory ----
+  for (int s = L0 + 1; s <= a.smax; ++s) {
+    const int k = s - L0;  // halvings from the base
+    const int tw = kPTX >> k, th = kPTY >> k;
+    const int Xs = X0 >> k, Ys = Y0 >> k;
+    const int Wsl = a.Ws[s], Hsl = a.Hs[s];
+    double* __restrict__ oimg = a.img[f][s];
+    double(*dst)[kPTX / 2] = lv[(k - 1) & 1];
+    double(*src)[kPTX / 2] = lv[k & 1];
+    for (int i = threadIdx.x; i < tw * th; i += 256) {
+      const int ly = i / tw, lx = i - ly * tw;
+      double p00, p01, p10, p11;
+      if (k == 1) {
+        p00 = base[2 * ly + 1][2 * lx + 1];
+        p01 = base[2 * ly + 1][2 * lx + 2];
+        p10 = base[2 * ly + 2][2 * lx + 1];
+        p11 = base[2 * ly + 2][2 * lx + 2];
+      } else {
+        p00 = src[2 * ly][2 * lx];
+        p01 = src[2 * ly][2 * lx + 1];
+        p10 = src[2 * ly + 1][2 * lx];
+        p11 = src[2 * ly + 1][2 * lx + 1];
+      }
+      const double v = ((p00 + p01) + (p10 + p11)) / 4.0;
+      dst[ly][lx] = v;
+      const int y = Ys + ly, x = Xs + lx;
+      if (y < Hsl && x < Wsl) oimg[(size_t)b * Wsl * Hsl + (size_t)y * Wsl + x] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// gradients of levels [g0, g1] of both frames: blockIdx.y = level - g0,
+// blockIdx.z = frame * B + pair; 64 x 8 outputs per block (k_gradients_xy)
+__global__ void __launch_bounds__(256) k_pyr_grad(PyrArgs a) {
+  const int s = a.g0 + (int)blockIdx.y;
+  const int z = blockIdx.z;
+  const int f = z / a.B, b = z - f * a.B;
+  double* __restrict__ ogx = a.gx[f][s];
+  double* __restrict__ ogy = a.gy[f][s];
+  if (!ogx && !ogy) return;
+  const int W = a.Ws[s], H = a.Hs[s];
+  const int tx = (W + 63) / 64;
+  const int tile = blockIdx.x;
+  if (tile >= tx * ((H + 7) / 8)) return;
+  const int ty = tile / tx;
+  const int x = 2 * ((tile - ty * tx) * 32 + (threadIdx.x & 31));
+  const int y = ty * 8 + (threadIdx.x >> 5);
+  if (x >= W || y >= H) return;
+  const size_t plane = (size_t)W * H;
+  const double* img = a.img[f][s] + b * plane;
+  const double* row = img + (size_t)y * W;
+  const double* up = img + (size_t)(y > 0 ? y - 1 : 0) * W;
+  const double* dn = img + (size_t)(y < H - 1 ? y + 1 : H - 1) * W;
+  const size_t o = b * plane + (size_t)y * W + x;
+  auto gxv = [&](int xx) {
+    const int xm = xx > 0 ? xx - 1 : 0, xp = xx < W - 1 ? xx + 1 : W - 1;
+    return 0.5 * (row[xp] - row[xm]);
+  };
+  auto gyv = [&](int xx) { return 0.5 * (dn[xx] - up[xx]); };
+  if (x + 1 < W && (o & 1) == 0) {
+    if (ogx) *reinterpret_cast<double2*>(ogx + o) = make_double2(gxv(x), gxv(x + 1));
+    if (ogy) *reinterpret_cast<double2*>(ogy + o) = make_double2(gyv(x), gyv(x + 1));
+  } else {
+    for (int q = 0; q < 2 && x + q < W; ++q) {
+      if (ogx) ogx[o + q] = gxv(x + q);
+      if (ogy) ogy[o + q] = gyv(x + q);
+    }
+  }
+}
+
+template <typename T>
+static void launch_pyramid_fused_t(PyrArgs& a, int nf, int coarsest, cudaStream_t st) {
+  prof_begin(KC_PYRAMID, st);
+  const int L0 = a.L0;
+  a.smax = L0 + kPTLevels < coarsest ? L0 + kPTLevels : coarsest;
+  dim3 g((unsigned)((a.Ws[L0] + kPTX - 1) / kPTX), (unsigned)((a.Hs[L0] + kPTY - 1) / kPTY),
+         (unsigned)(nf * a.B));
+  k_pyr_tile<T><<<g, 256, 0, st>>>(a);
+  note_launch();
+  // levels deeper than one tile's halvings: box means level by level
+  for (int s = a.smax + 1; s <= coarsest; ++s) {
+    for (int f = 0; f < nf; ++f) {
+      const int ho = a.Hs[s], wo = a.Ws[s];
+      k_downsample<<<grid_for((size_t)a.B * ho * ((wo + 1) / 2), 256), 256, 0, st>>>(
+          a.img[f][s - 1], a.B, a.Hs[s - 1], a.Ws[s - 1], a.img[f][s]);
+      note_launch();
+    }
+  }
+  a.g0 = L0 + 1;
+  a.g1 = coarsest;
+  int tiles = 0;
+  bool any = false;
+  for (int s = a.g0; s <= a.g1; ++s) {
+    const int t = ((a.Ws[s] + 63) / 64) * ((a.Hs[s] + 7) / 8);
+    tiles = t > tiles ? t : tiles;
+    for (int f = 0; f < nf; ++f) any |= a.gx[f][s] || a.gy[f][s];
+  }
+  if (any) {
+    dim3 gg((unsigned)tiles, (unsigned)(a.g1 - a.g0 + 1), (unsigned)(nf * a.B));
+    k_pyr_grad<<<gg, 256, 0, st>>>(a);
+    note_launch();
+  }
+  prof_end(KC_PYRAMID, st);
+}
+
+// both frames (f2 may be null: one frame); img[f][s] needed for s >= L0
+// (L0 = 0 when img[f][0] is requested, else 1); gx/gy where non-null
+void launch_pyramid_pair(const void* f1, const void* f2, int dtype, int B, int H, int W,
+                         int coarsest, double* const (*img)[32], double* const (*gx)[32],
+                         double* const (*gy)[32], uint32_t* status, cudaStream_t st) {
+  PyrArgs a{};
+  const int nf = f2 ? 2 : 1;
+  a.frames[0] = f1;
+  a.frames[1] = f2;
+  a.B = B;
+  a.H = H;
+  a.W = W;
+  a.L0 = (img[0][0] != nullptr || coarsest == 0) ? 0 : 1;
+  for (int s = 0; s <= coarsest && s < 32; ++s) {
+    a.Ws[s] = W >> s;
+    a.Hs[s] = H >> s;
+    for (int f = 0; f < nf; ++f) {
+      a.img[f][s] = img[f][s];
+      a.gx[f][s] = gx[f][s];
+      a.gy[f][s] = gy[f][s];
+    }
+  }
+  a.status = status;
+  switch (dtype) {
+    case DIS_DTYPE_F32:
+      launch_pyramid_fused_t<float>(a, nf, coarsest, st);
+      break;
+    case DIS_DTYPE_F64:
+      launch_pyramid_fused_t<double>(a, nf, coarsest, st);
+      break;
+    default:
+      launch_pyramid_fused_t<uint8_t>(a, nf, coarsest, st);
+      break;
+  }
+}
+
 template <typename T>
 static void launch_pyramid_t(const T* frames, int B, int H, int W, int coarsest,
                              double* const* img, double* const* gx, double* const* gy,
@@ -423,6 +682,20 @@ static void launch_pyramid_t(const T* frames, int B, int H, int W, int coarsest,
 void launch_pyramid(const void* frames, int dtype, int B, int H, int W, int coarsest,
                     double* const* img, double* const* gx, double* const* gy,
                     double* const* dd, uint32_t* status, cudaStream_t st) {
+  bool want_dd = false;
+  for (int s = 0; s <= coarsest; ++s) want_dd |= dd && dd[s];
+  if (!want_dd && coarsest < 32) {
+    double* im[1][32] = {};
+    double* x[1][32] = {};
+    double* y[1][32] = {};
+    for (int s = 0; s <= coarsest; ++s) {
+      im[0][s] = img[s];
+      x[0][s] = gx ? gx[s] : nullptr;
+      y[0][s] = gy ? gy[s] : nullptr;
+    }
+    launch_pyramid_pair(frames, nullptr, dtype, B, H, W, coarsest, im, x, y, status, st);
+    return;
+  }
   switch (dtype) {
     case DIS_DTYPE_F32:
       launch_pyramid_t((const float*)frames, B, H, W, coarsest, img, gx, gy, dd, status, st);

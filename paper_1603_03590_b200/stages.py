@@ -36,10 +36,13 @@ def grid_axis(dim: int, patch_size: int, overlap: float) -> np.ndarray:
     return np.frombuffer(out, dtype=np.int32).astype(np.int64)
 
 
-def build_pyramid(frames, coarsest: int, finest: int = 0, second_derivatives: bool = True):
+def build_pyramid(frames, coarsest: int, finest: int = 0, second_derivatives: bool = True,
+                  level0: bool = True):
     """build_pyramid (core.py:106-128) for a batch of frames: list over levels
     0..coarsest of dicts {img, gx, gy, dd}; gradients only for levels
-    >= finest (dd = (B, 4, H, W): gxx, gxy, gyx, gyy)."""
+    >= finest (dd = (B, 4, H, W): gxx, gxy, gyx, gyy).  ``level0=False``
+    leaves level 0's float64 image out (level 1 is built straight from the
+    frames, as on the flow path when the finest scale is >= 1)."""
     torch = _require_cuda()
     f = _to_device_frames(frames, "cuda")
     if f.dim() == 2:
@@ -48,7 +51,9 @@ def build_pyramid(frames, coarsest: int, finest: int = 0, second_derivatives: bo
     levels = []
     for s in range(coarsest + 1):
         h, w = H >> s, W >> s
-        lv = {"img": torch.empty((B, h, w), dtype=torch.float64, device=f.device)}
+        lv = {}
+        if s > 0 or level0 or finest == 0:
+            lv["img"] = torch.empty((B, h, w), dtype=torch.float64, device=f.device)
         if s >= finest:
             lv["gx"] = torch.empty_like(lv["img"])
             lv["gy"] = torch.empty_like(lv["img"])
@@ -56,7 +61,7 @@ def build_pyramid(frames, coarsest: int, finest: int = 0, second_derivatives: bo
                 lv["dd"] = torch.empty((B, 4, h, w), dtype=torch.float64, device=f.device)
         levels.append(lv)
     arr = ctypes.c_void_p * (coarsest + 1)
-    img = arr(*[lv["img"].data_ptr() for lv in levels])
+    img = arr(*[lv["img"].data_ptr() if "img" in lv else None for lv in levels])
     gx = arr(*[lv["gx"].data_ptr() if "gx" in lv else None for lv in levels])
     gy = arr(*[lv["gy"].data_ptr() if "gy" in lv else None for lv in levels])
     dd = arr(*[lv["dd"].data_ptr() if "dd" in lv else None for lv in levels])

@@ -368,7 +368,7 @@ def test_mixed_dtype_pair_promotes_to_float64(torch, orc):
 def test_engine_rejects_mismatched_buffers(torch):
     from paper_1603_03590_b200 import FlowEngine
 
-    cfg = synth.CONFIGS["c0"]
+    cfg = synth.CONFIGS["c1"]
     eng = FlowEngine(2, 64, 96, synth.dis_params(cfg, coarsest=2))
     f = np.zeros((2, 64, 96), dtype=np.float32)
     with pytest.raises(ValueError):
@@ -407,3 +407,38 @@ def test_default_stream_is_torch_current_stream(torch):
         got = eng.run(a, b)
         res = got.cpu().numpy()
     assert np.array_equal(res, want)
+
+
+@pytest.mark.parametrize("h,w,coarsest,finest", [(67, 95, 3, 1), (436, 1024, 5, 1), (64, 130, 4, 0),
+                                                 (256, 2049, 7, 1), (1080, 1920, 7, 2)])
+def test_fused_pyramid_matches_oracle(torch, st, orc, h, w, coarsest, finest):
+    """The flow path's fused pyramid (one tile kernel for the base level, its
+    gradients and the coarser images from shared memory, one launch for the
+    coarser gradients; deeper levels by box-mean launches): every level's
+    image and gradients bit-exact against the oracle, odd sizes, f32/f64/u8
+    frames, base level 0 and 1, pyramids deeper than one tile's halvings."""
+    rng = np.random.default_rng(h + w)
+    for dt in (np.float32, np.float64, np.uint8):
+        img = rng.uniform(0, 255, size=(2, h, w)).astype(dt)
+        lv = st.build_pyramid(img, coarsest, finest=finest, second_derivatives=False,
+                              level0=finest == 0)
+        for b in range(2):
+            ref = orc.build_pyramid(img[b].astype(np.float64), coarsest)
+            for s in range(0 if finest == 0 else 1, coarsest + 1):
+                assert np.array_equal(_np(lv[s]["img"])[b], ref[s][0]), (dt, b, s)
+                if s >= finest:
+                    assert np.array_equal(_np(lv[s]["gx"])[b], ref[s][1]), (dt, b, s)
+                    assert np.array_equal(_np(lv[s]["gy"])[b], ref[s][2]), (dt, b, s)
+
+
+@pytest.mark.parametrize("h,w", [(67, 95), (436, 1024), (65, 130)])
+def test_fused_pyramid_nonfinite_anywhere(torch, st, h, w):
+    rng = np.random.default_rng(h * 7 + w)
+    spots = [(0, 0), (h - 1, w - 1), (h - 1, 0), (0, w - 1), (h // 2, w // 2)]
+    for finest in (0, 1):
+        for y, x in spots:
+            img = rng.uniform(0, 255, (2, h, w)).astype(np.float32)
+            img[1, y, x] = np.nan
+            with pytest.raises(ValueError):
+                st.build_pyramid(img, 2, finest=finest, second_derivatives=False,
+                                 level0=finest == 0)
