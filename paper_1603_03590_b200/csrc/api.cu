@@ -590,17 +590,54 @@ size_t dis_workspace_bytes(int32_t B, int32_t H, int32_t W, const dis_params_t* 
 namespace {
 constexpr int kHostChunksMax = 16;
 
-// chunks of the host-buffer pipeline: more chunks overlap more of the copies
-// (the first H2D and the last D2H are exposed) at the cost of smaller kernels
-// (measured on c1 with the graph replay: 4 pairs per chunk, 4..16 chunks)
-int host_chunks(int B) {
+// Chunk schedule of the host-buffer pipeline.  The device->host copy of the
+// float64 flow is the bottleneck (2x the input bytes, one copy engine per
+// direction), and it can only start once the first chunk is computed, so the
+// first chunks are small (1, 1, 2, 4 pairs: a short exposed head) and the rest
+// are large enough for efficient kernels (up to 8 pairs); every chunk runs on
+// its own stream, so chunk i's copies overlap the kernels of the others.
+struct ChunkPlan {
+  int n = 0;
+  int first[kHostChunksMax + 1];  // chunk c holds pairs [first[c], first[c+1])
+  int bmax = 0;
+};
+ChunkPlan host_chunks(int B) {
   static const int forced = [] {
-    const char* e = getenv("DIS_HOST_CHUNKS");  // experiments only
+    const char* e = getenv("DIS_HOST_CHUNKS");  // experiments only: equal chunks
     return e ? atoi(e) : 0;
   }();
-  int want = forced > 0 ? forced : B / 4;
-  want = want < 4 ? 4 : (want > kHostChunksMax ? kHostChunksMax : want);
-  return B >= want ? want : (B < 1 ? 1 : B);
+  ChunkPlan p;
+  std::vector<int> sz;
+  if (forced > 0) {
+    const int n = forced < kHostChunksMax ? (forced < B ? forced : B) : kHostChunksMax;
+    const int bc = (B + n - 1) / n;
+    for (int left = B; left > 0; left -= bc) sz.push_back(left < bc ? left : bc);
+  } else {
+    const int ramp[] = {1, 1, 2, 4};
+    const int big = 8;
+    int left = B;
+    for (int r : ramp) {
+      if (left <= 0) break;
+      const int t = r < left ? r : left;
+      sz.push_back(t);
+      left -= t;
+    }
+    int slots = kHostChunksMax - (int)sz.size();
+    while (left > 0) {  // the rest in chunks of ~big pairs, within the stream budget
+      int t = (left + slots - 1) / slots;
+      t = t < big ? (left < big ? left : big) : t;
+      sz.push_back(t);
+      left -= t;
+      --slots;
+    }
+  }
+  p.n = (int)sz.size();
+  p.first[0] = 0;
+  for (int c = 0; c < p.n; ++c) {
+    p.first[c + 1] = p.first[c] + sz[c];
+    p.bmax = sz[c] > p.bmax ? sz[c] : p.bmax;
+  }
+  return p;
 }
 
 size_t host_chunk_bytes(int Bc, int H, int W, int dtype, const dis_params_t* p) {
@@ -616,9 +653,11 @@ size_t host_chunk_bytes(int Bc, int H, int W, int dtype, const dis_params_t* p) 
 
 struct HostStreams {
   int dev = -1;
-  cudaStream_t s[kHostChunksMax] = {};
+  cudaStream_t s[kHostChunksMax] = {};  // per-chunk kernels
+  cudaStream_t in = nullptr, out = nullptr;  // the copies, in chunk order
   cudaStream_t cap = nullptr;  // graph capture origin (never the legacy stream)
   cudaEvent_t start = nullptr, done[kHostChunksMax] = {};
+  cudaEvent_t landed[kHostChunksMax] = {}, computed[kHostChunksMax] = {};
 };
 std::mutex g_host_mu;
 HostStreams g_host[16];
@@ -626,10 +665,10 @@ HostStreams g_host[16];
 
 size_t dis_host_workspace_bytes(int32_t B, int32_t H, int32_t W, int32_t dtype,
                                 const dis_params_t* p) {
-  const int n = host_chunks(B);
-  const int Bc = (B + n - 1) / n;
-  const size_t per = host_chunk_bytes(Bc, H, W, dtype, p);
-  return per ? per * n : 0;
+  if (B < 1) return 0;
+  const ChunkPlan cp = host_chunks(B);
+  const size_t per = host_chunk_bytes(cp.bmax, H, W, dtype, p);
+  return per ? per * cp.n : 0;
 }
 
 }  // extern "C"
@@ -805,7 +844,41 @@ bool is_pinned(const void* ptr) {
 int host_batch_enqueue(const void* host_frame1, const void* host_frame2, int32_t dtype,
                        int32_t B, int32_t H, int32_t W, const dis_params_t* p,
                        double* host_flow_out, void* workspace, cudaStream_t st, bool stereo,
-                       int n, int Bc, size_t per, int* used_out);
+                       const ChunkPlan& cp, size_t per, int* used_out);
+
+// experiments only (DIS_HOST_TRACE=1 with DIS_HOST_GRAPH=0): per-chunk event
+// times (frames landed, kernels done, flow copied) printed after each call
+bool host_trace_on() {
+  static const bool on = [] {
+    const char* e = getenv("DIS_HOST_TRACE");
+    return e && atoi(e) != 0;
+  }();
+  return on;
+}
+cudaEvent_t g_tr[kHostChunksMax][3];
+cudaEvent_t g_tr0;
+int g_tr_n = 0;
+void host_trace_mark(int c, cudaStream_t in, cudaStream_t cs, cudaStream_t out) {
+  if (!g_tr0) {
+    cudaEventCreate(&g_tr0);
+    for (int i = 0; i < kHostChunksMax; ++i)
+      for (int j = 0; j < 3; ++j) cudaEventCreate(&g_tr[i][j]);
+  }
+  if (c == 0) cudaEventRecord(g_tr0, in);  // (recorded after chunk 0's copies were enqueued)
+  cudaEventRecord(g_tr[c][0], in);
+  cudaEventRecord(g_tr[c][1], cs);
+  cudaEventRecord(g_tr[c][2], out);
+  g_tr_n = c + 1;
+}
+void host_trace_print() {
+  cudaDeviceSynchronize();
+  for (int c = 0; c < g_tr_n; ++c) {
+    float t[3];
+    for (int j = 0; j < 3; ++j) cudaEventElapsedTime(&t[j], g_tr0, g_tr[c][j]);
+    fprintf(stderr, "chunk %2d: landed %7.3f  computed %7.3f  copied out %7.3f ms\n", c, t[0],
+            t[1], t[2]);
+  }
+}
 
 int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dtype, int32_t B,
                     int32_t H, int32_t W, const dis_params_t* p, double* host_flow_out,
@@ -820,18 +893,26 @@ int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dt
   const size_t need = dis_host_workspace_bytes(B, H, W, dtype, p);
   if (workspace_bytes < need)
     return fail(DIS_ERR_WORKSPACE, "workspace holds %zu bytes, need %zu", workspace_bytes, need);
-  const int n = host_chunks(B);
-  const int Bc = (B + n - 1) / n;
-  const size_t per = host_chunk_bytes(Bc, H, W, dtype, p);
+  const ChunkPlan cp = host_chunks(B);
+  const size_t per = host_chunk_bytes(cp.bmax, H, W, dtype, p);
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> guard(g_host_mu);
   HostStreams& hs = g_host[dev & 15];
   if (hs.dev != dev) {
+    // the first (small) chunks get the highest stream priority: the flow's
+    // device->host copy, the pipeline's bottleneck, starts once chunk 0 is done
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
     for (int i = 0; i < kHostChunksMax; ++i) {
-      cudaStreamCreateWithFlags(&hs.s[i], cudaStreamNonBlocking);
+      const int pr = prio_hi + i < prio_lo ? prio_hi + i : prio_lo;
+      cudaStreamCreateWithPriority(&hs.s[i], cudaStreamNonBlocking, pr);
       cudaEventCreateWithFlags(&hs.done[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&hs.landed[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&hs.computed[i], cudaEventDisableTiming);
     }
+    cudaStreamCreateWithFlags(&hs.in, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&hs.out, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&hs.start, cudaEventDisableTiming);
     cudaStreamCreateWithFlags(&hs.cap, cudaStreamNonBlocking);
     hs.dev = dev;
@@ -874,14 +955,14 @@ int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dt
   if (hg && hg->exec) {  // replay
     if (cudaGraphLaunch(hg->exec, st) != cudaSuccess)
       return fail(DIS_ERR_CUDA, "dis_flow_batch_host: graph launch failed");
-    used = (B + Bc - 1) / Bc;
+    used = cp.n;
     g_launches = hg->launches;
   } else if (hg && hg->seen >= 1) {  // capture this call, then replay it
     cudaGraph_t graph = nullptr;
     if (cudaStreamBeginCapture(hs.cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
       return fail(DIS_ERR_CUDA, "dis_flow_batch_host: stream capture failed");
     rc = host_batch_enqueue(host_frame1, host_frame2, dtype, B, H, W, p, host_flow_out,
-                            workspace, hs.cap, stereo, n, Bc, per, &used);
+                            workspace, hs.cap, stereo, cp, per, &used);
     const cudaError_t ce = cudaStreamEndCapture(hs.cap, &graph);
     if (rc) {
       if (graph) cudaGraphDestroy(graph);
@@ -899,11 +980,12 @@ int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dt
   } else {
     if (hg) ++hg->seen;
     rc = host_batch_enqueue(host_frame1, host_frame2, dtype, B, H, W, p, host_flow_out,
-                            workspace, st, stereo, n, Bc, per, &used);
+                            workspace, st, stereo, cp, per, &used);
     if (rc) return rc;
   }
   cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return fail(DIS_ERR_CUDA, "dis_flow_batch_host: %s", cudaGetErrorString(e));
+  if (host_trace_on()) host_trace_print();
   uint32_t any = 0;
   for (int c = 0; c < used; ++c) {
     uint32_t status = 0;
@@ -917,7 +999,7 @@ int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dt
 int host_batch_enqueue(const void* host_frame1, const void* host_frame2, int32_t dtype,
                        int32_t B, int32_t H, int32_t W, const dis_params_t* p,
                        double* host_flow_out, void* workspace, cudaStream_t st, bool stereo,
-                       int n, int Bc, size_t per, int* used_out) {
+                       const ChunkPlan& cp, size_t per, int* used_out) {
   int dev = 0;
   cudaGetDevice(&dev);
   HostStreams& hs = g_host[dev & 15];
@@ -927,13 +1009,19 @@ int host_batch_enqueue(const void* host_frame1, const void* host_frame2, int32_t
   const size_t px = (size_t)H * W;
   long long launches = 0;
   int used = 0;
-  for (int c = 0; c < n; ++c) {
-    const int b0 = c * Bc;
-    const int bn = B - b0 < Bc ? B - b0 : Bc;
+  // copies in chunk order on one stream per direction (each chunk's frames
+  // land as early as possible, the flow leaves in order without the copy
+  // engine interleaving the chunks); each chunk's kernels on its own stream
+  // so that they overlap each other and the copies
+  const int Bc = cp.bmax;
+  cudaStreamWaitEvent(hs.in, hs.start, 0);
+  cudaStreamWaitEvent(hs.out, hs.start, 0);
+  for (int c = 0; c < cp.n; ++c) {
+    const int b0 = cp.first[c];
+    const int bn = cp.first[c + 1] - b0;
     if (bn <= 0) break;
     ++used;
     cudaStream_t cs = hs.s[c];
-    cudaStreamWaitEvent(cs, hs.start, 0);
     char* wsc = static_cast<char*>(workspace) + (size_t)c * per;
     Plan pl;
     make_plan(p, bn, H, W, &pl);
@@ -944,17 +1032,26 @@ int host_batch_enqueue(const void* host_frame1, const void* host_frame2, int32_t
     void* d2 = wsc + take(cur, (size_t)Bc * px * esz);
     double* dout = reinterpret_cast<double*>(wsc + take(cur, (size_t)Bc * px * 2 * sizeof(double)));
     cudaMemcpyAsync(d1, static_cast<const char*>(host_frame1) + (size_t)b0 * px * esz, fbytes,
-                    cudaMemcpyHostToDevice, cs);
+                    cudaMemcpyHostToDevice, hs.in);
     cudaMemcpyAsync(d2, static_cast<const char*>(host_frame2) + (size_t)b0 * px * esz, fbytes,
-                    cudaMemcpyHostToDevice, cs);
+                    cudaMemcpyHostToDevice, hs.in);
+    cudaEventRecord(hs.landed[c], hs.in);
+    cudaStreamWaitEvent(cs, hs.landed[c], 0);
     rc = flow_batch_impl(d1, d2, dtype, bn, H, W, p, dout, wsc, pl.total, cs, stereo);
     if (rc) return rc;
     launches += g_launches.load();
+    cudaEventRecord(hs.computed[c], cs);
+    cudaStreamWaitEvent(hs.out, hs.computed[c], 0);
     cudaMemcpyAsync(host_flow_out + (size_t)b0 * px * 2, dout, obytes, cudaMemcpyDeviceToHost,
-                    cs);
-    cudaEventRecord(hs.done[c], cs);
+                    hs.out);
+    if (host_trace_on()) host_trace_mark(c, hs.in, cs, hs.out);
   }
-  for (int c = 0; c < used; ++c) cudaStreamWaitEvent(st, hs.done[c], 0);
+  cudaEventRecord(hs.done[0], hs.out);
+  cudaStreamWaitEvent(st, hs.done[0], 0);
+  for (int c = 0; c < used; ++c) {  // every chunk stream joins (graph capture)
+    cudaEventRecord(hs.done[c], hs.s[c]);
+    cudaStreamWaitEvent(st, hs.done[c], 0);
+  }
   g_launches = launches;
   *used_out = used;
   return DIS_OK;

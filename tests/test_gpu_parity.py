@@ -442,3 +442,24 @@ def test_fused_pyramid_nonfinite_anywhere(torch, st, h, w):
             with pytest.raises(ValueError):
                 st.build_pyramid(img, 2, finest=finest, second_derivatives=False,
                                  level0=finest == 0)
+
+
+@pytest.mark.parametrize("B", [1, 5, 13])
+def test_host_path_chunk_ramp_matches_device(torch, B):
+    """The host-buffer pipeline's chunk schedule (1, 1, 2, 4, then up to 8
+    pairs per chunk, each on its own stream) returns the device path's flows
+    for every pair, eagerly and from the captured graph."""
+    from paper_1603_03590_b200 import FlowEngine
+
+    cfg = synth.CONFIGS["c1"]
+    f1, f2 = synth.make_batch(cfg, seed=40, count=B, h=109, w=256)
+    params = synth.dis_params(cfg, coarsest=3)
+    eng = FlowEngine(B, 109, 256, params)
+    want = eng.run(torch.from_numpy(f1).cuda(), torch.from_numpy(f2).cuda()).cpu().numpy()
+    p1 = torch.from_numpy(f1).pin_memory()
+    p2 = torch.from_numpy(f2).pin_memory()
+    po = torch.empty((B, 109, 256, 2), dtype=torch.float64).pin_memory()
+    for _ in range(3):  # eager, capture, replay
+        po.zero_()
+        eng.run_host(p1.numpy(), p2.numpy(), out=po.numpy())
+        assert np.array_equal(po.numpy(), want)
