@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define DIS_B200_ABI_VERSION 1
+#define DIS_B200_ABI_VERSION 2
 
 /* status codes */
 #define DIS_OK 0
@@ -92,7 +92,7 @@ typedef struct dis_params_t {
   int32_t iterations;            /* theta_it                          */
   int32_t finest_scale;          /* theta_sf                          */
   int32_t coarsest_scale;        /* theta_ss                          */
-  int32_t downscale;             /* must be 2 on this path            */
+  int32_t downscale;             /* pyramid factor k, 2..128          */
   int32_t use_mean_normalization;
   int32_t use_densification;     /* carried; dense path always densifies */
   int32_t residual_norm;         /* DIS_NORM_*                        */
@@ -115,7 +115,7 @@ typedef struct dis_params_t {
 DIS_API void dis_params_default(dis_params_t* p);
 
 /* DisParams.validate + VarParams.validate (core.py:296-316, 215-223) plus
- * this path's own restriction downscale == 2. */
+ * this path's own limit downscale <= 128. */
 DIS_API int dis_params_validate(const dis_params_t* p);
 
 /* Workspace bytes for dis_flow_batch on B pairs of H x W frames. */
@@ -212,8 +212,10 @@ DIS_API int dis_status_to_error(uint32_t status);
  * as described at the top; `B` pairs are processed per call.
  * ---------------------------------------------------------------------- */
 
-/* build_pyramid (core.py:106-128): levels 0..coarsest of B frames.
- *   levels_img[s]  : device B x (H>>s) x (W>>s) float64 for every s in
+/* build_pyramid (core.py:106-128): levels 0..coarsest of B frames, factor
+ * `downscale` (k >= 2; level s is floor(dim / k^s), _box_downsample
+ * core.py:88-98 in numpy's summation order).
+ *   levels_img[s]  : device B x H_s x W_s float64 for every s in
  *                    0..coarsest (levels_img[0] may be NULL: level 1 is then
  *                    computed from the frames directly)
  *   levels_gx/gy[s]: gradients (image_gradients core.py:75-85), NULL = skip
@@ -221,9 +223,10 @@ DIS_API int dis_status_to_error(uint32_t status);
  *                    (_second_derivatives variational.py:168-171), NULL = skip
  *   status         : device uint32, OR-ed with DIS_STATUS_NONFINITE_INPUT */
 DIS_API int dis_build_pyramid(const void* frames, int32_t dtype, int32_t B, int32_t H,
-                      int32_t W, int32_t coarsest, double* const* levels_img,
-                      double* const* levels_gx, double* const* levels_gy,
-                      double* const* levels_dd, uint32_t* status, void* stream);
+                      int32_t W, int32_t coarsest, int32_t downscale,
+                      double* const* levels_img, double* const* levels_gx,
+                      double* const* levels_gy, double* const* levels_dd, uint32_t* status,
+                      void* stream);
 
 /* init_patches + precompute_patch_set + optimize_patch_set + reset_outliers
  * + refresh_patch_stats for one scale (pipeline.py:54-82).  p->mode == 1
@@ -286,11 +289,12 @@ DIS_API int dis_refine(const double* ref_img, const double* ref_gx, const double
                double* flow_u, double* flow_v, void* workspace,
                size_t workspace_bytes, uint32_t* status, void* stream);
 
-/* upsample_flow (core.py:178-190) by the factor 2 from a W x H level to a
- * Wn x Hn level (planar u, v in and out). */
+/* upsample_flow (core.py:178-190) by `scale_factor` from a W x H level to
+ * a Wn x Hn level (planar u, v in and out):
+ * out(x) = scale_factor * bilinear_map(flow, x / scale_factor). */
 DIS_API int dis_upsample_flow(const double* in_u, const double* in_v, int32_t B,
                       int32_t W, int32_t H, double* out_u, double* out_v,
-                      int32_t Wn, int32_t Hn, void* stream);
+                      int32_t Wn, int32_t Hn, int32_t scale_factor, void* stream);
 
 /* compose_flows (pipeline.py:186-199): out(x) = ab(x) + bc(x + ab(x)) with
  * bc sampled by bilinear_map (core.py:154-170).  B fields, each H x W x 2

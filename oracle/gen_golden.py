@@ -403,6 +403,67 @@ def gen_sparse():
     save("next_sparse.npz", **d)
 
 
+def gen_downscale():
+    """downscale > 2 (core.py:88-128 box means over k x k blocks, init_patches
+    densification.py:82-95, upsample_flow core.py:178-190, the sparse chain
+    pipeline.py:202-231): pyramids for k = 3, 4, 8, 9 and end-to-end flows,
+    stereo and sparse correspondences for k = 3 and 4."""
+    rng = np.random.default_rng(700)
+    d = {}
+    for k, (h, w) in {3: (97, 131), 4: (131, 257), 8: (130, 140), 9: (200, 190)}.items():
+        img = rng.uniform(0, 255, (h, w))
+        pyr = core.build_pyramid(img, 2 if k < 8 else 1, downscale=k)
+        d[f"pyr{k}_img"] = img
+        for s in range(len(pyr.levels)):
+            d[f"pyr{k}_L{s}"] = pyr[s].image
+            d[f"pyr{k}_L{s}_gx"] = pyr[s].grad_x
+            d[f"pyr{k}_L{s}_gy"] = pyr[s].grad_y
+    cases = {
+        # name: (seed, h, w, maxmag, params)
+        "f3": (40, 109, 256, 6.0, core.DisParams(
+            patch_size=8, overlap=0.5, iterations=32, finest_scale=1, coarsest_scale=2,
+            downscale=3, variational=VarParamsFixed(fixed_outer=1))),
+        "f3_default_outer": (41, 120, 200, 5.0, core.DisParams(
+            patch_size=8, overlap=0.3, iterations=16, finest_scale=1, coarsest_scale=2,
+            downscale=3)),
+        "f4": (42, 160, 300, 8.0, core.DisParams(
+            patch_size=8, overlap=0.5, iterations=32, finest_scale=1, coarsest_scale=2,
+            downscale=4, variational=VarParamsFixed(fixed_outer=1))),
+        "f3_s0": (43, 120, 200, 5.0, core.DisParams(
+            patch_size=12, overlap=0.75, iterations=64, finest_scale=0, coarsest_scale=2,
+            downscale=3, variational=VarParamsFixed(fixed_outer=1))),
+        "f3_bidir": (44, 109, 256, 6.0, core.DisParams(
+            patch_size=8, overlap=0.5, iterations=16, finest_scale=1, coarsest_scale=2,
+            downscale=3, variational=VarParamsFixed(fixed_outer=1), bidirectional=True)),
+    }
+    for name, (seed, h, w, mm, p) in cases.items():
+        f1, f2, _ = synth.make_pair(seed, h, w, mm, True, mm)
+        d[f"{name}_f1"] = f1
+        d[f"{name}_f2"] = f2
+        d[f"{name}_flow"] = pipeline.dis_flow(f1, f2, p)
+        for kk, v in _params_dict(p).items():
+            d[f"{name}_{kk}"] = v
+        d[f"{name}_downscale"] = p.downscale
+    f1, f2, _ = synth.make_stereo_pair(45, 96, 200, 6.0)
+    sp = core.DisParams(patch_size=8, overlap=0.5, iterations=16, finest_scale=1,
+                        coarsest_scale=2, downscale=3, mode="stereo",
+                        variational=VarParamsFixed(fixed_outer=1))
+    d["st3_f1"], d["st3_f2"] = f1, f2
+    d["st3_flow"] = pipeline.dis_stereo(f1, f2, sp)
+    f1, f2, _ = synth.make_pair(46, 109, 256, 6.0, True, 6.0)
+    seeds = np.concatenate([rng.uniform([0, 0], [255, 108], (30, 2)),
+                            np.array([[0.0, 0.0], [255.0, 108.0], [-1.0, 3.0]])])
+    d["sp_f1"], d["sp_f2"], d["sp_seeds"] = f1, f2, seeds
+    for name, dens in (("sp_dense", True), ("sp_chain", False)):
+        p = core.DisParams(patch_size=8, overlap=0.5, iterations=32, finest_scale=1,
+                           coarsest_scale=2, downscale=3, use_densification=dens,
+                           variational=VarParamsFixed(fixed_outer=1))
+        m = pipeline.sparse_correspondences(f1, f2, seeds, p)
+        d[f"{name}_disp"] = np.array([mm.displacement for mm in m])
+        d[f"{name}_valid"] = np.array([mm.valid for mm in m])
+    save("downscale.npz", **d)
+
+
 def gen_flowio():
     """flowio.py: .flo bytes written by the reference, images decoded by it
     (P5 8/16-bit with header comments, P6 luminance), written PGM/PPM bytes."""
@@ -450,7 +511,7 @@ def gen_flowio():
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     which = sys.argv[1:] or ["pyramid", "samplers", "search", "refine", "e2e", "full",
-                             "compose", "stereo", "bidir", "sparse", "flowio"]
+                             "compose", "stereo", "bidir", "sparse", "flowio", "downscale"]
     pipeline.warmup()
     if "pyramid" in which:
         gen_pyramid()
@@ -474,3 +535,5 @@ if __name__ == "__main__":
         gen_sparse()
     if "flowio" in which:
         gen_flowio()
+    if "downscale" in which:
+        gen_downscale()

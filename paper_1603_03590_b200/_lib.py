@@ -80,8 +80,8 @@ def lib() -> ctypes.CDLL:
     L.dis_read_status.restype = ctypes.c_int
     L.dis_status_to_error.argtypes = [ctypes.c_uint32]
     L.dis_status_to_error.restype = ctypes.c_int
-    L.dis_build_pyramid.argtypes = [_vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp,
-                                    _vp, _vp]
+    L.dis_build_pyramid.argtypes = [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp,
+                                    _vp, _vp, _vp]
     L.dis_build_pyramid.restype = ctypes.c_int
     L.dis_patch_search.argtypes = [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _i32, _i32,
                                    _pp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]
@@ -96,7 +96,7 @@ def lib() -> ctypes.CDLL:
     L.dis_refine.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _pp,
                              _i32, _vp, _vp, _vp, _sz, _vp, _vp]
     L.dis_refine.restype = ctypes.c_int
-    L.dis_upsample_flow.argtypes = [_vp, _vp, _i32, _i32, _i32, _vp, _vp, _i32, _i32, _vp]
+    L.dis_upsample_flow.argtypes = [_vp, _vp, _i32, _i32, _i32, _vp, _vp, _i32, _i32, _i32, _vp]
     L.dis_upsample_flow.restype = ctypes.c_int
     L.dis_flow_batch_levels.argtypes = [_vp] * 6 + [_i32, _i32, _i32, _pp, _vp, _vp, _sz, _vp]
     L.dis_flow_batch_levels.restype = ctypes.c_int
@@ -144,8 +144,8 @@ def lib() -> ctypes.CDLL:
     L.dis_selftest_fp64_peak.restype = ctypes.c_int
     L.dis_abi_version.argtypes = []
     L.dis_abi_version.restype = _i32
-    if L.dis_abi_version() != 1:
-        raise DisB200Error(f"libdis_b200 ABI {L.dis_abi_version()} != 1")
+    if L.dis_abi_version() != 2:
+        raise DisB200Error(f"libdis_b200 ABI {L.dis_abi_version()} != 2")
     return L
 
 

@@ -131,7 +131,7 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 // ---- workspace plan -------------------------------------------------------
 struct Plan {
-  int B, H, W, ss, sf, ps;
+  int B, H, W, ss, sf, ps, ds;
   bool var;
   int hs[32], ws[32];
   GridAxis ax[32], ay[32];
@@ -165,10 +165,11 @@ void make_plan(const dis_params_t* p, int B, int H, int W, Plan* pl) {
   pl->ps = p->patch_size;
   pl->var = p->variational != 0;
   pl->bidir = p->bidirectional != 0;
+  pl->ds = p->downscale;
   const int sp = grid_spacing(p->patch_size, p->overlap);
-  for (int s = 0; s <= pl->ss; ++s) {
-    pl->hs[s] = H >> s;
-    pl->ws[s] = W >> s;
+  for (int s = 0; s <= pl->ss; ++s) {  // floor(dim / k^s) (core.py:88-98 per level)
+    pl->hs[s] = s ? pl->hs[s - 1] / pl->ds : H;
+    pl->ws[s] = s ? pl->ws[s - 1] / pl->ds : W;
     if (s >= pl->sf) {
       pl->ax[s] = make_axis(pl->ws[s], pl->ps, sp);
       pl->ay[s] = make_axis(pl->hs[s], pl->ps, sp);
@@ -256,23 +257,27 @@ int check_dims(const dis_params_t* p, int B, int H, int W) {
   if (H < 1 || W < 1)
     return fail(DIS_ERR_VALUE, "image must be 2D and non-empty, got shape (%d, %d)", H, W);
   if (H < 2 || W < 2) return fail(DIS_ERR_VALUE, "image must be at least 2x2");
+  int hc = H, wc = W;
   for (int s = 1; s <= p->coarsest_scale; ++s) {
-    if ((H >> s) < 2 || (W >> s) < 2)
+    hc /= p->downscale;
+    wc /= p->downscale;
+    if (hc < 2 || wc < 2)
       return fail(DIS_ERR_VALUE,
                   "downsampled level would be %dx%d; levels below 2 pixels per axis are not "
                   "representable",
-                  W >> s, H >> s);
+                  wc, hc);
   }
-  const int hc = H >> p->coarsest_scale, wc = W >> p->coarsest_scale;
   if (wc < p->patch_size || hc < p->patch_size)
     return fail(DIS_ERR_VALUE,
                 "coarsest level %dx%d cannot hold a %dpx patch; lower coarsest_scale", wc, hc,
                 p->patch_size);
-  if (p->variational && (H >> p->finest_scale) > 2048)
+  int hf = H;
+  for (int s = 1; s <= p->finest_scale; ++s) hf /= p->downscale;
+  if (p->variational && hf > 2048)
     return fail(DIS_ERR_VALUE,
                 "variational refinement of a level taller than 2048 rows is not supported by "
                 "this build (level %d is %d rows)",
-                p->finest_scale, H >> p->finest_scale);
+                p->finest_scale, hf);
   return DIS_OK;
 }
 
@@ -299,6 +304,7 @@ void search_scale(const Plan& pl, const dis_params_t* p, void* ws, int s, int di
   a.mean_norm = p->use_mean_normalization;
   a.code = p->residual_norm;
   a.hb = p->huber_b;
+  a.ds = p->downscale;
   a.out_u = pu;
   a.out_v = pv;
   a.out_off = poff;
@@ -402,11 +408,12 @@ int run_pipeline(const Plan& pl, const dis_params_t* p, double* out, void* ws, c
       const int hn = pl.hs[s - 1], wn = pl.ws[s - 1];
       if (s - 1 == 0) {
         launch_upsample(prev_u, prev_v, pl.B, prev_w, prev_h, nullptr, nullptr, out, wn, hn,
-                        st);
+                        pl.ds, st);
       } else {
         double* nu = at<double>(ws, pl.off_fu[s - 1]);
         double* nv = at<double>(ws, pl.off_fv[s - 1]);
-        launch_upsample(prev_u, prev_v, pl.B, prev_w, prev_h, nu, nv, nullptr, wn, hn, st);
+        launch_upsample(prev_u, prev_v, pl.B, prev_w, prev_h, nu, nv, nullptr, wn, hn, pl.ds,
+                        st);
         prev_u = nu;
         prev_v = nv;
         prev_w = wn;
@@ -429,7 +436,7 @@ void build_pyramids(const Plan& pl, const void* f1, const void* f2, int dtype, v
       gx[f][s] = at<double>(ws, pl.off_gx[f][s]);
       gy[f][s] = at<double>(ws, pl.off_gy[f][s]);
     }
-  launch_pyramid_pair(f1, f2, dtype, pl.B, pl.H, pl.W, pl.ss, img, gx, gy, status, st);
+  launch_pyramid_pair(f1, f2, dtype, pl.B, pl.H, pl.W, pl.ss, pl.ds, img, gx, gy, status, st);
 }
 
 size_t dtype_size(int dtype) {
@@ -553,8 +560,8 @@ int dis_params_validate(const dis_params_t* p) {
     return fail(DIS_ERR_PARAMETER, "need 0 <= finest_scale <= coarsest_scale");
   if (p->coarsest_scale > 30) return fail(DIS_ERR_PARAMETER, "coarsest_scale too large");
   if (p->downscale < 2) return fail(DIS_ERR_PARAMETER, "downscale must be an integer >= 2");
-  if (p->downscale != 2)
-    return fail(DIS_ERR_PARAMETER, "this path implements downscale == 2 only");
+  if (p->downscale > 128)
+    return fail(DIS_ERR_PARAMETER, "this path implements downscale factors up to 128");
   if (p->residual_norm < 0 || p->residual_norm > 2)
     return fail(DIS_ERR_PARAMETER, "residual_norm must be one of ('l2', 'l1', 'huber')");
   if (p->residual_norm == DIS_NORM_HUBER && !(p->huber_b > 0))
@@ -1063,14 +1070,27 @@ extern "C" {
 // ---- stage entry points -----------------------------------------------------
 
 int dis_build_pyramid(const void* frames, int32_t dtype, int32_t B, int32_t H, int32_t W,
-                      int32_t coarsest, double* const* levels_img, double* const* levels_gx,
-                      double* const* levels_gy, double* const* levels_dd, uint32_t* status,
-                      void* stream) {
+                      int32_t coarsest, int32_t downscale, double* const* levels_img,
+                      double* const* levels_gx, double* const* levels_gy,
+                      double* const* levels_dd, uint32_t* status, void* stream) {
   if (coarsest < 0) return fail(DIS_ERR_PARAMETER, "coarsest_scale must be >= 0");
+  if (downscale < 2) return fail(DIS_ERR_PARAMETER, "downscale must be an integer >= 2");
+  if (downscale > 128)
+    return fail(DIS_ERR_PARAMETER, "this path implements downscale factors up to 128");
+  if (coarsest > 30) return fail(DIS_ERR_PARAMETER, "coarsest_scale too large");
   if (H < 2 || W < 2) return fail(DIS_ERR_VALUE, "image must be at least 2x2");
-  for (int s = 1; s <= coarsest; ++s)
-    if ((H >> s) < 2 || (W >> s) < 2)
-      return fail(DIS_ERR_VALUE, "downsampled level would be %dx%d", W >> s, H >> s);
+  {
+    int h = H, w = W;
+    for (int s = 1; s <= coarsest; ++s) {
+      h /= downscale;
+      w /= downscale;
+      if (h < 2 || w < 2)
+        return fail(DIS_ERR_VALUE,
+                    "downsampled level would be %dx%d; levels below 2 pixels per axis are not "
+                    "representable",
+                    w, h);
+    }
+  }
   if (!levels_img) return fail(DIS_ERR_VALUE, "levels_img is NULL");
   for (int s = 1; s <= coarsest; ++s)
     if (!levels_img[s]) return fail(DIS_ERR_VALUE, "levels_img[%d] is NULL", s);
@@ -1081,8 +1101,8 @@ int dis_build_pyramid(const void* frames, int32_t dtype, int32_t B, int32_t H, i
     if ((gx[s] || gy[s] || (levels_dd && levels_dd[s])) && !levels_img[s])
       return fail(DIS_ERR_VALUE, "gradients of level %d need its image", s);
   }
-  launch_pyramid(frames, dtype, B, H, W, coarsest, levels_img, gx.data(), gy.data(), levels_dd,
-                 status, as_stream(stream));
+  launch_pyramid(frames, dtype, B, H, W, coarsest, downscale, levels_img, gx.data(), gy.data(),
+                 levels_dd, status, as_stream(stream));
   return check_cuda("dis_build_pyramid");
 }
 
@@ -1138,6 +1158,7 @@ int dis_patch_search(const double* ref_img, const double* ref_gx, const double* 
   a.mean_norm = p->use_mean_normalization;
   a.code = p->residual_norm;
   a.hb = p->huber_b;
+  a.ds = p->downscale;
   a.out_u = out_u;
   a.out_v = out_v;
   a.out_off = out_off;
@@ -1246,8 +1267,10 @@ int dis_sparse_correspondences(const void* frame1, const void* frame2, int32_t d
     rc = run_pipeline(pl, &sp.q, nullptr, workspace, st, false, false);
     if (rc) return rc;
     const int sf = pl.sf;
+    double scale = 1.0;  // params.downscale ** finest_scale (pipeline.py:266)
+    for (int s = 0; s < sf; ++s) scale *= (double)pl.ds;
     launch_sparse_sample(at<double>(workspace, pl.off_fu[sf]), at<double>(workspace, pl.off_fv[sf]),
-                         pl.ws[sf], pl.hs[sf], sf, d_seeds, d_valid, n_seeds, d_out, st);
+                         pl.ws[sf], pl.hs[sf], scale, d_seeds, d_valid, n_seeds, d_out, st);
   } else {
     SparseChainArgs a{};
     for (int s = 0; s <= pl.ss; ++s) {
@@ -1265,6 +1288,7 @@ int dis_sparse_correspondences(const void* frame1, const void* frame2, int32_t d
     a.mean_norm = p->use_mean_normalization;
     a.code = p->residual_norm;
     a.hb = p->huber_b;
+    a.ds = p->downscale;
     a.seeds = d_seeds;
     a.valid = d_valid;
     a.n = n_seeds;
@@ -1362,8 +1386,11 @@ int dis_refine(const double* ref_img, const double* ref_gx, const double* ref_gy
 }
 
 int dis_upsample_flow(const double* in_u, const double* in_v, int32_t B, int32_t W, int32_t H,
-                      double* out_u, double* out_v, int32_t Wn, int32_t Hn, void* stream) {
-  launch_upsample(in_u, in_v, B, W, H, out_u, out_v, nullptr, Wn, Hn, as_stream(stream));
+                      double* out_u, double* out_v, int32_t Wn, int32_t Hn, int32_t scale_factor,
+                      void* stream) {
+  if (scale_factor < 1) return fail(DIS_ERR_PARAMETER, "scale_factor must be >= 1");
+  launch_upsample(in_u, in_v, B, W, H, out_u, out_v, nullptr, Wn, Hn, scale_factor,
+                  as_stream(stream));
   return check_cuda("dis_upsample_flow");
 }
 

@@ -35,15 +35,17 @@ int current_device();
 int device_sm_count();
 
 // pyramid.cu
+// downscale: the pyramid factor k (core.py:88-128); level s is floor(dim / k^s)
 void launch_pyramid(const void* frames, int dtype, int B, int H, int W, int coarsest,
-                    double* const* img, double* const* gx, double* const* gy,
+                    int downscale, double* const* img, double* const* gx, double* const* gy,
                     double* const* dd, uint32_t* status, cudaStream_t st);
 
 // both frames of a batch at once (the flow path): img[f][s] / gx / gy per
 // frame f and level s (null = not needed); no second derivatives
 void launch_pyramid_pair(const void* f1, const void* f2, int dtype, int B, int H, int W,
-                         int coarsest, double* const (*img)[32], double* const (*gx)[32],
-                         double* const (*gy)[32], uint32_t* status, cudaStream_t st);
+                         int coarsest, int downscale, double* const (*img)[32],
+                         double* const (*gx)[32], double* const (*gy)[32], uint32_t* status,
+                         cudaStream_t st);
 
 // patch_search.cu — init + precompute + condition + GN + reset + refresh
 struct SearchArgs {
@@ -58,6 +60,7 @@ struct SearchArgs {
   GridAxis ax, ay;
   int ps, iters, mean_norm, code;
   double hb;
+  int ds;            // pyramid factor (init_patches: centre / ds, times ds)
   double* out_u;
   double* out_v;
   double* out_off;
@@ -107,9 +110,11 @@ struct RefineArgs {
 size_t refine_scratch_doubles(int B, int W, int H);
 int launch_refine(const RefineArgs& a, cudaStream_t st);
 
-// upsample.cu — upsample_flow by 2 (planar in, planar or interleaved out)
+// upsample.cu — upsample_flow by the pyramid factor (planar in, planar or
+// interleaved out)
 void launch_upsample(const double* iu, const double* iv, int B, int W, int H, double* ou,
-                     double* ov, double* out_interleaved, int Wn, int Hn, cudaStream_t st);
+                     double* ov, double* out_interleaved, int Wn, int Hn, int factor,
+                     cudaStream_t st);
 void launch_interleave(const double* u, const double* v, int B, int W, int H, double* out,
                        cudaStream_t st);
 
@@ -122,6 +127,7 @@ struct SparseChainArgs {
   int W[32], H[32];
   int coarsest, finest, ps, iters, mean_norm, code;
   double hb;
+  int ds;                // pyramid factor
   const double* seeds;   // (n, 2) device
   const uint8_t* valid;  // (n) device
   int n;
@@ -129,7 +135,7 @@ struct SparseChainArgs {
   double* out;           // (n, 2)
 };
 void launch_sparse_chain(const SparseChainArgs& a, cudaStream_t st);
-void launch_sparse_sample(const double* fu, const double* fv, int W, int H, int finest,
+void launch_sparse_sample(const double* fu, const double* fv, int W, int H, double scale,
                           const double* seeds, const uint8_t* valid, int n, double* out,
                           cudaStream_t st);
 

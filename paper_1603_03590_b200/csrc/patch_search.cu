@@ -115,10 +115,11 @@ __global__ void __launch_bounds__(128) k_patch_prep(SearchArgs a, double* __rest
   if (a.cu) {
     const size_t cplane = (size_t)a.Wc * a.Hc;
     const double half = 0.5 * ps;
-    const double xs = ((double)x0i + half) / 2.0;
-    const double ys = ((double)y0i + half) / 2.0;
-    u0 = bilin_np(a.cu + b * cplane, a.Wc, a.Hc, xs, ys) * 2.0;
-    v0 = bilin_np(a.cv + b * cplane, a.Wc, a.Hc, xs, ys) * 2.0;
+    const double k = (double)a.ds;
+    const double xs = ((double)x0i + half) / k;
+    const double ys = ((double)y0i + half) / k;
+    u0 = bilin_np(a.cu + b * cplane, a.Wc, a.Hc, xs, ys) * k;
+    v0 = bilin_np(a.cv + b * cplane, a.Wc, a.Hc, xs, ys) * k;
   }
 
   // ---- _patch_precompute (inverse_search.py:75-98) ----

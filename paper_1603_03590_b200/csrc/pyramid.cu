@@ -109,6 +109,53 @@ __global__ void k_downsample(const double* __restrict__ in, int B, int H, int W,
   }
 }
 
+// numpy's pairwise_sum of n contiguous values (the inner loop of np.add's
+// reduction, numpy/_core/src/umath/loops_utils.h.src) for n <= 128: n < 8
+// sequential from 0.0; else eight strided accumulators combined
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the remainder
+template <typename T>
+__device__ __forceinline__ double np_pairwise_sum(const T* a, int n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; ++i) res += to_f64(a[i]);
+    return res;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = to_f64(a[j]);
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] += to_f64(a[i + j]);
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < n; ++i) res += to_f64(a[i]);
+  return res;
+}
+
+// _box_downsample by a factor k != 2 (core.py:88-98):
+// crop.reshape(h, k, w, k).mean(axis=(1, 3)) = (sum over the k block rows,
+// in order from 0, of each row's pairwise sum) / (k*k) — numpy 2.3's order,
+// pinned by tests/test_downscale.py against the reference (k = 3, 4, 8, 9).
+// T = the frame type for level 1 from the frames, double otherwise.
+template <typename T>
+__global__ void __launch_bounds__(256) k_downsample_k(const T* __restrict__ in, int B, int H,
+                                                      int W, int k, double* __restrict__ out) {
+  const int Ho = H / k, Wo = W / k;
+  const size_t n = (size_t)B * Ho * Wo;
+  const double kk = (double)k * (double)k;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int X = (int)(i % Wo);
+    const size_t t = i / Wo;
+    const int Y = (int)(t % Ho);
+    const int b = (int)(t / Ho);
+    const T* blk = in + ((size_t)b * H + (size_t)k * Y) * W + (size_t)k * X;
+    double acc = 0.0;
+    for (int r = 0; r < k; ++r) acc += np_pairwise_sum(blk + (size_t)r * W, k);
+    out[i] = acc / kk;
+  }
+}
+
 // gradient of a raster along x / y with the reference's border rules
 struct RowGrad {
   const double* img;
@@ -598,11 +645,52 @@ static void launch_pyramid_fused_t(PyrArgs& a, int nf, int coarsest, cudaStream_
   prof_end(KC_PYRAMID, st);
 }
 
+// pyramid factor k != 2: a box-mean launch per level and frame (the first
+// from the frames, after a finiteness pass over them when level 0 is not
+// stored), then every level's gradients in one launch
+template <typename T>
+static void launch_pyramid_k_t(PyrArgs& a, int nf, int coarsest, int k, cudaStream_t st) {
+  prof_begin(KC_PYRAMID, st);
+  const int TH = 256;
+  for (int f = 0; f < nf; ++f) {
+    const T* fr = static_cast<const T*>(a.frames[f]);
+    const size_t n0 = (size_t)a.B * a.H * a.W;
+    k_level0<T><<<grid_for(n0, TH), TH, 0, st>>>(fr, a.B, a.H, a.W, a.img[f][0], a.status);
+    note_launch();
+    for (int s = 1; s <= coarsest; ++s) {
+      const size_t n = (size_t)a.B * a.Hs[s] * a.Ws[s];
+      if (s == 1 && a.img[f][0] == nullptr)
+        k_downsample_k<T><<<grid_for(n, TH), TH, 0, st>>>(fr, a.B, a.H, a.W, k, a.img[f][1]);
+      else
+        k_downsample_k<double><<<grid_for(n, TH), TH, 0, st>>>(a.img[f][s - 1], a.B,
+                                                               a.Hs[s - 1], a.Ws[s - 1], k,
+                                                               a.img[f][s]);
+      note_launch();
+    }
+  }
+  a.g0 = a.L0;
+  a.g1 = coarsest;
+  int tiles = 0;
+  bool any = false;
+  for (int s = a.g0; s <= a.g1; ++s) {
+    const int t = ((a.Ws[s] + 63) / 64) * ((a.Hs[s] + 7) / 8);
+    tiles = t > tiles ? t : tiles;
+    for (int f = 0; f < nf; ++f) any |= a.gx[f][s] || a.gy[f][s];
+  }
+  if (any) {
+    dim3 gg((unsigned)tiles, (unsigned)(a.g1 - a.g0 + 1), (unsigned)(nf * a.B));
+    k_pyr_grad<<<gg, 256, 0, st>>>(a);
+    note_launch();
+  }
+  prof_end(KC_PYRAMID, st);
+}
+
 // both frames (f2 may be null: one frame); img[f][s] needed for s >= L0
 // (L0 = 0 when img[f][0] is requested, else 1); gx/gy where non-null
 void launch_pyramid_pair(const void* f1, const void* f2, int dtype, int B, int H, int W,
-                         int coarsest, double* const (*img)[32], double* const (*gx)[32],
-                         double* const (*gy)[32], uint32_t* status, cudaStream_t st) {
+                         int coarsest, int downscale, double* const (*img)[32],
+                         double* const (*gx)[32], double* const (*gy)[32], uint32_t* status,
+                         cudaStream_t st) {
   PyrArgs a{};
   const int nf = f2 ? 2 : 1;
   a.frames[0] = f1;
@@ -611,9 +699,10 @@ void launch_pyramid_pair(const void* f1, const void* f2, int dtype, int B, int H
   a.H = H;
   a.W = W;
   a.L0 = (img[0][0] != nullptr || coarsest == 0) ? 0 : 1;
+  const int k = downscale;
   for (int s = 0; s <= coarsest && s < 32; ++s) {
-    a.Ws[s] = W >> s;
-    a.Hs[s] = H >> s;
+    a.Ws[s] = s ? a.Ws[s - 1] / k : W;
+    a.Hs[s] = s ? a.Hs[s - 1] / k : H;
     for (int f = 0; f < nf; ++f) {
       a.img[f][s] = img[f][s];
       a.gx[f][s] = gx[f][s];
@@ -621,6 +710,20 @@ void launch_pyramid_pair(const void* f1, const void* f2, int dtype, int B, int H
     }
   }
   a.status = status;
+  if (k != 2) {
+    switch (dtype) {
+      case DIS_DTYPE_F32:
+        launch_pyramid_k_t<float>(a, nf, coarsest, k, st);
+        break;
+      case DIS_DTYPE_F64:
+        launch_pyramid_k_t<double>(a, nf, coarsest, k, st);
+        break;
+      default:
+        launch_pyramid_k_t<uint8_t>(a, nf, coarsest, k, st);
+        break;
+    }
+    return;
+  }
   switch (dtype) {
     case DIS_DTYPE_F32:
       launch_pyramid_fused_t<float>(a, nf, coarsest, st);
@@ -635,7 +738,7 @@ void launch_pyramid_pair(const void* f1, const void* f2, int dtype, int B, int H
 }
 
 template <typename T>
-static void launch_pyramid_t(const T* frames, int B, int H, int W, int coarsest,
+static void launch_pyramid_t(const T* frames, int B, int H, int W, int coarsest, int k,
                              double* const* img, double* const* gx, double* const* gy,
                              double* const* dd, uint32_t* status, cudaStream_t st) {
   const int TH = 256;
@@ -647,9 +750,26 @@ static void launch_pyramid_t(const T* frames, int B, int H, int W, int coarsest,
     k_level0<T><<<grid_for(n0, TH), TH, 0, st>>>(frames, B, H, W, img[0], status);
     note_launch();
   }
+  if (k != 2 && img[0] == nullptr && coarsest > 0) {  // finiteness pass over the frames
+    k_level0<T><<<grid_for((size_t)B * H * W, TH), TH, 0, st>>>(frames, B, H, W, nullptr,
+                                                                status);
+    note_launch();
+  }
+  int hl[32], wl[32];
+  hl[0] = H;
+  wl[0] = W;
   for (int s = 1; s <= coarsest; ++s) {
-    const int ho = h / 2, wo = w / 2;
-    if (s == 1 && img[0] == nullptr) {
+    const int ho = h / k, wo = w / k;
+    hl[s] = ho;
+    wl[s] = wo;
+    if (k != 2) {
+      if (s == 1 && img[0] == nullptr)
+        k_downsample_k<T><<<grid_for((size_t)B * ho * wo, TH), TH, 0, st>>>(frames, B, h, w, k,
+                                                                            img[1]);
+      else
+        k_downsample_k<double><<<grid_for((size_t)B * ho * wo, TH), TH, 0, st>>>(
+            img[s - 1], B, h, w, k, img[s]);
+    } else if (s == 1 && img[0] == nullptr) {
       dim3 g((unsigned)((wo + 63) / 64), (unsigned)((ho + 7) / 8), (unsigned)B);
       k_level1_checked<T><<<g, TH, 0, st>>>(frames, H, W, img[1], status);
     } else {
@@ -660,9 +780,9 @@ static void launch_pyramid_t(const T* frames, int B, int H, int W, int coarsest,
     h = ho;
     w = wo;
   }
-  h = H;
-  w = W;
   for (int s = 0; s <= coarsest; ++s) {
+    h = hl[s];
+    w = wl[s];
     if (gx[s] || gy[s] || (dd && dd[s])) {
       dim3 g((unsigned)((w + kGTX - 1) / kGTX), (unsigned)((h + kGTY - 1) / kGTY), (unsigned)B);
       if (dd && dd[s]) {
@@ -673,14 +793,12 @@ static void launch_pyramid_t(const T* frames, int B, int H, int W, int coarsest,
       }
       note_launch();
     }
-    h /= 2;
-    w /= 2;
   }
   prof_end(KC_PYRAMID, st);
 }
 
 void launch_pyramid(const void* frames, int dtype, int B, int H, int W, int coarsest,
-                    double* const* img, double* const* gx, double* const* gy,
+                    int downscale, double* const* img, double* const* gx, double* const* gy,
                     double* const* dd, uint32_t* status, cudaStream_t st) {
   bool want_dd = false;
   for (int s = 0; s <= coarsest; ++s) want_dd |= dd && dd[s];
@@ -693,19 +811,22 @@ void launch_pyramid(const void* frames, int dtype, int B, int H, int W, int coar
       x[0][s] = gx ? gx[s] : nullptr;
       y[0][s] = gy ? gy[s] : nullptr;
     }
-    launch_pyramid_pair(frames, nullptr, dtype, B, H, W, coarsest, im, x, y, status, st);
+    launch_pyramid_pair(frames, nullptr, dtype, B, H, W, coarsest, downscale, im, x, y, status,
+                        st);
     return;
   }
   switch (dtype) {
     case DIS_DTYPE_F32:
-      launch_pyramid_t((const float*)frames, B, H, W, coarsest, img, gx, gy, dd, status, st);
+      launch_pyramid_t((const float*)frames, B, H, W, coarsest, downscale, img, gx, gy, dd,
+                       status, st);
       break;
     case DIS_DTYPE_F64:
-      launch_pyramid_t((const double*)frames, B, H, W, coarsest, img, gx, gy, dd, status, st);
+      launch_pyramid_t((const double*)frames, B, H, W, coarsest, downscale, img, gx, gy, dd,
+                       status, st);
       break;
     default:
-      launch_pyramid_t((const uint8_t*)frames, B, H, W, coarsest, img, gx, gy, dd, status,
-                       st);
+      launch_pyramid_t((const uint8_t*)frames, B, H, W, coarsest, downscale, img, gx, gy, dd,
+                       status, st);
       break;
   }
 }

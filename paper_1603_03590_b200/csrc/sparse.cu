@@ -29,13 +29,15 @@ __global__ void __launch_bounds__(128) k_sparse_chain(SparseChainArgs a) {
   double* sdy = sdx + nn;
   const double sx = a.seeds[2 * i], sy = a.seeds[2 * i + 1];
   double u = 0.0, v = 0.0;
-  for (int s = a.coarsest; s >= a.finest; --s) {
+  const double kd = (double)a.ds;
+  double scale = 1.0;  // params.downscale ** s (pipeline.py:213), exact
+  for (int s = 0; s < a.coarsest; ++s) scale *= kd;
+  for (int s = a.coarsest; s >= a.finest; --s, scale /= kd) {
     const int W = a.W[s], H = a.H[s];
     const double* __restrict__ img = a.img[s];
     const double* __restrict__ gx = a.gx[s];
     const double* __restrict__ gy = a.gy[s];
     const double* __restrict__ q = a.qry[s];
-    const double scale = (double)(1 << s);
     // pipeline.py:215-218
     double x0 = sx / scale - 0.5 * ps;
     double y0 = sy / scale - 0.5 * ps;
@@ -77,8 +79,8 @@ __global__ void __launch_bounds__(128) k_sparse_chain(SparseChainArgs a) {
     const double i01 = valid ? -h01 / det : 0.0;
     const double i11 = valid ? h00 / det : 0.0;
     // _patch_optimize (inverse_search.py:113-189)
-    const double u0 = s == a.coarsest ? 0.0 : u * 2.0;
-    const double v0 = s == a.coarsest ? 0.0 : v * 2.0;
+    const double u0 = s == a.coarsest ? 0.0 : u * kd;  // init_displacement * downscale
+    const double v0 = s == a.coarsest ? 0.0 : v * kd;
     u = u0;
     v = v0;
     double prev_ssd = 1e300, prev_u = u, prev_v = v;
@@ -125,20 +127,20 @@ __global__ void __launch_bounds__(128) k_sparse_chain(SparseChainArgs a) {
       }
     }
   }
-  const double f = (double)(1 << a.finest);
+  double f = 1.0;  // params.downscale ** finest_scale (pipeline.py:231)
+  for (int s = 0; s < a.finest; ++s) f *= kd;
   a.out[2 * i] = u * f;
   a.out[2 * i + 1] = v * f;
 }
 
 __global__ void __launch_bounds__(128) k_sparse_sample(const double* __restrict__ fu,
                                                        const double* __restrict__ fv, int W,
-                                                       int H, int finest,
+                                                       int H, double scale,
                                                        const double* __restrict__ seeds,
                                                        const uint8_t* __restrict__ valid, int n,
                                                        double* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n || !valid[i]) return;
-  const double scale = (double)(1 << finest);
   const double gx = seeds[2 * i] / scale, gy = seeds[2 * i + 1] / scale;
   out[2 * i] = bilin_np(fu, W, H, gx, gy) * scale;
   out[2 * i + 1] = bilin_np(fv, W, H, gx, gy) * scale;
@@ -149,10 +151,10 @@ void launch_sparse_chain(const SparseChainArgs& a, cudaStream_t st) {
   note_launch();
 }
 
-void launch_sparse_sample(const double* fu, const double* fv, int W, int H, int finest,
+void launch_sparse_sample(const double* fu, const double* fv, int W, int H, double scale,
                           const double* seeds, const uint8_t* valid, int n, double* out,
                           cudaStream_t st) {
-  k_sparse_sample<<<(n + 127) / 128, 128, 0, st>>>(fu, fv, W, H, finest, seeds, valid, n, out);
+  k_sparse_sample<<<(n + 127) / 128, 128, 0, st>>>(fu, fv, W, H, scale, seeds, valid, n, out);
   note_launch();
 }
 

@@ -1,5 +1,6 @@
-// upsample.cu — upsample_flow (core.py:178-190) by the factor 2:
-//   out(x, y) = 2 * bilinear_map(flow, x / 2, y / 2)  (numpy bilinear form)
+// upsample.cu — upsample_flow (core.py:178-190) by the pyramid factor k
+// (DisParams.downscale, 2 on the benchmark configs):
+//   out(x, y) = k * bilinear_map(flow, x / k, y / k)  (numpy bilinear form)
 // applied level by level (_upscale_to_full, pipeline.py:129-133), plus the
 // planar -> (H, W, 2) interleave of the final field.  HBM-bound gathers.
 #include "common.cuh"
@@ -11,9 +12,9 @@ namespace disb200 {
 // clamp/floor/fraction setup, then the numpy formula for each component
 __device__ __forceinline__ void upsample_px(const double* __restrict__ U,
                                             const double* __restrict__ V, int W, int H, int x,
-                                            int y, double& u, double& v) {
-  double xs = (double)x / 2.0;
-  double ys = (double)y / 2.0;
+                                            int y, double k, double& u, double& v) {
+  double xs = (double)x / k;
+  double ys = (double)y / k;
   xs = xs > W - 1.0 ? W - 1.0 : xs;
   ys = ys > H - 1.0 ? H - 1.0 : ys;
   const int x0 = (int)xs, y0 = (int)ys;  // xs, ys >= 0: floor
@@ -26,8 +27,8 @@ __device__ __forceinline__ void upsample_px(const double* __restrict__ U,
   const double ub = __ldg(U + r1 + x0) * gx + __ldg(U + r1 + x1) * fx;
   const double vt = __ldg(V + r0 + x0) * gx + __ldg(V + r0 + x1) * fx;
   const double vb = __ldg(V + r1 + x0) * gx + __ldg(V + r1 + x1) * fx;
-  u = (ut * gy + ub * fy) * 2.0;
-  v = (vt * gy + vb * fy) * 2.0;
+  u = (ut * gy + ub * fy) * k;
+  v = (vt * gy + vb * fy) * k;
 }
 
 // Two horizontally adjacent output pixels per thread (x = 2i, 2i + 1 share
@@ -37,7 +38,8 @@ __global__ void __launch_bounds__(256) k_upsample(const double* __restrict__ iu,
                                                   const double* __restrict__ iv, int W, int H,
                                                   double* __restrict__ ou,
                                                   double* __restrict__ ov,
-                                                  double* __restrict__ oi, int Wn, int Hn) {
+                                                  double* __restrict__ oi, int Wn, int Hn,
+                                                  double k) {
   const int b = blockIdx.z;
   const int x = 2 * (blockIdx.x * 32 + (threadIdx.x & 31));
   const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
@@ -47,10 +49,10 @@ __global__ void __launch_bounds__(256) k_upsample(const double* __restrict__ iu,
   const double* V = iv + b * plane;
   const size_t g = ((size_t)b * Hn + y) * Wn + x;
   double u0, v0;
-  upsample_px(U, V, W, H, x, y, u0, v0);
+  upsample_px(U, V, W, H, x, y, k, u0, v0);
   if (x + 1 < Wn) {
     double u1, v1;
-    upsample_px(U, V, W, H, x + 1, y, u1, v1);
+    upsample_px(U, V, W, H, x + 1, y, k, u1, v1);
     if (oi) {
       double* d = oi + 2 * g;
       if ((reinterpret_cast<uintptr_t>(d) & 31) == 0) {  // streamed: not re-read
@@ -90,10 +92,11 @@ static unsigned blocks_for(size_t n) {
 }
 
 void launch_upsample(const double* iu, const double* iv, int B, int W, int H, double* ou,
-                     double* ov, double* out_interleaved, int Wn, int Hn, cudaStream_t st) {
+                     double* ov, double* out_interleaved, int Wn, int Hn, int factor,
+                     cudaStream_t st) {
   prof_begin(KC_UPSAMPLE, st);
   dim3 g((unsigned)((Wn + 63) / 64), (unsigned)((Hn + 7) / 8), (unsigned)B);
-  k_upsample<<<g, 256, 0, st>>>(iu, iv, W, H, ou, ov, out_interleaved, Wn, Hn);
+  k_upsample<<<g, 256, 0, st>>>(iu, iv, W, H, ou, ov, out_interleaved, Wn, Hn, (double)factor);
   prof_end(KC_UPSAMPLE, st);
   note_launch();
 }

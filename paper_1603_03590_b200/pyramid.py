@@ -80,8 +80,6 @@ def build_pyramid(img, coarsest_scale: int, downscale: int = 2) -> ImagePyramid:
         raise ParameterError("coarsest_scale must be >= 0")
     if downscale < 2 or int(downscale) != downscale:
         raise ParameterError("downscale must be an integer >= 2")
-    if downscale != 2:
-        raise ParameterError("this path implements downscale == 2 only")
     shape = tuple(img.shape)
     if len(shape) != 2 or shape[0] < 1 or shape[1] < 1:
         raise ValueError(f"image must be 2D and non-empty, got shape {shape}")
@@ -90,10 +88,10 @@ def build_pyramid(img, coarsest_scale: int, downscale: int = 2) -> ImagePyramid:
     from . import stages
 
     lv = stages.build_pyramid(_to_device_frames(img, torch.device("cuda")), int(coarsest_scale),
-                              finest=0, second_derivatives=False)
+                              finest=0, second_derivatives=False, downscale=int(downscale))
     levels = tuple(PyramidLevel(d["img"][0], d["gx"][0], d["gy"][0], s)
                    for s, d in enumerate(lv))
-    return ImagePyramid(levels, 2)
+    return ImagePyramid(levels, int(downscale))
 
 
 def image_gradients(img):
@@ -105,17 +103,15 @@ def image_gradients(img):
 
 def upsample_flow(flow, new_width: int, new_height: int, scale_factor: int):
     """output(x) = scale * flow(x / scale), bilinear_map form (core.py:178-190),
-    on the GPU (``dis_upsample_flow``); this path implements scale 2."""
+    on the GPU (``dis_upsample_flow``)."""
     from . import stages
     from .pipeline import _require_cuda
 
     torch = _require_cuda()
-    if scale_factor != 2:
-        raise ParameterError("this path implements downscale == 2 only")
     f = np.asarray(flow, dtype=np.float64)
     u = torch.from_numpy(np.ascontiguousarray(f[None, :, :, 0])).cuda()
     v = torch.from_numpy(np.ascontiguousarray(f[None, :, :, 1])).cuda()
-    ou, ov = stages.upsample_flow(u, v, int(new_width), int(new_height))
+    ou, ov = stages.upsample_flow(u, v, int(new_width), int(new_height), int(scale_factor))
     return np.stack([ou[0].cpu().numpy(), ov[0].cpu().numpy()], axis=-1)
 
 
@@ -141,6 +137,11 @@ def dis_flow_on_pyramids(pyr_ref, pyr_qry, params: DisParams, threads: int = 1):
         raise ValueError(f"frame dimensions differ: {tuple(pyr_ref[0].image.shape)[::-1]} vs "
                          f"{tuple(pyr_qry[0].image.shape)[::-1]}")
     ss = params.coarsest_scale
+    for pyr in (pyr_ref, pyr_qry):
+        k = getattr(pyr, "downscale", params.downscale)
+        if int(k) != int(params.downscale):
+            raise ValueError(f"pyramid factor {k} differs from params.downscale "
+                             f"{params.downscale}; this path uses one factor for both")
     if len(pyr_ref) <= ss or len(pyr_qry) <= ss:
         raise IndexError("pyramid has fewer levels than coarsest_scale + 1")
     coarse = pyr_ref[ss]

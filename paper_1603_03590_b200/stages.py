@@ -37,7 +37,7 @@ def grid_axis(dim: int, patch_size: int, overlap: float) -> np.ndarray:
 
 
 def build_pyramid(frames, coarsest: int, finest: int = 0, second_derivatives: bool = True,
-                  level0: bool = True):
+                  level0: bool = True, downscale: int = 2):
     """build_pyramid (core.py:106-128) for a batch of frames: list over levels
     0..coarsest of dicts {img, gx, gy, dd}; gradients only for levels
     >= finest (dd = (B, 4, H, W): gxx, gxy, gyx, gyy).  ``level0=False``
@@ -49,8 +49,10 @@ def build_pyramid(frames, coarsest: int, finest: int = 0, second_derivatives: bo
         f = f.unsqueeze(0)
     B, H, W = f.shape
     levels = []
+    h, w = H, W
     for s in range(coarsest + 1):
-        h, w = H >> s, W >> s
+        if s:
+            h, w = h // downscale, w // downscale
         lv = {}
         if s > 0 or level0 or finest == 0:
             lv["img"] = torch.empty((B, h, w), dtype=torch.float64, device=f.device)
@@ -67,7 +69,8 @@ def build_pyramid(frames, coarsest: int, finest: int = 0, second_derivatives: bo
     dd = arr(*[lv["dd"].data_ptr() if "dd" in lv else None for lv in levels])
     status = torch.zeros(1, dtype=torch.int32, device=f.device)
     _lib.check(_lib.lib().dis_build_pyramid(f.data_ptr(), _dtype_code(f), B, H, W, coarsest,
-                                            img, gx, gy, dd, status.data_ptr(), _cur(f)))
+                                            int(downscale), img, gx, gy, dd, status.data_ptr(),
+                                            _cur(f)))
     if int(status.item()) != 0:
         raise ValueError("image contains non-finite values")
     return levels
@@ -142,15 +145,16 @@ def refine(fu, fv, ref: dict, qry: dict, params: DisParams, outer: int):
     return u, v
 
 
-def upsample_flow(fu, fv, new_width: int, new_height: int):
-    """upsample_flow by 2 (core.py:178-190) -> (u, v) (B, new_height, new_width)."""
+def upsample_flow(fu, fv, new_width: int, new_height: int, scale_factor: int = 2):
+    """upsample_flow (core.py:178-190) by ``scale_factor`` -> (u, v)
+    (B, new_height, new_width)."""
     torch = _require_cuda()
     B, H, W = fu.shape
     ou = torch.empty((B, new_height, new_width), dtype=torch.float64, device=fu.device)
     ov = torch.empty_like(ou)
     _lib.check(_lib.lib().dis_upsample_flow(fu.data_ptr(), fv.data_ptr(), B, W, H,
                                             ou.data_ptr(), ov.data_ptr(), new_width,
-                                            new_height, _cur(fu)))
+                                            new_height, int(scale_factor), _cur(fu)))
     return ou, ov
 
 
