@@ -296,6 +296,59 @@ DIS_API int dis_upsample_flow(const double* in_u, const double* in_v, int32_t B,
                       int32_t W, int32_t H, double* out_u, double* out_v,
                       int32_t Wn, int32_t Hn, int32_t scale_factor, void* stream);
 
+/* ---- the reference's inverse-search stage functions on materialised
+ * per-patch arrays (device memory; one level, n patches; the flow path fuses
+ * these inside dis_patch_search) -------------------------------------------
+ * precompute_patch_set (inverse_search.py:306-341): window origins x_starts,
+ * y_starts (n, real coordinates) -> templates, steep_x, steep_y (n, ps*ps),
+ * template_mean (n), hessian / hessian_inv (n, 3 packed [00, 01, 11]) and
+ * valid (n, uint8) from _patch_precompute (75-98) and _condition_hessians
+ * (255-276; horizontal_only = the stereo form 259-264). */
+DIS_API int dis_precompute_patch_set(const double* img, const double* gx, const double* gy,
+                                     int32_t W, int32_t H, const double* x_starts,
+                                     const double* y_starts, int32_t n, int32_t patch_size,
+                                     int32_t horizontal_only, double* templates,
+                                     double* steep_x, double* steep_y, double* template_mean,
+                                     double* hessian, double* hessian_inv, uint8_t* valid,
+                                     void* stream);
+
+/* optimize_patch_set (inverse_search.py:344-371): _patch_optimize (113-189)
+ * for every patch from init_displacement (n, 2) -> displacement (n, 2),
+ * offset (n), mean_abs_residual (n).  residual_norm: DIS_NORM_*. */
+DIS_API int dis_optimize_patch_set(const double* qry, int32_t W, int32_t H,
+                                   const double* x_starts, const double* y_starts, int32_t n,
+                                   int32_t patch_size, const double* templates,
+                                   const double* steep_x, const double* steep_y,
+                                   const double* hessian_inv, const double* template_mean,
+                                   const uint8_t* valid, const double* init_displacement,
+                                   int32_t iterations, int32_t mean_normalization,
+                                   int32_t residual_norm, double huber_b, double* displacement,
+                                   double* offset, double* mean_abs_residual, void* stream);
+
+/* refresh_patch_stats (inverse_search.py:374-387, _window_stats 227-248):
+ * offset and mean_abs_residual of the selected patches (select, n uint8) at
+ * their displacement (n, 2); the others are left untouched. */
+DIS_API int dis_refresh_patch_stats(const double* qry, int32_t W, int32_t H,
+                                    const double* x_starts, const double* y_starts, int32_t n,
+                                    int32_t patch_size, const double* templates,
+                                    const double* template_mean, const uint8_t* select,
+                                    const double* displacement, int32_t mean_normalization,
+                                    double* offset, double* mean_abs_residual, void* stream);
+
+/* init_patches (densification.py:82-95): the coarser field (Hc x Wc x 2
+ * interleaved, or NULL = zeros) sampled with bilinear_map at centers (n, 2)
+ * / downscale, times downscale -> init_out (n, 2). */
+DIS_API int dis_init_patches(const double* coarser_flow, int32_t Wc, int32_t Hc,
+                             const double* centers, int32_t n, int32_t downscale,
+                             double* init_out, void* stream);
+
+/* reset_outliers (densification.py:98-107): out = init where
+ * hypot(displacement - init) > patch_size (correctly rounded), else
+ * displacement; was_reset (optional, n uint8) marks the reset patches. */
+DIS_API int dis_reset_outliers(const double* displacement, const double* init_displacement,
+                               int32_t n, int32_t patch_size, double* out, uint8_t* was_reset,
+                               void* stream);
+
 /* compose_flows (pipeline.py:186-199): out(x) = ab(x) + bc(x + ab(x)) with
  * bc sampled by bilinear_map (core.py:154-170).  B fields, each H x W x 2
  * float64 interleaved (u, v), device memory; `out` must not alias the

@@ -464,6 +464,64 @@ def gen_downscale():
     save("downscale.npz", **d)
 
 
+def gen_stage_search():
+    """The inverse-search stage functions (inverse_search.py:306-494) at real
+    (non-grid) window origins, all three residual norms, with and without
+    mean normalisation, plus refresh_patch_stats on a selection and the
+    single-patch interface."""
+    f1, f2, _ = synth.make_pair(50, 96, 160, 4.0, True, 4.0)
+    lv1 = core.build_pyramid(f1, 0)[0]
+    lv2 = core.build_pyramid(f2, 0)[0]
+    rng = np.random.default_rng(51)
+    n = 300
+    xs = rng.uniform(-3.0, 160.0 - 6.0, n)
+    ys = rng.uniform(-3.0, 96.0 - 6.0, n)
+    xs[:10] = np.floor(xs[:10])  # some integer origins too
+    d = dict(f1=f1, f2=f2, xs=xs, ys=ys)
+    for ps in (8, 12):
+        for hz in (False, True):
+            pset = inverse_search.precompute_patch_set(lv1, xs, ys, ps, horizontal_only=hz)
+            tag = f"ps{ps}_{'h' if hz else 'f'}"
+            d[f"{tag}_tmpl"] = pset.templates
+            d[f"{tag}_sdx"] = pset.steep_x
+            d[f"{tag}_sdy"] = pset.steep_y
+            d[f"{tag}_hess"] = pset.hessian
+            d[f"{tag}_hinv"] = pset.hessian_inv
+            d[f"{tag}_mean"] = pset.template_mean
+            d[f"{tag}_valid"] = pset.valid
+    init = rng.normal(0, 1.5, (n, 2))
+    d["init"] = init
+    for norm in ("l2", "l1", "huber"):
+        for mn in (True, False):
+            pset = inverse_search.precompute_patch_set(lv1, xs, ys, 8)
+            pset.init_displacement = init.copy()
+            inverse_search.optimize_patch_set(pset, lv2, 24, residual_norm=norm, huber_b=2.0,
+                                              mean_normalization=mn)
+            tag = f"opt_{norm}_{int(mn)}"
+            d[f"{tag}_disp"] = pset.displacement.copy()
+            d[f"{tag}_off"] = pset.offset.copy()
+            d[f"{tag}_mar"] = pset.mean_abs_residual.copy()
+            if norm == "l2" and mn:
+                sel = rng.uniform(0, 1, n) < 0.3
+                kept = densification.reset_outliers(pset.displacement, init, 8)
+                pset.displacement = kept
+                inverse_search.refresh_patch_stats(pset, lv2, sel, True)
+                d["refresh_sel"] = sel
+                d["refresh_disp"] = kept
+                d["refresh_off"] = pset.offset.copy()
+                d["refresh_mar"] = pset.mean_abs_residual.copy()
+    st = inverse_search.precompute_patch(lv1, (70.3, 40.8), 8)
+    st = dataclasses.replace(st, init_displacement=np.array([1.25, -0.5]))
+    out = inverse_search.optimize_patch(st, lv2, 32, residual_norm="huber", huber_b=1.5)
+    d["single_tmpl"] = st.template
+    d["single_sd"] = st.steepest_descent
+    d["single_hinv"] = st.hessian_inverse
+    d["single_disp"] = out.displacement
+    d["single_off"] = np.array(out.mean_offset)
+    d["single_mar"] = np.array(out.mean_abs_residual)
+    save("stage_search.npz", **d)
+
+
 def gen_flowio():
     """flowio.py: .flo bytes written by the reference, images decoded by it
     (P5 8/16-bit with header comments, P6 luminance), written PGM/PPM bytes."""
@@ -511,7 +569,8 @@ def gen_flowio():
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     which = sys.argv[1:] or ["pyramid", "samplers", "search", "refine", "e2e", "full",
-                             "compose", "stereo", "bidir", "sparse", "flowio", "downscale"]
+                             "compose", "stereo", "bidir", "sparse", "flowio", "downscale",
+                             "stage_search"]
     pipeline.warmup()
     if "pyramid" in which:
         gen_pyramid()
@@ -537,3 +596,5 @@ if __name__ == "__main__":
         gen_flowio()
     if "downscale" in which:
         gen_downscale()
+    if "stage_search" in which:
+        gen_stage_search()

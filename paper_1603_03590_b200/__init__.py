@@ -34,6 +34,15 @@ from .densification import (
     reset_outliers,
 )
 from .variational import refine
+from .inverse_search import (
+    PatchSet,
+    PatchState,
+    optimize_patch,
+    optimize_patch_set,
+    precompute_patch,
+    precompute_patch_set,
+    refresh_patch_stats,
+)
 from .pipeline import (
     FlowEngine,
     SparseMatch,
@@ -75,4 +84,11 @@ __all__ = [
     "init_patches",
     "reset_outliers",
     "refine",
+    "PatchSet",
+    "PatchState",
+    "precompute_patch_set",
+    "optimize_patch_set",
+    "refresh_patch_stats",
+    "precompute_patch",
+    "optimize_patch",
 ]

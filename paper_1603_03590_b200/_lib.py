@@ -42,6 +42,8 @@ EXPORTED = (
     "dis_stereo_batch_host", "dis_densify_bidirectional",
     "dis_densify_bidirectional_workspace_bytes", "dis_sparse_workspace_bytes",
     "dis_sparse_correspondences", "dis_flow_batch_levels", "dis_profile_log",
+    "dis_precompute_patch_set", "dis_optimize_patch_set", "dis_refresh_patch_stats",
+    "dis_init_patches", "dis_reset_outliers",
 )
 
 KERNEL_CLASSES = ("pyramid", "patch_search", "densify", "tensor_assemble", "sor", "upsample")
@@ -114,6 +116,19 @@ def lib() -> ctypes.CDLL:
     L.dis_sparse_correspondences.argtypes = [_vp, _vp, _i32, _i32, _i32, _pp, _vp, _i32, _vp,
                                              _vp, _vp, _sz, _vp]
     L.dis_sparse_correspondences.restype = ctypes.c_int
+    L.dis_precompute_patch_set.argtypes = [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _i32, _i32,
+                                           _i32] + [_vp] * 8
+    L.dis_precompute_patch_set.restype = ctypes.c_int
+    L.dis_optimize_patch_set.argtypes = [_vp, _i32, _i32, _vp, _vp, _i32, _i32] + [_vp] * 7 + [
+        _i32, _i32, _i32, ctypes.c_double, _vp, _vp, _vp, _vp]
+    L.dis_optimize_patch_set.restype = ctypes.c_int
+    L.dis_refresh_patch_stats.argtypes = [_vp, _i32, _i32, _vp, _vp, _i32, _i32, _vp, _vp, _vp,
+                                          _vp, _i32, _vp, _vp, _vp]
+    L.dis_refresh_patch_stats.restype = ctypes.c_int
+    L.dis_init_patches.argtypes = [_vp, _i32, _i32, _vp, _i32, _i32, _vp, _vp]
+    L.dis_init_patches.restype = ctypes.c_int
+    L.dis_reset_outliers.argtypes = [_vp, _vp, _i32, _i32, _vp, _vp, _vp]
+    L.dis_reset_outliers.restype = ctypes.c_int
     L.dis_compose_flows.argtypes = [_vp, _vp, _i32, _i32, _i32, _vp, _vp]
     L.dis_compose_flows.restype = ctypes.c_int
     L.dis_grid_axis.argtypes = [_i32, _i32, ctypes.c_double, ctypes.POINTER(_i32), _i32]

@@ -1171,6 +1171,81 @@ int dis_patch_search(const double* ref_img, const double* ref_gx, const double* 
   return check_cuda("dis_patch_search");
 }
 
+// ---- the reference's inverse-search stage functions (inverse_search.py:306-387)
+// and init / reset (densification.py:82-107) on materialised arrays ----------
+
+int dis_precompute_patch_set(const double* img, const double* gx, const double* gy, int32_t W,
+                             int32_t H, const double* x_starts, const double* y_starts,
+                             int32_t n, int32_t patch_size, int32_t horizontal_only,
+                             double* templates, double* steep_x, double* steep_y,
+                             double* template_mean, double* hessian, double* hessian_inv,
+                             uint8_t* valid, void* stream) {
+  if (patch_size < 1) return fail(DIS_ERR_PARAMETER, "patch_size must be >= 1");
+  if (W < 1 || H < 1 || n < 0) return fail(DIS_ERR_VALUE, "bad level or patch count");
+  g_launches = 0;
+  if (n == 0) return DIS_OK;
+  launch_precompute_set(img, gx, gy, W, H, x_starts, y_starts, n, patch_size, horizontal_only,
+                        templates, steep_x, steep_y, template_mean, hessian, hessian_inv, valid,
+                        as_stream(stream));
+  return check_cuda("dis_precompute_patch_set");
+}
+
+int dis_optimize_patch_set(const double* qry, int32_t W, int32_t H, const double* x_starts,
+                           const double* y_starts, int32_t n, int32_t patch_size,
+                           const double* templates, const double* steep_x, const double* steep_y,
+                           const double* hessian_inv, const double* template_mean,
+                           const uint8_t* valid, const double* init_displacement,
+                           int32_t iterations, int32_t mean_normalization, int32_t residual_norm,
+                           double huber_b, double* displacement, double* offset,
+                           double* mean_abs_residual, void* stream) {
+  if (residual_norm < 0 || residual_norm > 2)
+    return fail(DIS_ERR_VALUE, "unknown residual norm code %d", residual_norm);
+  if (W < 1 || H < 1 || n < 0 || patch_size < 1)
+    return fail(DIS_ERR_VALUE, "bad level, patch size or patch count");
+  g_launches = 0;
+  if (n == 0) return DIS_OK;
+  launch_optimize_set(qry, W, H, x_starts, y_starts, n, patch_size, templates, steep_x, steep_y,
+                      hessian_inv, template_mean, valid, init_displacement, iterations,
+                      mean_normalization, residual_norm, huber_b, displacement, offset,
+                      mean_abs_residual, as_stream(stream));
+  return check_cuda("dis_optimize_patch_set");
+}
+
+int dis_refresh_patch_stats(const double* qry, int32_t W, int32_t H, const double* x_starts,
+                            const double* y_starts, int32_t n, int32_t patch_size,
+                            const double* templates, const double* template_mean,
+                            const uint8_t* select, const double* displacement,
+                            int32_t mean_normalization, double* offset,
+                            double* mean_abs_residual, void* stream) {
+  if (W < 1 || H < 1 || n < 0 || patch_size < 1)
+    return fail(DIS_ERR_VALUE, "bad level, patch size or patch count");
+  g_launches = 0;
+  if (n == 0) return DIS_OK;
+  launch_window_stats(qry, W, H, x_starts, y_starts, n, patch_size, templates, template_mean,
+                      select, displacement, mean_normalization, offset, mean_abs_residual,
+                      as_stream(stream));
+  return check_cuda("dis_refresh_patch_stats");
+}
+
+int dis_init_patches(const double* coarser_flow, int32_t Wc, int32_t Hc, const double* centers,
+                     int32_t n, int32_t downscale, double* init_out, void* stream) {
+  if (downscale < 1) return fail(DIS_ERR_PARAMETER, "downscale must be >= 1");
+  if (coarser_flow && (Wc < 1 || Hc < 1)) return fail(DIS_ERR_VALUE, "empty coarser field");
+  g_launches = 0;
+  if (n <= 0) return DIS_OK;
+  launch_init_patches(coarser_flow, Wc, Hc, centers, n, downscale, init_out, as_stream(stream));
+  return check_cuda("dis_init_patches");
+}
+
+int dis_reset_outliers(const double* displacement, const double* init_displacement, int32_t n,
+                       int32_t patch_size, double* out, uint8_t* was_reset, void* stream) {
+  g_launches = 0;
+  if (n <= 0) return DIS_OK;
+  launch_reset_outliers(displacement, init_displacement, n, patch_size, out, was_reset,
+                        as_stream(stream));
+  return check_cuda("dis_reset_outliers");
+}
+
 int dis_densify(const double* ref_img, const double* qry_img, int32_t B, int32_t W, int32_t H,
                 const dis_params_t* p, const double* patch_u, const double* patch_v,
                 const double* patch_off, double* flow_u, double* flow_v, uint32_t* status,

@@ -75,6 +75,26 @@ struct SearchArgs {
 size_t patch_search_scratch_bytes(int B, int P);
 void launch_patch_search(const SearchArgs& a, void* scratch, cudaStream_t st);
 
+// stage_search.cu — the reference's inverse-search / init / reset stage
+// functions on materialised per-patch arrays (one thread per patch)
+void launch_precompute_set(const double* img, const double* gx, const double* gy, int W, int H,
+                           const double* xs, const double* ys, int n, int ps, int horizontal,
+                           double* tmpl, double* sdx, double* sdy, double* mean_t, double* hess,
+                           double* hinv, uint8_t* valid, cudaStream_t st);
+void launch_optimize_set(const double* qry, int W, int H, const double* xs, const double* ys,
+                         int n, int ps, const double* tmpl, const double* sdx, const double* sdy,
+                         const double* hinv, const double* mean_t, const uint8_t* valid,
+                         const double* init, int iters, int mean_norm, int code, double hb,
+                         double* disp, double* offset, double* mar, cudaStream_t st);
+void launch_window_stats(const double* qry, int W, int H, const double* xs, const double* ys,
+                         int n, int ps, const double* tmpl, const double* mean_t,
+                         const uint8_t* sel, const double* disp, int mean_norm, double* offset,
+                         double* mar, cudaStream_t st);
+void launch_init_patches(const double* coarse, int Wc, int Hc, const double* centers, int n,
+                         int ds, double* init, cudaStream_t st);
+void launch_reset_outliers(const double* disp, const double* init, int n, int ps, double* out,
+                           uint8_t* was_reset, cudaStream_t st);
+
 // densify.cu
 void launch_densify(const double* ref, const double* qry, int B, int W, int H, GridAxis ax,
                     GridAxis ay, int ps, const double* pu, const double* pv,

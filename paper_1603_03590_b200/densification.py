@@ -1,11 +1,13 @@
 """Reference-signature stage functions of the densification module
 (reference densification.py): patch grids, per-scale initialisation,
 outlier reset and the weighted densification — numpy in, numpy out, the
-densification itself on the GPU through the C ABI (``dis_densify``,
+computation on the GPU through the C ABI (``dis_grid_axis``,
+``dis_init_patches``, ``dis_reset_outliers``, ``dis_densify``,
 ``dis_densify_bidirectional``).
 
 Same names, arguments and exceptions as the reference so its callers (and
-tests) run unchanged; bit-identical results (tests/test_stage_api_gpu.py).
+tests) run unchanged; bit-identical results (tests/test_stage_api.py,
+tests/test_stage_search_gpu.py).
 """
 
 from __future__ import annotations
@@ -14,6 +16,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import _lib
 from .params import DisParams
 
 
@@ -59,49 +62,46 @@ def create_grid(width: int, height: int, patch_size: int, overlap: float) -> Pat
     return PatchGrid(int(width), int(height), int(patch_size), spacing, xo, yo)
 
 
-def _bilinear_map(img, xs, ys):
-    """core.py:154-170 (numpy form) — host helper for init_patches."""
-    h, w = img.shape
-    x = np.clip(xs, 0.0, w - 1.0)
-    y = np.clip(ys, 0.0, h - 1.0)
-    x0 = np.floor(x).astype(np.int64)
-    y0 = np.floor(y).astype(np.int64)
-    x1 = np.minimum(x0 + 1, w - 1)
-    y1 = np.minimum(y0 + 1, h - 1)
-    fx = x - x0
-    fy = y - y0
-    top = img[y0, x0] * (1.0 - fx) + img[y0, x1] * fx
-    bot = img[y1, x0] * (1.0 - fx) + img[y1, x1] * fx
-    return top * (1.0 - fy) + bot * fy
-
-
 def init_patches(grid: PatchGrid, coarser_flow, downscale: int) -> np.ndarray:
     """Initial displacements (densification.py:82-95): zero at the coarsest
-    scale, else the coarser field at center / downscale, times downscale.
-    (The flow path computes this inside ``k_patch_prep``; this host form is
-    for stage-level callers.)"""
-    centers = grid.centers
+    scale, else the coarser field (bilinear_map) at center / downscale, times
+    downscale — on the GPU (``dis_init_patches``; the flow path computes the
+    same inside ``k_patch_prep``)."""
+    from .inverse_search import _dev, _stream, _torch
+
+    centers = np.ascontiguousarray(grid.centers, dtype=np.float64)
+    n = centers.shape[0]
     if coarser_flow is None:
-        return np.zeros((centers.shape[0], 2))
-    cf = np.asarray(coarser_flow, dtype=np.float64)
-    xs = centers[:, 0] / downscale
-    ys = centers[:, 1] / downscale
-    out = np.empty((centers.shape[0], 2))
-    out[:, 0] = _bilinear_map(cf[:, :, 0], xs, ys) * downscale
-    out[:, 1] = _bilinear_map(cf[:, :, 1], xs, ys) * downscale
-    return out
+        return np.zeros((n, 2))
+    torch = _torch()
+    cf = _dev(torch, np.asarray(coarser_flow, dtype=np.float64)
+              if not isinstance(coarser_flow, torch.Tensor) else coarser_flow)
+    if cf.dim() != 3 or cf.shape[2] != 2:
+        raise ValueError(f"coarser flow must be (H, W, 2), got {tuple(cf.shape)}")
+    out = torch.empty((n, 2), dtype=torch.float64, device="cuda")
+    c = _dev(torch, centers)
+    _lib.check(_lib.lib().dis_init_patches(cf.data_ptr(), int(cf.shape[1]), int(cf.shape[0]),
+                                           c.data_ptr(), n, int(downscale), out.data_ptr(),
+                                           _stream(torch)))
+    return out.cpu().numpy()
 
 
 def reset_outliers(displacements, init_displacements, patch_size: int) -> np.ndarray:
     """Back to the initialisation where |update| > patch size
-    (densification.py:98-107); returns a new array."""
-    disp = np.asarray(displacements, dtype=np.float64)
-    init = np.asarray(init_displacements, dtype=np.float64)
-    delta = disp - init
-    bad = np.hypot(delta[:, 0], delta[:, 1]) > patch_size
-    out = disp.copy()
-    out[bad] = init[bad]
-    return out
+    (densification.py:98-107), decided for a correctly rounded hypot; returns
+    a new array (GPU, ``dis_reset_outliers``)."""
+    from .inverse_search import _dev, _stream, _torch
+
+    torch = _torch()
+    d = _dev(torch, np.asarray(displacements, dtype=np.float64))
+    i = _dev(torch, np.asarray(init_displacements, dtype=np.float64))
+    if tuple(d.shape) != tuple(i.shape) or d.dim() != 2 or d.shape[1] != 2:
+        raise ValueError("displacements and init_displacements must both be (N, 2)")
+    out = torch.empty_like(d)
+    _lib.check(_lib.lib().dis_reset_outliers(d.data_ptr(), i.data_ptr(), int(d.shape[0]),
+                                             int(patch_size), out.data_ptr(), None,
+                                             _stream(torch)))
+    return out.cpu().numpy()
 
 
 def _grid_params(grid: PatchGrid) -> DisParams:

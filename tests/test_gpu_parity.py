@@ -463,3 +463,20 @@ def test_host_path_chunk_ramp_matches_device(torch, B):
         po.zero_()
         eng.run_host(p1.numpy(), p2.numpy(), out=po.numpy())
         assert np.array_equal(po.numpy(), want)
+
+
+def test_refinement_height_limit_is_a_documented_value_error(torch):
+    """Variational refinement of a level taller than 2048 rows (16 cluster
+    CTAs x 128 rows of the wavefront SOR) raises ValueError with the
+    documented message instead of running; without
+    refinement such levels run."""
+    from paper_1603_03590_b200 import FlowEngine
+
+    p = DisParams(patch_size=8, overlap=0.3, iterations=4, finest_scale=0, coarsest_scale=5,
+                  variational=VarParams(outer_iters_fixed=1))
+    with pytest.raises(ValueError, match="taller than 2048 rows"):
+        FlowEngine(1, 2050, 256, p)
+    q = dataclasses.replace(p, finest_scale=1)  # level 1 is 1025 rows: fine
+    FlowEngine(1, 2050, 256, q)
+    r = dataclasses.replace(p, variational=None)
+    FlowEngine(1, 2050, 256, r)

@@ -1,7 +1,8 @@
 """The reference-signature stage functions (paper_1603_03590_b200.densification,
 .variational, image_gradients, upsample_flow) against the reference's own
-outputs (tests/golden).  Grid / init / reset run on the host (CPU tests); the
-densification, refinement, gradients and upsampling on the GPU.  Bit-exact."""
+outputs (tests/golden).  The grid axes come from the library's host grid
+code (CPU test); init, reset, densification, refinement, gradients and
+upsampling run on the GPU.  Bit-exact."""
 
 import numpy as np
 import pytest
@@ -29,7 +30,12 @@ def test_create_grid_matches_reference_grids():
         create_grid(16, 16, 8, 1.0)
 
 
+@gpu
 def test_init_patches_and_reset_outliers_match_reference():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA GPU")
     from paper_1603_03590_b200 import create_grid, init_patches, reset_outliers
 
     g = golden("search_c1_like.npz")
