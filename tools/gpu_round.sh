@@ -13,7 +13,7 @@ if [ "${TESTS:-1}" = "1" ]; then
   timeout 1500 python -m pytest tests -m gpu -q -rfE > $OUT/pytest_gpu_$TAG.log 2>&1
 fi
 timeout 900 python bench.py --steps 20 --warmup 3 --config $CFG > $OUT/bench_$TAG.log 2>&1
-PROF="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --config $CFG"
+PROF="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-c3 --config $CFG"
 if [ "${NCU:-1}" = "1" ]; then
   $PROF > $OUT/prof_plain_$TAG.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv $PROF > $OUT/ncu_launch_$TAG.log 2>&1

@@ -36,7 +36,7 @@ CLASS_OF = [
     (r"k_patch|k_bidir_prep", "patch_search"),
     (r"k_densify", "densify"),
     (r"k_upsample|k_interleave", "upsample"),
-    (r"k_level1|k_downsample|k_gradients|k_convert|k_level0", "pyramid"),
+    (r"k_level1|k_downsample|k_gradients|k_convert|k_level0|k_pyr_", "pyramid"),
 ]
 
 
