@@ -84,6 +84,24 @@ __device__ __forceinline__ void load_run256(const double* p, double* s) {
 // _patch_precompute and _condition_hessians.  Writes the kPrep record the
 // Gauss-Newton stage needs; resets the GN work counter.
 // ---------------------------------------------------------------------------
+// Lane kernel work distribution: block b owns the contiguous patch range
+// [b N / nb, (b+1) N / nb) and its warps refill their pools from it in
+// order, so the 8 warps of an SM work on neighbouring grid rows and share
+// their template and window rows in L1 (a global queue scatters an SM's
+// warps over 8 distant regions: L1 hit rate 47 %); a block whose range is
+// used up steals pools from the following blocks' ranges.
+#ifndef DIS_GN_PREFETCH
+#define DIS_GN_PREFETCH 0  // experiments: prefetch the template rows into L1
+#endif
+#ifndef DIS_GN_RANGES
+#define DIS_GN_RANGES 0  // lane kernel: per-block patch ranges (0: one global queue)
+#endif
+#ifndef DIS_GN_CARVEOUT
+#define DIS_GN_CARVEOUT -1  // experiments: the lane kernel's shared-memory carveout (%)
+#endif
+constexpr int kRangeCounters = 4;     // counter[4 ..]: consumed patches per block range
+constexpr int kMaxGnBlocks = 1024;
+
 enum PrepField { PR_U0 = 0, PR_V0, PR_MEAN, PR_I00, PR_I01, PR_I11, PR_VALID, kPrep };
 
 __global__ void __launch_bounds__(128) k_patch_prep(SearchArgs a, double* __restrict__ prep,
@@ -97,6 +115,9 @@ __global__ void __launch_bounds__(128) k_patch_prep(SearchArgs a, double* __rest
     counter[1] = 0u;  // parked patches
     counter[2] = 0u;  // parked-patch queue
   }
+  // the lane kernel's per-block range counters
+  for (size_t i = gid; i < kMaxGnBlocks; i += (size_t)gridDim.x * blockDim.x)
+    counter[kRangeCounters + i] = 0u;
   if (gid >= N) return;
   const int b = (int)(gid / P);
   const int i = (int)(gid - (size_t)b * P);
@@ -257,7 +278,10 @@ __device__ __forceinline__ Axis1 axis_sample(double c, int n) {
   return a;
 }
 
-constexpr unsigned kPool = 64;   // patches per warp-pool refill
+#ifndef DIS_GN_POOL
+#define DIS_GN_POOL 64
+#endif
+constexpr unsigned kPool = DIS_GN_POOL;  // patches per warp-pool refill
 constexpr int kSpillStride = 16;  // doubles per parked patch state
 
 struct Lane {
@@ -467,6 +491,36 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
     load_run256<S1>(qry + idx, s);
   };
   double wsum = 0.0;
+#if DIS_GN_PREFETCH & 2
+  {  // all window rows into L1 at once (their misses overlap)
+    const double* wp = qry + (size_t)ybase * W + xbase;
+#pragma unroll
+    for (int oy = 0; oy <= PS; ++oy) {
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(wp));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(wp + PS));
+      wp += W;
+    }
+  }
+#endif
+#if DIS_GN_PREFETCH & 1
+  {  // the template rows pass 2 reads: into L1 while pass 1 runs
+    const double* tp = ref + (size_t)y0i * W + x0i;
+    const double* xp = rgx + (size_t)y0i * W + x0i;
+    const double* yp = rgy + (size_t)y0i * W + x0i;
+#pragma unroll
+    for (int oy = 0; oy < PS; ++oy) {
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(tp + PS - 1));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(xp + PS - 1));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(yp + PS - 1));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(tp));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(xp));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(yp));
+      tp += W;
+      xp += W;
+      yp += W;
+    }
+  }
+#endif
   {
     size_t idx = (size_t)ybase * W + xbase;
     double A[PS], s1[S1], s2[kPre ? S1 : 1];
@@ -583,6 +637,82 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
   mar = exact_div_pos(mar, dn);
 }
 
+// 8-pixel patches, template rows 32-byte aligned: the same evaluation with the
+// window's samples kept in registers between the passes (pass 2 reads them
+// back instead of reloading and re-interpolating the window rows) and pass
+// 2's template rows loaded one row ahead of their arithmetic (their load
+// latency was 60 % of the kernel's long-scoreboard stalls).  Same values,
+// same sums in the same order: bit-identical to eval_regular.
+template <int CODE>
+__device__ __forceinline__ void eval_regular8_t256(
+    const double* __restrict__ qry, const double* __restrict__ ref,
+    const double* __restrict__ rgx, const double* __restrict__ rgy, int W, int H, int x0i,
+    int y0i, double by, const double* FX, int xbase, int ybase, double mean_t, bool mean_norm,
+    double hb, double& off, double& ssd, double& b0, double& b1, double& mar) {
+  constexpr int PS = 8, S1 = PS + 1;
+  const double dn = (double)(PS * PS);
+  double V[PS * PS];
+  double wsum = 0.0;
+  {
+    size_t idx = (size_t)ybase * W + xbase;
+    double A[PS], s1[S1], s2[S1];
+    load_run256<S1>(qry + idx, s1);
+    idx += W;
+    load_run256<S1>(qry + idx, s2);
+#pragma unroll
+    for (int c = 0; c < PS; ++c) A[c] = s1[c] + FX[c] * (s1[c + 1] - s1[c]);
+#pragma unroll
+    for (int oy = 0; oy < PS; ++oy) {
+#pragma unroll
+      for (int c = 0; c < S1; ++c) s1[c] = s2[c];
+      if (oy + 1 < PS) {
+        idx += W;
+        load_run256<S1>(qry + idx, s2);
+      }
+      const double fy = axis_sample(by + oy, H).f;
+#pragma unroll
+      for (int ox = 0; ox < PS; ++ox) {
+        const double Bv = s1[ox] + FX[ox] * (s1[ox + 1] - s1[ox]);
+        V[oy * PS + ox] = A[ox] + fy * (Bv - A[ox]);
+        wsum += V[oy * PS + ox];
+        A[ox] = Bv;
+      }
+    }
+  }
+  const double* tr = ref + (size_t)y0i * W + x0i;
+  const double* gxr = rgx + (size_t)y0i * W + x0i;
+  const double* gyr = rgy + (size_t)y0i * W + x0i;
+  double T[2][3][PS];  // template rows oy (arithmetic) and oy + 1 (in flight)
+  auto load_t = [&](int oy, double (*t)[PS]) {
+#pragma unroll
+    for (int ox = 0; ox < PS; ox += 4) {
+      ldg256(tr + (size_t)oy * W + ox, t[0] + ox);
+      ldg256(gxr + (size_t)oy * W + ox, t[1] + ox);
+      ldg256(gyr + (size_t)oy * W + ox, t[2] + ox);
+    }
+  };
+  load_t(0, T[0]);
+  off = mean_norm ? exact_div_pos(wsum, dn) - mean_t : 0.0;
+  ssd = 0.0;
+  b0 = 0.0;
+  b1 = 0.0;
+  mar = 0.0;
+#pragma unroll
+  for (int oy = 0; oy < PS; ++oy) {
+    if (oy + 1 < PS) load_t(oy + 1, T[(oy + 1) & 1]);
+#pragma unroll
+    for (int ox = 0; ox < PS; ++ox) {
+      const double e = V[oy * PS + ox] - off - T[oy & 1][0][ox];
+      mar += fabs(e);
+      const double et = transform_residual(e, CODE, hb);
+      ssd += et * et;
+      b0 += T[oy & 1][1][ox] * et;
+      b1 += T[oy & 1][2][ox] * et;
+    }
+  }
+  mar = exact_div_pos(mar, dn);
+}
+
 // One window evaluation for any window and patch size: every sample gathers
 // its own four pixels with the reference's clamping.
 __device__ __forceinline__ void eval_general(const double* __restrict__ qry,
@@ -662,18 +792,38 @@ __global__ void __launch_bounds__(256, MINB) k_patch_gn(SearchArgs a,
   L.pid = -1;
   bool done = false;
   unsigned pool_next = 0, pool_end = 0;  // warp-uniform
+  // block ranges (see kRangeCounters); victim = the range refills come from
+  const unsigned nb = gridDim.x;
+  unsigned victim = blockIdx.x, tried = 0;
+  auto range_start = [&](unsigned v) {
+    return (unsigned)(((unsigned long long)N * v) / nb);
+  };
   for (;;) {
     const bool need = !done && L.pid < 0;
     unsigned mask = __ballot_sync(FULL, need);
     unsigned g = 0xffffffffu;
     while (mask) {
       if (pool_next >= pool_end) {
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(counter, kPool);
-        base = __shfl_sync(FULL, base, 0);
-        if (base >= N) break;
-        pool_next = base;
-        pool_end = base + kPool < N ? base + kPool : N;
+        bool got = false;
+        while (tried < nb) {  // own range first, then the following blocks'
+          const unsigned rs = range_start(victim);
+          unsigned re = range_start(victim + 1);
+          unsigned base = 0;
+          if (lane == 0)
+            base = DIS_GN_RANGES ? rs + atomicAdd(counter + kRangeCounters + victim, kPool)
+                                 : atomicAdd(counter, kPool);
+          if (!DIS_GN_RANGES) re = N;
+          base = __shfl_sync(FULL, base, 0);
+          if (base < re) {
+            pool_next = base;
+            pool_end = base + kPool < re ? base + kPool : re;
+            got = true;
+            break;
+          }
+          tried = DIS_GN_RANGES ? tried + 1 : nb;
+          victim = victim + 1 == nb ? 0 : victim + 1;
+        }
+        if (!got) break;
       }
       const unsigned avail = pool_end - pool_next;
       const unsigned rank = (unsigned)__popc(mask & ((1u << lane) - 1u));
@@ -709,9 +859,14 @@ __global__ void __launch_bounds__(256, MINB) k_patch_gn(SearchArgs a,
     const bool tmpl128 = (PS & 1) == 0 && __all_sync(am, ((toff | (size_t)W) & 1) == 0);
     const bool tmpl256 = (PS & 3) == 0 && __all_sync(am, ((toff | (size_t)W) & 3) == 0);
     double off, ssd, b0, b1, mar;
-    eval_regular<PS, CODE, (PS == 8 ? PS : (MINB == 1 ? 2 : 1))>(a.qry + po, a.ref + po, a.rgx + po, a.rgy + po, W, H, L.x0i, L.y0i,
-                           by, FX, xbase, ybase, L.mean_t, mean_norm, a.hb, tmpl128, tmpl256, off,
-                           ssd, b0, b1, mar);
+    if (PS == 8 && tmpl256)
+      eval_regular8_t256<CODE>(a.qry + po, a.ref + po, a.rgx + po, a.rgy + po, W, H, L.x0i,
+                               L.y0i, by, FX, xbase, ybase, L.mean_t, mean_norm, a.hb, off, ssd,
+                               b0, b1, mar);
+    else
+      eval_regular<PS, CODE, (PS == 8 ? PS : (MINB == 1 ? 2 : 1))>(
+          a.qry + po, a.ref + po, a.rgx + po, a.rgy + po, W, H, L.x0i, L.y0i, by, FX, xbase,
+          ybase, L.mean_t, mean_norm, a.hb, tmpl128, tmpl256, off, ssd, b0, b1, mar);
     gn_update(L, a, PS, off, ssd, b0, b1, mar);
   }
 }
@@ -960,10 +1115,15 @@ static void launch_gn_lane_minb(const SearchArgs& a, const double* prep, unsigne
   static int per_sms[kMaxDevices];
   int& per_sm = per_sms[current_device()];
   if (!per_sm) {
+#if DIS_GN_CARVEOUT >= 0
+    cudaFuncSetAttribute(k_patch_gn<PS, CODE, MINB>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, DIS_GN_CARVEOUT);
+#endif
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_patch_gn<PS, CODE, MINB>, 256, 0);
     if (per_sm < 1) per_sm = 1;
   }
   size_t blocks = (size_t)per_sm * sms;
+  if (blocks > (size_t)kMaxGnBlocks) blocks = kMaxGnBlocks;
   const size_t need = (n + 255) / 256;
   if (blocks > need) blocks = need;
   k_patch_gn<PS, CODE, MINB>
@@ -998,7 +1158,8 @@ static void launch_gn_lane(const SearchArgs& a, const double* prep, unsigned* co
 constexpr size_t kGroupLanes = (size_t)148 * 2048 * 4;  // group kernel up to ~4 waves
 
 size_t patch_search_scratch_bytes(int B, int P) {
-  return ((size_t)(kPrep + kSpillStride) * B * P) * sizeof(double) + 256;
+  return ((size_t)(kPrep + kSpillStride) * B * P) * sizeof(double) +
+         (kRangeCounters + kMaxGnBlocks) * sizeof(unsigned) + 256;
 }
 
 void launch_patch_search(const SearchArgs& a, void* scratch, cudaStream_t st) {
