@@ -1155,7 +1155,11 @@ static void launch_gn_lane(const SearchArgs& a, const double* prep, unsigned* co
     launch_gn_lane_code<PS, DIS_NORM_L2>(a, prep, counter, spill, spill_count, n, sms, st);
 }
 
-constexpr size_t kGroupLanes = (size_t)148 * 2048 * 4;  // group kernel up to ~4 waves
+// lane-group kernel up to ~2 (8px) / ~4 (12px) waves of group lanes; above, the
+// lane kernel (measured: c1's 256x109 level, 105k patches, is 0.03 ms faster
+// on the 8px lane kernel; c2's 256x109 level is faster on the group kernel)
+constexpr size_t kGroupLanes8 = (size_t)148 * 2048 * 2;
+constexpr size_t kGroupLanes12 = (size_t)148 * 2048 * 4;
 
 size_t patch_search_scratch_bytes(int B, int P) {
   return ((size_t)(kPrep + kSpillStride) * B * P) * sizeof(double) +
@@ -1172,10 +1176,11 @@ void launch_patch_search(const SearchArgs& a, void* scratch, cudaStream_t st) {
   const int TH = 128;
   k_patch_prep<<<(unsigned)((n + TH - 1) / TH), TH, 0, st>>>(a, prep, counter);
   note_launch();
-  static const size_t glanes = [] {
+  static const size_t forced = [] {
     const char* e = getenv("DIS_GROUP_LANES");  // experiments only
-    return e ? (size_t)atoll(e) : kGroupLanes;
+    return e ? (size_t)atoll(e) : 0;
   }();
+  const size_t glanes = forced ? forced : (a.ps == 8 ? kGroupLanes8 : kGroupLanes12);
   // coarse levels (few patches): a group of lanes per patch; fine levels: a
   // lane per patch (+ the general kernel for the parked, irregular windows)
   const bool group = (a.ps == 8 && n * 8 <= glanes) || (a.ps == 12 && n * 16 <= glanes);
