@@ -811,7 +811,8 @@ static int choose_cluster(int B, int H) {
 template <int S, bool HZ>
 static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const double* dvi,
                         double* duo, double* dvo, bool final_pass, cudaStream_t st) {
-  const int C = choose_cluster<S>(a.B, a.H);
+  int C = choose_cluster<S>(a.B, a.H);
+  while (C > 1 && (C - 1) * ((a.H + C - 1) / C) >= a.H) --C;  // no empty band (forced sizes)
   const int Hc = (a.H + C - 1) / C;
   const int hp = (Hc + 31) / 32 * 32;
   const int P = sor_group_size<S>();
