@@ -137,8 +137,9 @@ __global__ void __launch_bounds__(128) k_patch_prep(SearchArgs a, double* __rest
     const size_t cplane = (size_t)a.Wc * a.Hc;
     const double half = 0.5 * ps;
     const double k = (double)a.ds;
-    const double xs = ((double)x0i + half) / k;
-    const double ys = ((double)y0i + half) / k;
+    // (/ 2 is the exact multiplication by 0.5: no IEEE division for the usual factor)
+    const double xs = a.ds == 2 ? ((double)x0i + half) * 0.5 : ((double)x0i + half) / k;
+    const double ys = a.ds == 2 ? ((double)y0i + half) * 0.5 : ((double)y0i + half) / k;
     u0 = bilin_np(a.cu + b * cplane, a.Wc, a.Hc, xs, ys) * k;
     v0 = bilin_np(a.cv + b * cplane, a.Wc, a.Hc, xs, ys) * k;
   }

@@ -33,13 +33,17 @@ __device__ __forceinline__ void upsample_px(const double* __restrict__ U,
 
 // Two horizontally adjacent output pixels per thread (x = 2i, 2i + 1 share
 // their source columns through L1); the interleaved final field is written
-// as one 32-byte streaming store per thread.
+// as one 32-byte streaming store per thread.  KC = the factor at compile
+// time (2: x / 2.0 is the exact multiplication by 0.5; a runtime factor
+// costs an IEEE division per coordinate), 0 = the runtime factor kr.
+template <int KC>
 __global__ void __launch_bounds__(256) k_upsample(const double* __restrict__ iu,
                                                   const double* __restrict__ iv, int W, int H,
                                                   double* __restrict__ ou,
                                                   double* __restrict__ ov,
                                                   double* __restrict__ oi, int Wn, int Hn,
-                                                  double k) {
+                                                  double kr) {
+  const double k = KC > 0 ? (double)KC : kr;
   const int b = blockIdx.z;
   const int x = 2 * (blockIdx.x * 32 + (threadIdx.x & 31));
   const int y = blockIdx.y * 8 + (threadIdx.x >> 5);
@@ -96,7 +100,11 @@ void launch_upsample(const double* iu, const double* iv, int B, int W, int H, do
                      cudaStream_t st) {
   prof_begin(KC_UPSAMPLE, st);
   dim3 g((unsigned)((Wn + 63) / 64), (unsigned)((Hn + 7) / 8), (unsigned)B);
-  k_upsample<<<g, 256, 0, st>>>(iu, iv, W, H, ou, ov, out_interleaved, Wn, Hn, (double)factor);
+  if (factor == 2)
+    k_upsample<2><<<g, 256, 0, st>>>(iu, iv, W, H, ou, ov, out_interleaved, Wn, Hn, 2.0);
+  else
+    k_upsample<0><<<g, 256, 0, st>>>(iu, iv, W, H, ou, ov, out_interleaved, Wn, Hn,
+                                     (double)factor);
   prof_end(KC_UPSAMPLE, st);
   note_launch();
 }
