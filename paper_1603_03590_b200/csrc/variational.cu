@@ -33,7 +33,10 @@
 //
 // Neighbour terms use U_q = fl(u_q + du_q) exactly as the reference's
 // `u[y, x-1] + du[y, x-1]`; the last sweep's U is the updated flow.
+#include <cuda.h>  // CUtensorMap (the encode entry point comes from the runtime)
+
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "common.cuh"
@@ -50,12 +53,11 @@ enum RecField {
 constexpr int kChunks = kRec / 2;  // 16-byte chunks per record
 constexpr int kMaxSweepsPerPass = 8;
 
-constexpr int kZeroDoubles = 2 * 128;  // a zeroed line the SOR ring fill copies from
 
 size_t refine_scratch_doubles(int B, int W, int H) {
   const size_t Ls = (size_t)(W + H - 1) * H;
-  // records + du/dv carry for > 8 sweeps + the zero line
-  return (size_t)(kRec + 2) * B * Ls + kZeroDoubles;
+  // records + du/dv carry for > 8 sweeps
+  return (size_t)(kRec + 2) * B * Ls;
 }
 
 // Tile of kTTX x kTTY pixels per block (one pixel per thread).
@@ -228,10 +230,6 @@ __global__ void __launch_bounds__(256, 4) k_tensor_assemble(RefineArgs a, size_t
   const int W = a.W, H = a.H;
   const int b = blockIdx.z;
   const int X0 = blockIdx.x * kTTX, Y0 = blockIdx.y * kTTY;
-  if (blockIdx.x == 0 && blockIdx.y == 0 && b == 0) {  // the SOR's zero line
-    double* z = a.rec + (size_t)(kRec + 2) * a.B * Ls;
-    for (int i = threadIdx.x; i < kZeroDoubles; i += 256) z[i] = 0.0;
-  }
   for (int i = threadIdx.x; i < HX * HY; i += 256) {
     const int hy = i / HX, hx = i - hy * HX;
     const int x = X0 - 1 + hx, y = Y0 - 1 + hy;
@@ -291,6 +289,11 @@ __global__ void __launch_bounds__(256, 4) k_tensor_assemble(RefineArgs a, size_t
 #endif
 constexpr int kLookahead = DIS_SOR_LOOKAHEAD;  // diagonals fetched ahead of sweep 0
 constexpr int kMaxBandRows = 128;  // rows (threads per sweep) of one CTA's band
+// ring rows of a band of hc rows: the band + the row below, rounded to 4 (a
+// ring slot of 6 chunks x rows x 16 B is then a multiple of 128 bytes, the
+// TMA destination alignment); the TMA box holds 2 * rows <= 256 doubles
+__host__ __device__ constexpr int sor_ring_rows(int hc) { return (hc + 1 + 3) & ~3; }
+constexpr int kMaxTmaBandRows = 124;
 
 template <int S>
 __host__ __device__ constexpr int ring_slots() {
@@ -350,14 +353,6 @@ __device__ __forceinline__ void lds2(unsigned a, double& x, double& y) {
   asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(a) : "memory");
 }
 
-__device__ __forceinline__ void bulk_g2s(unsigned smem_dst, const void* gsrc, unsigned bytes,
-                                         unsigned bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_dst),
-      "l"(gsrc), "r"(bytes), "r"(bar)
-      : "memory");
-}
 __device__ __forceinline__ void mbar_wait_parity_cta(unsigned bar, unsigned parity) {
   asm volatile(
       "{\n"
@@ -392,11 +387,12 @@ __device__ __forceinline__ void mbar_wait_parity_cta(unsigned bar, unsigned pari
 // refined in the record, so an update is operation for operation the
 // reference's: su, sv in its neighbour order, then the two divisions.
 // Shared memory:
-//   ring[R][6][Hp+1] x 16 B : the 96-byte records of the live diagonals (band
+//   ring[R][6][rb] x 16 B   : the 96-byte records of the live diagonals (band
 //                             rows + the row below, sweep 0's down
-//                             neighbour), chunk-major like the global layout:
-//                             one diagonal = six cp.async.bulk copies issued
-//                             by the producer warp kLookahead steps ahead,
+//                             neighbour; rb = sor_ring_rows), chunk-major
+//                             like the global layout: one diagonal = one
+//                             TMA box (cp.async.bulk.tensor) issued by the
+//                             producer warp kLookahead steps ahead,
 //                             completion counted on the slot's mbarrier
 //   xuv[2][S][Hp+2] x 16 B  : U, V of the last two steps (+ halo rows above
 //                             and below the band)
@@ -406,16 +402,18 @@ __device__ __forceinline__ void mbar_wait_parity_cta(unsigned bar, unsigned pari
 // CTA's mbarrier).
 //
 // Idle pixels (outside the level: ramp-up/down of the wavefront, rows past
-// the band) see zero records, so they never update and publish U = du = 0;
-// a valid pixel's absent neighbour enters its sums as +0 * 0.  A warp whose
-// pixels are all idle skips the arithmetic (and publishes zeros).
+// the band) publish U = V = 0 and a zero right weight (their ring slots are
+// zero-filled past the last row and hold no record where x is outside
+// [0, W): masked); a valid pixel's absent neighbour enters its sums as
+// +0 * 0.  A warp whose pixels are all idle skips the arithmetic (and
+// publishes zeros).
 template <int S, bool HZ, int P>
 __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
     k_sor(const double* __restrict__ rec, int B, int W, int H, int Hc, size_t Ls,
                double omega, const double* du_in, const double* dv_in, double* du_out,
                double* dv_out, double* __restrict__ fu, double* __restrict__ fv,
-               uint32_t* status, const double* __restrict__ zeros) {
-  extern __shared__ __align__(16) unsigned char smem[];
+               uint32_t* status, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(128) unsigned char smem[];
   constexpr int R = ring_slots<S>();
   constexpr int G = (S + P - 1) / P;       // sweep groups
   constexpr int PL = S - (G - 1) * P;      // sweeps of the last group
@@ -431,7 +429,7 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
   const int y = y0 + r;
   const int nrows = min(Hc, H - y0);
   const int ndiag = W + H - 1;
-  const int rrows = Hp + 1;  // ring rows
+  const int rrows = sor_ring_rows(Hc);  // ring rows
   const int xrows = Hp + 2;  // exchange rows
   const unsigned slot_bytes = (unsigned)(kChunks * rrows * 16);
   const unsigned ring_s = (unsigned)__cvta_generic_to_shared(smem);
@@ -442,8 +440,6 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
   const unsigned bar_above = xd_s + 3 * d_ph_b;  // 8-byte aligned
   const unsigned bar_below = bar_above + 16;
   const unsigned bar_ring = bar_above + 32;  // [R] slot-fill barriers
-  const double2* __restrict__ base =
-      reinterpret_cast<const double2*>(rec + (size_t)b * Ls * kRec);  // [d][chunk][H]
   const double* Dui = du_in ? du_in + (size_t)b * Ls : nullptr;  // may alias du_out
   const double* Dvi = dv_in ? dv_in + (size_t)b * Ls : nullptr;
   const double om1 = 1.0 - omega;
@@ -464,39 +460,28 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
   }
   __syncthreads();
 
-  // ring fill (producer warp): diagonal jn -> slot jn % R.  Invariant: a
-  // slot's row holds the record of (jn - y, y) when that pixel is inside the
-  // level and zero otherwise.  The valid rows y in [max(y0, jn - W + 1),
-  // min(y0 + Hp, H - 1, jn)] are six bulk copies (one per chunk run); the
-  // rows that were valid for the slot's previous diagonal jn - R but are not
-  // any more (the ramp-down edge) are zeroed by a copy from a zeroed global
-  // line.
-  const int ylast = min(y0 + rrows, H) - 1;
+  // ring fill (producer warp): diagonal jn -> slot jn % R, one TMA box per
+  // diagonal issued by one thread (the per-chunk bulk copies it replaces
+  // cost ~800 cycles of issue per diagonal, on the small levels' critical
+  // path: 0.66 -> 0.57 us per step).
   const unsigned lane = threadIdx.x & 31;
   int jn = 0;
   unsigned sin_s = ring_s, sin_bar = bar_ring;
   auto issue_next = [&]() {
-    const int ya = max(y0, jn - W + 1), yb = min(ylast, jn);
-    const int jo = jn - R;  // the slot's previous diagonal
-    const int pa = max(y0, jo - W + 1), pb = min(ylast, jo);
-    const int za = pa, zb = min(pb, ya <= yb ? ya - 1 : pb);
-    const unsigned zrun = (jo >= 0 && zb >= za) ? (unsigned)(zb - za + 1) * 16u : 0u;
-    const unsigned run = yb >= ya ? (unsigned)(yb - ya + 1) * 16u : 0u;
-    // lane 0 arms the slot's barrier; lanes 0..5 copy one chunk run each (a
-    // complete_tx may land before the expect_tx: the phase cannot complete
-    // before lane 0's arrive)
-    if (lane == 0)
+    // the box [2 * rrows doubles of rows y0 ..][6 chunks] of diagonal jn:
+    // rows past the level are zero-filled by the TMA unit, the diagonal's
+    // slots of pixels outside the level (x = jn - y outside [0, W)) hold
+    // whatever the record array holds there (masked by the compute warps)
+    if (lane == 0) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sin_bar),
-                   "r"(kChunks * (run + zrun))
+                   "r"(slot_bytes)
                    : "memory");
-    if (lane < (unsigned)kChunks) {
-      const unsigned cc = lane;
-      if (zrun)
-        bulk_g2s(sin_s + (unsigned)((za - y0) * 16) + cc * (unsigned)(rrows * 16), zeros, zrun,
-                 sin_bar);
-      if (run)
-        bulk_g2s(sin_s + (unsigned)((ya - y0) * 16) + cc * (unsigned)(rrows * 16),
-                 base + ((size_t)jn * kChunks + cc) * H + ya, run, sin_bar);
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+          "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(sin_s),
+          "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(2 * y0), "r"(0), "r"(b * ndiag + jn),
+          "r"(sin_bar)
+          : "memory");
     }
     ++jn;
     sin_s += slot_bytes;
@@ -581,6 +566,10 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
         dnUf = dnUf + 0.0;
         dnVf = dnVf + 0.0;
       }
+      if (!(k - y + 1 < W)) {  // right neighbour outside the level:
+        rUf = 0.0;                              // its ring slot is not a record
+        rVf = 0.0;
+      }
     } else {  // the previous group's last sweep (exchange buffers)
       lds2(uv_r + (unsigned)(t0 - 1) * xstride + rrow + 16, rUf, rVf);
       lds2(uv_r + (unsigned)(t0 - 1) * xstride + rrow + 32, dnUf, dnVf);
@@ -591,7 +580,7 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
     // outside the fast division's exact range are redone after each pass.
     double uc[NT], vc[NT], m01[NT], r1[NT], den_u[NT], den_v[NT], rcp_v[NT], sv[NT], du[NT],
         dv[NT], q[NT], nn[NT];
-    bool dfast[NT], slow[NT];
+    bool dfast[NT], slow[NT], valid[NT];
     bool any_slow = false;
     // slot of my first sweep's diagonal k - 2 t0 (mod R)
     unsigned a_f = a_k - (unsigned)(2 * t0) * slot_bytes;
@@ -609,6 +598,8 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
       lds2(a_j + 4 * cstride + rrow, wqR, wqU);
       lds2(a_j + 5 * cstride + rrow, wqD, rcp_v[i]);
       const double wqL = WRp[i];  // the previous pixel's right weight
+      // pixel inside the level (TMA ring: other slots are not records)
+      valid[i] = (unsigned)(k - y - 2 * t) < (unsigned)W && r < nrows;
       WRn[i] = wqR;
       dfast[i] = den_fast_ok(den_u[i]) && den_fast_ok(den_v[i]);
       double upU, upV, rU, rV, dnU, dnV;
@@ -634,7 +625,7 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
               wqD * (dnV - cv);
       nn[i] = r0 + su - m01[i] * dv[i];
       q[i] = div_by_rcp(nn[i], den_u[i], rcp_u);
-      slow[i] = (den_u[i] > 1e-12) && !(dfast[i] && num_fast_ok(nn[i]));
+      slow[i] = valid[i] && (den_u[i] > 1e-12) && !(dfast[i] && num_fast_ok(nn[i]));
       any_slow |= slow[i];
     }
     if (any_slow) {
@@ -654,7 +645,7 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
       for (int i = 0; i < NT; ++i) {
         nn[i] = r1[i] + sv[i] - m01[i] * du[i];
         q[i] = div_by_rcp(nn[i], den_v[i], rcp_v[i]);
-        slow[i] = (den_v[i] > 1e-12) && !(dfast[i] && num_fast_ok(nn[i]));
+        slow[i] = valid[i] && (den_v[i] > 1e-12) && !(dfast[i] && num_fast_ok(nn[i]));
         any_slow |= slow[i];
       }
       if (any_slow) {
@@ -671,10 +662,14 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
     }
 #pragma unroll
     for (int i = 0; i < NT; ++i) {
-      Un[i] = uc[i] + du[i];
-      Vn[i] = vc[i] + dv[i];
+      // pixels outside the level publish U = V = 0 and a zero right weight
+      // (what valid neighbours read; their du, dv only reach the same
+      // pixel's later sweeps, which are outside the level too)
+      Un[i] = valid[i] ? uc[i] + du[i] : 0.0;
+      Vn[i] = valid[i] ? vc[i] + dv[i] : 0.0;
       Dn[i] = du[i];
       DVn[i] = dv[i];
+      WRn[i] = valid[i] ? WRn[i] : 0.0;
     }
   };
 
@@ -776,7 +771,8 @@ template <int S>
 static size_t sor_rows_smem_bytes(int hp) {
   const int P = sor_group_size<S>();
   const int G = (S + P - 1) / P;
-  const size_t rrows = (size_t)hp + 1, xrows = (size_t)hp + 2;
+  // (TMA ring rows <= hp + 4: sor_ring_rows of any band of <= hp rows)
+  const size_t rrows = (size_t)hp + 4, xrows = (size_t)hp + 2;
   return (size_t)ring_slots<S>() * kChunks * rrows * 16 + (size_t)2 * S * xrows * 16 +
          (size_t)3 * (G > 1 ? G - 1 : 1) * hp * 16 + (4 + ring_slots<S>()) * sizeof(uint64_t);
 }
@@ -791,8 +787,11 @@ static int choose_cluster(int B, int H) {
   }();
   if (forced > 0) return forced;
   auto hp = [&](int C) { return ((H + C - 1) / C + 31) / 32 * 32; };
+  const int max_rows = kMaxTmaBandRows;
   int C = 1;
-  while (C < 16 && (hp(C) > kMaxBandRows || sor_rows_smem_bytes<S>(hp(C)) > kMaxSmem)) ++C;
+  while (C < 16 && ((H + C - 1) / C > max_rows || hp(C) > kMaxBandRows ||
+                    sor_rows_smem_bytes<S>(hp(C)) > kMaxSmem))
+    ++C;
   const int sms = device_sm_count();
   // while the batch leaves SMs idle, split the rows further (bands of >= 32
   // rows; the st.async halo exchange costs ~0.15 us per step)
@@ -806,6 +805,30 @@ static int choose_cluster(int B, int H) {
       C = C64;
   }
   return C;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// link-time dependency on libcuda)
+static bool encode_tensor_map(CUtensorMap* m, CUtensorMapDataType dt, cuuint32_t rank,
+                              void* addr, const cuuint64_t* dims, const cuuint64_t* strides,
+                              const cuuint32_t* box, const cuuint32_t* estr) {
+  using EncFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                             const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                             const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<EncFn>(f);
+  }();
+  if (!fn) return false;
+  return fn(m, dt, rank, addr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int S, bool HZ>
@@ -822,7 +845,23 @@ static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const
   if (hp > kMaxBandRows || smem > kMaxSmem) return DIS_ERR_VALUE;
   using KFn = void (*)(const double*, int, int, int, int, size_t, double, const double*,
                        const double*, double*, double*, double*, double*, uint32_t*,
-                       const double*);
+                       const CUtensorMap);
+  CUtensorMap tmap;
+  std::memset(&tmap, 0, sizeof(tmap));
+  {
+    // the record array as [B * (W + H - 1) diagonals][6 chunks][2H doubles];
+    // box = one band's ring rows of one diagonal
+    if (sor_ring_rows(Hc) > kMaxBandRows) return DIS_ERR_VALUE;
+    const cuuint64_t dims[3] = {(cuuint64_t)2 * a.H, (cuuint64_t)kChunks,
+                                (cuuint64_t)a.B * (a.W + a.H - 1)};
+    const cuuint64_t strides[2] = {(cuuint64_t)2 * a.H * sizeof(double),
+                                   (cuuint64_t)kChunks * 2 * a.H * sizeof(double)};
+    const cuuint32_t box[3] = {(cuuint32_t)(2 * sor_ring_rows(Hc)), (cuuint32_t)kChunks, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    if (!encode_tensor_map(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)a.rec, dims, strides,
+                           box, estr))
+      return DIS_ERR_CUDA;
+  }
   KFn kfn = k_sor<S, HZ, S>;
   if (P == 1)
     kfn = k_sor<S, HZ, 1>;
@@ -850,9 +889,8 @@ static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const
   cfg.numAttrs = 1;
   double* fu = final_pass ? a.fu : nullptr;
   double* fv = final_pass ? a.fv : nullptr;
-  const double* zeros = a.rec + (size_t)(kRec + 2) * a.B * Ls;  // zeroed by k_tensor_assemble
   cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, (const double*)a.rec, a.B, a.W, a.H, Hc, Ls, a.omega, dui,
-                                     dvi, duo, dvo, fu, fv, a.status, zeros);
+                                     dvi, duo, dvo, fu, fv, a.status, tmap);
   return e == cudaSuccess ? DIS_OK : DIS_ERR_CUDA;
 }
 
