@@ -758,18 +758,23 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
 }
 
 template <int S>
-static int sor_group_size() {
-  static const int p = [] {
+static int sor_group_size(int hc, int ctas) {
+  static const int forced = [] {
     const char* e = getenv("DIS_SOR_P");  // experiments only
-    const int v = e ? atoi(e) : 1;  // measured best (c1, c3, c4)
-    return v == 1 || v == 2 ? v : S;
+    const int v = e ? atoi(e) : 0;
+    return v == 1 || v == 2 ? v : (v > 2 ? S : 0);
   }();
+  // two sweeps per thread (half the threads, two independent chains each)
+  // where the step is issue-bound: tall bands or more CTAs than SMs
+  // (measured: 218-row levels 1.075 -> 1.015 us/step, c3's 60-row bands
+  // over 2304 CTAs 0.979 -> 0.937); one sweep per thread on the small,
+  // latency-bound levels (13-row level 0.557 vs 0.608 us/step)
+  const int p = forced ? forced : ((hc >= 96 || ctas > device_sm_count()) ? 2 : 1);
   return p < S ? p : S;
 }
 
 template <int S>
-static size_t sor_rows_smem_bytes(int hp) {
-  const int P = sor_group_size<S>();
+static size_t sor_rows_smem_bytes(int hp, int P = 1) {
   const int G = (S + P - 1) / P;
   // (TMA ring rows <= hp + 4: sor_ring_rows of any band of <= hp rows)
   const size_t rrows = (size_t)hp + 4, xrows = (size_t)hp + 2;
@@ -838,10 +843,10 @@ static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const
   while (C > 1 && (C - 1) * ((a.H + C - 1) / C) >= a.H) --C;  // no empty band (forced sizes)
   const int Hc = (a.H + C - 1) / C;
   const int hp = (Hc + 31) / 32 * 32;
-  const int P = sor_group_size<S>();
+  const int P = sor_group_size<S>(Hc, a.B * C);
   const int G = (S + P - 1) / P;
   const int threads = hp * G + 32;  // + the producer warp
-  const size_t smem = sor_rows_smem_bytes<S>(hp);
+  const size_t smem = sor_rows_smem_bytes<S>(hp, P);
   if (hp > kMaxBandRows || smem > kMaxSmem) return DIS_ERR_VALUE;
   using KFn = void (*)(const double*, int, int, int, int, size_t, double, const double*,
                        const double*, double*, double*, double*, double*, uint32_t*,
@@ -867,13 +872,15 @@ static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const
     kfn = k_sor<S, HZ, 1>;
   else if (P == 2)
     kfn = k_sor<S, HZ, (S >= 2 ? 2 : 1)>;
-  // function attributes are per device: set them once on each device used
-  static bool attr[kMaxDevices];
+  // function attributes are per device and kernel: set them once for each
+  // (device, group size) used
+  static bool attr[kMaxDevices][3];
   const int dev = current_device();
-  if (!attr[dev]) {
+  const int pi = P == 1 ? 0 : (P == 2 ? 1 : 2);
+  if (!attr[dev][pi]) {
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
     cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr[dev] = true;
+    attr[dev][pi] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(a.B * C));
