@@ -120,13 +120,12 @@ __device__ __forceinline__ double bilin_raster(const double* __restrict__ f, int
 // (91-118) at one pixel: u, v, m00, m01, m11, r0, r1.  The second
 // derivatives of both levels (and their bilinear samples at the warped
 // position) are formed from the gradient rasters on the fly.
+// (up_, vp_: the pixel's flow, loaded by the caller)
 __device__ __forceinline__ void pixel_system(const RefineArgs& a, int b, int x, int y,
-                                             double* r) {
+                                             double up_, double vp_, double* r) {
   const int W = a.W, H = a.H;
   const size_t plane = (size_t)W * H;
   const size_t p = (size_t)y * W + x;
-  const double* __restrict__ u = a.fu + b * plane;
-  const double* __restrict__ v = a.fv + b * plane;
   const double* __restrict__ ref = a.ref + b * plane;
   const double* __restrict__ rgx = a.rgx + b * plane;
   const double* __restrict__ rgy = a.rgy + b * plane;
@@ -134,7 +133,6 @@ __device__ __forceinline__ void pixel_system(const RefineArgs& a, int b, int x, 
   const double* __restrict__ qgx = a.qgx + b * plane;
   const double* __restrict__ qgy = a.qgy + b * plane;
 
-  const double up_ = u[p], vp_ = v[p];
   double t0xx = 0.0, t0xy = 0.0, t0xz = 0.0, t0yy = 0.0, t0yz = 0.0, t0zz = 0.0;
   double tgxx = 0.0, tgxy = 0.0, tgxz = 0.0, tgyy = 0.0, tgyz = 0.0, tgzz = 0.0;
   const double wxp = x + up_;
@@ -230,18 +228,29 @@ __global__ void __launch_bounds__(256, 4) k_tensor_assemble(RefineArgs a, size_t
   const int W = a.W, H = a.H;
   const int b = blockIdx.z;
   const int X0 = blockIdx.x * kTTX, Y0 = blockIdx.y * kTTY;
+  const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
+  const int x = X0 + lx, y = Y0 + ly;
+  const bool inside = x < W && y < H;
+  // the pixel's flow first: its loads are in flight while the smoothness
+  // ring's are issued, and the system's warped gathers need only it (one
+  // memory latency fewer on each thread's chain than ring -> barrier ->
+  // system)
+  double up_ = 0.0, vp_ = 0.0;
+  if (inside) {
+    const size_t p = (size_t)b * W * H + (size_t)y * W + x;
+    up_ = a.fu[p];
+    vp_ = a.fv[p];
+  }
   for (int i = threadIdx.x; i < HX * HY; i += 256) {
     const int hy = i / HX, hx = i - hy * HX;
-    const int x = X0 - 1 + hx, y = Y0 - 1 + hy;
-    ws_t[hy][hx] = (x >= 0 && x < W && y >= 0 && y < H) ? pixel_ws(a, b, x, y) : 0.0;
+    const int xx = X0 - 1 + hx, yy = Y0 - 1 + hy;
+    ws_t[hy][hx] = (xx >= 0 && xx < W && yy >= 0 && yy < H) ? pixel_ws(a, b, xx, yy) : 0.0;
   }
+  double r[7];
+  if (inside) pixel_system(a, b, x, y, up_, vp_, r);
   __syncthreads();
   {
-    const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
-    const int x = X0 + lx, y = Y0 + ly;
-    if (x < W && y < H) {
-      double r[7];
-      pixel_system(a, b, x, y, r);
+    if (inside) {
       // _sor_sweeps' static part (variational.py:133-158): absent neighbours
       // give wq = +0, and adding +0 to the non-negative partial sum sw
       // leaves it unchanged
@@ -271,16 +280,16 @@ __global__ void __launch_bounds__(256, 4) k_tensor_assemble(RefineArgs a, size_t
   constexpr int ndd = kTTX + kTTY - 1;
   constexpr int npairs = ndd * kChunks;
   double2* __restrict__ out = reinterpret_cast<double2*>(a.rec + (size_t)b * Ls * kRec);
-  const int ly = threadIdx.x & 7;
-  const int y = Y0 + ly;
+  const int wy = threadIdx.x & 7;
+  const int oy = Y0 + wy;
   for (int m = (threadIdx.x >> 3); m < npairs; m += 32) {
     const int dd = m / kChunks;
     const int c = m - dd * kChunks;
-    const int lxx = dd - ly;
-    const int x = X0 + lxx;
-    if (lxx < 0 || lxx >= kTTX || x >= W || y >= H) continue;
-    const size_t d = (size_t)(x + y);
-    out[(d * kChunks + c) * H + y] = rs[ly * kTTX + lxx][c];
+    const int lxx = dd - wy;
+    const int ox = X0 + lxx;
+    if (lxx < 0 || lxx >= kTTX || ox >= W || oy >= H) continue;
+    const size_t d = (size_t)(ox + oy);
+    out[(d * kChunks + c) * H + oy] = rs[wy * kTTX + lxx][c];
   }
 }
 
