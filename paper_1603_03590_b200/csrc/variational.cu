@@ -265,9 +265,13 @@ __global__ void __launch_bounds__(256, 4) k_tensor_assemble(RefineArgs a, size_t
       o[1] = make_double2(r[3], r[5]);       // m01, r0
       o[2] = make_double2(r[6], r[2] + sw);  // r1, den_u = m00 + sw
       const double den_u = r[2] + sw, den_v = r[4] + sw;
-      o[3] = make_double2(den_v, rcp_refined(den_u));  // den_v = m11 + sw
+      // the reciprocals carry the SOR's fast-division flag in their sign:
+      // both denominators in the fast path's exact range -> the positive
+      // refined reciprocals, else -1 (the SOR then divides exactly)
+      const bool dfast = den_fast_ok(den_u) && den_fast_ok(den_v);
+      o[3] = make_double2(den_v, dfast ? rcp_refined(den_u) : -1.0);  // den_v = m11 + sw
       o[4] = make_double2(wqR, wqU);
-      o[5] = make_double2(wqD, rcp_refined(den_v));
+      o[5] = make_double2(wqD, dfast ? rcp_refined(den_v) : -1.0);
     }
   }
   __syncthreads();
@@ -545,12 +549,14 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
   // one step of my group's NT sweeps (NT = P, or PL for the last group)
   auto step = [&](auto ntc, int k, unsigned a_p) {
     constexpr int NT = decltype(ntc)::value;
-#pragma unroll
-    for (int i = 0; i < NT; ++i) Un[i] = Vn[i] = Dn[i] = DVn[i] = WRn[i] = 0.0;
     // warp-uniform: any of my warp's pixels inside the level in any of my
     // sweeps?  (lane 0 holds the warp's largest x; sweep t's x is k - y - 2t)
     const int xw0 = k - y0 - wr0 - 2 * t0;
-    if (!(live_warp && xw0 >= 0 && xw0 - 2 * (NT - 1) < W + 31)) return;
+    if (!(live_warp && xw0 >= 0 && xw0 - 2 * (NT - 1) < W + 31)) {
+#pragma unroll
+      for (int i = 0; i < NT; ++i) Un[i] = Vn[i] = Dn[i] = DVn[i] = WRn[i] = 0.0;
+      return;
+    }
     // my first sweep's right / down neighbours and own du
     double rUf, rVf, dnUf, dnVf, duf = 0.0, dvf = 0.0;
     if (g == 0) {  // sweep 0: the records (+ the carried du of a chained pass)
@@ -610,7 +616,7 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
       // pixel inside the level (TMA ring: other slots are not records)
       valid[i] = (unsigned)(k - y - 2 * t) < (unsigned)W && r < nrows;
       WRn[i] = wqR;
-      dfast[i] = den_fast_ok(den_u[i]) && den_fast_ok(den_v[i]);
+      dfast[i] = rcp_u > 0.0;  // (tensor_assemble: -1 when not both in range)
       double upU, upV, rU, rV, dnU, dnV;
       lds2(uv_r + (unsigned)t * xstride + rrow, upU, upV);  // exchange row r = band row r-1
       if (i > 0) {
