@@ -76,3 +76,56 @@ def test_band_split_and_sweep_groups_match_oracle(reference, tmp_path, bands, gr
     subprocess.run([sys.executable, "-c", CHILD, ROOT, str(sweeps), str(out)], env=env,
                    check=True, timeout=300, cwd=ROOT)
     assert np.array_equal(np.load(out), reference[sweeps])
+
+
+# The ring is filled by one TMA box per diagonal: the box holds the band's
+# rows + the row below rounded up to 4 (at most 128 rows, so bands are at most
+# 124 rows), rows past the level are zero-filled by the TMA unit and slots of
+# pixels outside the level are masked in the kernel.  Shapes at those edges:
+# a 124-row band (the largest box), 125 rows (forces two bands), band heights
+# whose ring rows need rounding, and levels much wider / much taller than the
+# other dimension (most of a diagonal's slots outside the level).
+CHILD_SHAPE = r"""
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, sys.argv[1])
+from paper_1603_03590_b200 import stages
+from paper_1603_03590_b200.params import DisParams, VarParams
+H, W, B = int(sys.argv[2]), int(sys.argv[3]), 2
+rng = np.random.default_rng(H * 1000 + W)
+f1 = rng.uniform(0, 255, (B, H, W))
+f2 = np.roll(f1, 1, axis=2) + rng.normal(0, 2, (B, H, W))
+init = rng.normal(0, 1.5, (B, H, W, 2))
+l1 = stages.build_pyramid(f1, 0)[0]
+l2 = stages.build_pyramid(f2, 0)[0]
+t = torch.tensor(init, device="cuda")
+u, v = stages.refine(t[..., 0].contiguous(), t[..., 1].contiguous(), l1, l2, DisParams(), 1)
+np.save(sys.argv[4], np.stack([u.cpu().numpy(), v.cpu().numpy()], -1))
+"""
+
+
+@pytest.mark.parametrize("H,W,bands", [(124, 40, 1), (125, 40, 0), (123, 37, 1), (94, 61, 2),
+                                       (17, 300, 0), (250, 9, 0)])
+def test_tma_ring_edges_match_oracle(tmp_path, H, W, bands):
+    from oracle import oracle as orc
+    from paper_1603_03590_b200.params import VarParams
+
+    env = dict(os.environ)
+    env.pop("DIS_SOR_P", None)
+    if bands:
+        env["DIS_SOR_CLUSTER"] = str(bands)
+    else:
+        env.pop("DIS_SOR_CLUSTER", None)
+    out = tmp_path / "flow.npy"
+    subprocess.run([sys.executable, "-c", CHILD_SHAPE, ROOT, str(H), str(W), str(out)], env=env,
+                   check=True, timeout=300, cwd=ROOT)
+    B = 2
+    rng = np.random.default_rng(H * 1000 + W)
+    f1 = rng.uniform(0, 255, (B, H, W))
+    f2 = np.roll(f1, 1, axis=2) + rng.normal(0, 2, (B, H, W))
+    init = rng.normal(0, 1.5, (B, H, W, 2))
+    want = np.stack([orc.refine(init[b], orc.build_pyramid(f1[b], 0)[0],
+                                orc.build_pyramid(f2[b], 0)[0], VarParams(), 1)
+                     for b in range(B)])
+    assert np.array_equal(np.load(out), want)
