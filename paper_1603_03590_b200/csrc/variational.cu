@@ -302,11 +302,18 @@ __global__ void __launch_bounds__(256, 4) k_tensor_assemble(RefineArgs a, size_t
 #endif
 constexpr int kLookahead = DIS_SOR_LOOKAHEAD;  // diagonals fetched ahead of sweep 0
 constexpr int kMaxBandRows = 128;  // rows (threads per sweep) of one CTA's band
-// ring rows of a band of hc rows: the band + the row below, rounded to 4 (a
-// ring slot of 6 chunks x rows x 16 B is then a multiple of 128 bytes, the
-// TMA destination alignment); the TMA box holds 2 * rows <= 256 doubles
-__host__ __device__ constexpr int sor_ring_rows(int hc) { return (hc + 1 + 3) & ~3; }
-constexpr int kMaxTmaBandRows = 124;
+// ring rows of a band of hc rows: the band + the row below (sweep 0's down
+// neighbour of the band's last row), rounded to 4 (a ring slot of 6 chunks x
+// rows x 16 B is then a multiple of 128 bytes, the TMA destination
+// alignment); the TMA box holds 2 * rows <= 256 doubles.  A 128-row band
+// (levels of 2033..2048 rows: 16 bands) has no room for the row below in
+// the box: its u, v come as a second 16-byte box into a 128-byte slot beside
+// the ring ("below mode").
+__host__ __device__ constexpr bool sor_below_mode(int hc) { return hc + 1 > 128; }
+__host__ __device__ constexpr int sor_ring_rows(int hc) {
+  return sor_below_mode(hc) ? ((hc + 3) & ~3) : ((hc + 1 + 3) & ~3);
+}
+constexpr int kBelowSlot = 128;  // below mode: bytes after a ring slot for the row below
 
 template <int S>
 __host__ __device__ constexpr int ring_slots() {
@@ -425,7 +432,8 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
     k_sor(const double* __restrict__ rec, int B, int W, int H, int Hc, size_t Ls,
                double omega, const double* du_in, const double* dv_in, double* du_out,
                double* dv_out, double* __restrict__ fu, double* __restrict__ fv,
-               uint32_t* status, const __grid_constant__ CUtensorMap tmap) {
+               uint32_t* status, const __grid_constant__ CUtensorMap tmap,
+               const __grid_constant__ CUtensorMap tmap_below) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int R = ring_slots<S>();
   constexpr int G = (S + P - 1) / P;       // sweep groups
@@ -444,7 +452,9 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
   const int ndiag = W + H - 1;
   const int rrows = sor_ring_rows(Hc);  // ring rows
   const int xrows = Hp + 2;  // exchange rows
-  const unsigned slot_bytes = (unsigned)(kChunks * rrows * 16);
+  const bool below = sor_below_mode(Hc);  // the row below has its own 16 bytes
+  const unsigned below_off = (unsigned)(kChunks * rrows * 16);  // (after the slot's chunks)
+  const unsigned slot_bytes = below_off + (below ? (unsigned)kBelowSlot : 0u);
   const unsigned ring_s = (unsigned)__cvta_generic_to_shared(smem);
   const unsigned ring_end = ring_s + (unsigned)R * slot_bytes;
   const unsigned xuv_s = ring_end;
@@ -487,7 +497,7 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
     // whatever the record array holds there (masked by the compute warps)
     if (lane == 0) {
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sin_bar),
-                   "r"(slot_bytes)
+                   "r"(below_off + (below ? 16u : 0u))
                    : "memory");
       asm volatile(
           "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
@@ -495,6 +505,13 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
           "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(2 * y0), "r"(0), "r"(b * ndiag + jn),
           "r"(sin_bar)
           : "memory");
+      if (below)
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(sin_s + below_off),
+            "l"(reinterpret_cast<uint64_t>(&tmap_below)), "r"(2 * (y0 + Hc)), "r"(0),
+            "r"(b * ndiag + jn), "r"(sin_bar)
+            : "memory");
     }
     ++jn;
     sin_s += slot_bytes;
@@ -533,6 +550,9 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
   bool bad = false;
   unsigned a_k = ring_s;  // slot of diagonal k
   const unsigned rrow = (unsigned)(r * 16);
+  // sweep 0's down neighbour in the next diagonal's slot: ring row r + 1, or
+  // (below mode, the band's last row) the row-below area
+  const unsigned dn_off = below && r == Hc - 1 ? below_off : rrow + 16;
   const unsigned cstride = (unsigned)(rrows * 16);
   const unsigned xstride = (unsigned)(xrows * 16);
   unsigned uv_r = xuv_s + (unsigned)S * xstride, uv_w = xuv_s;  // step k-1 / step k
@@ -561,7 +581,8 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
     double rUf, rVf, dnUf, dnVf, duf = 0.0, dvf = 0.0;
     if (g == 0) {  // sweep 0: the records (+ the carried du of a chained pass)
       lds2(a_p + rrow, rUf, rVf);
-      lds2(a_p + rrow + 16, dnUf, dnVf);
+      // (below mode, the band's last row: the row below has its own slot)
+      lds2(a_p + dn_off, dnUf, dnVf);
       if (Dui) {
         const int j = k;
         const bool hasD = y < H - 1;
@@ -791,9 +812,9 @@ static int sor_group_size(int hc, int ctas) {
 template <int S>
 static size_t sor_rows_smem_bytes(int hp, int P = 1) {
   const int G = (S + P - 1) / P;
-  // (TMA ring rows <= hp + 4: sor_ring_rows of any band of <= hp rows)
+  // (TMA ring rows = sor_ring_rows(band) <= hp + 4 for any band of <= hp rows)
   const size_t rrows = (size_t)hp + 4, xrows = (size_t)hp + 2;
-  return (size_t)ring_slots<S>() * kChunks * rrows * 16 + (size_t)2 * S * xrows * 16 +
+  return (size_t)ring_slots<S>() * (kChunks * rrows * 16 + kBelowSlot) + (size_t)2 * S * xrows * 16 +
          (size_t)3 * (G > 1 ? G - 1 : 1) * hp * 16 + (4 + ring_slots<S>()) * sizeof(uint64_t);
 }
 
@@ -807,7 +828,7 @@ static int choose_cluster(int B, int H) {
   }();
   if (forced > 0) return forced;
   auto hp = [&](int C) { return ((H + C - 1) / C + 31) / 32 * 32; };
-  const int max_rows = kMaxTmaBandRows;
+  const int max_rows = kMaxBandRows;
   int C = 1;
   while (C < 16 && ((H + C - 1) / C > max_rows || hp(C) > kMaxBandRows ||
                     sor_rows_smem_bytes<S>(hp(C)) > kMaxSmem))
@@ -865,12 +886,14 @@ static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const
   if (hp > kMaxBandRows || smem > kMaxSmem) return DIS_ERR_VALUE;
   using KFn = void (*)(const double*, int, int, int, int, size_t, double, const double*,
                        const double*, double*, double*, double*, double*, uint32_t*,
-                       const CUtensorMap);
-  CUtensorMap tmap;
+                       const CUtensorMap, const CUtensorMap);
+  CUtensorMap tmap, tmap_below;
   std::memset(&tmap, 0, sizeof(tmap));
+  std::memset(&tmap_below, 0, sizeof(tmap_below));
   {
     // the record array as [B * (W + H - 1) diagonals][6 chunks][2H doubles];
-    // box = one band's ring rows of one diagonal
+    // box = one band's ring rows of one diagonal (tmap) / the u, v of one
+    // row (tmap_below: the row below the band)
     if (sor_ring_rows(Hc) > kMaxBandRows) return DIS_ERR_VALUE;
     const cuuint64_t dims[3] = {(cuuint64_t)2 * a.H, (cuuint64_t)kChunks,
                                 (cuuint64_t)a.B * (a.W + a.H - 1)};
@@ -878,8 +901,11 @@ static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const
                                    (cuuint64_t)kChunks * 2 * a.H * sizeof(double)};
     const cuuint32_t box[3] = {(cuuint32_t)(2 * sor_ring_rows(Hc)), (cuuint32_t)kChunks, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
+    const cuuint32_t box_below[3] = {2, 1, 1};
     if (!encode_tensor_map(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)a.rec, dims, strides,
-                           box, estr))
+                           box, estr) ||
+        !encode_tensor_map(&tmap_below, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)a.rec, dims,
+                           strides, box_below, estr))
       return DIS_ERR_CUDA;
   }
   KFn kfn = k_sor<S, HZ, S>;
@@ -912,7 +938,7 @@ static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const
   double* fu = final_pass ? a.fu : nullptr;
   double* fv = final_pass ? a.fv : nullptr;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, (const double*)a.rec, a.B, a.W, a.H, Hc, Ls, a.omega, dui,
-                                     dvi, duo, dvo, fu, fv, a.status, tmap);
+                                     dvi, duo, dvo, fu, fv, a.status, tmap, tmap_below);
   return e == cudaSuccess ? DIS_OK : DIS_ERR_CUDA;
 }
 

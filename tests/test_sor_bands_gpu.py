@@ -79,12 +79,13 @@ def test_band_split_and_sweep_groups_match_oracle(reference, tmp_path, bands, gr
 
 
 # The ring is filled by one TMA box per diagonal: the box holds the band's
-# rows + the row below rounded up to 4 (at most 128 rows, so bands are at most
-# 124 rows), rows past the level are zero-filled by the TMA unit and slots of
-# pixels outside the level are masked in the kernel.  Shapes at those edges:
-# a 124-row band (the largest box), 125 rows (forces two bands), band heights
-# whose ring rows need rounding, and levels much wider / much taller than the
-# other dimension (most of a diagonal's slots outside the level).
+# rows rounded up to 4 (at most 128), the row below the band is a second
+# 16-byte box, rows past the level are zero-filled by the TMA unit and slots
+# of pixels outside the level are masked in the kernel.  Shapes at those
+# edges: 124- and 128-row bands (the largest box), 125 rows, band heights
+# whose ring rows need rounding, levels much wider / much taller than the
+# other dimension (most of a diagonal's slots outside the level), and the
+# tallest supported levels (16 bands of 128 rows: 2048 rows; 2033).
 CHILD_SHAPE = r"""
 import sys
 import numpy as np
@@ -106,7 +107,8 @@ np.save(sys.argv[4], np.stack([u.cpu().numpy(), v.cpu().numpy()], -1))
 
 
 @pytest.mark.parametrize("H,W,bands", [(124, 40, 1), (125, 40, 0), (123, 37, 1), (94, 61, 2),
-                                       (17, 300, 0), (250, 9, 0)])
+                                       (128, 40, 1), (17, 300, 0), (250, 9, 0), (2048, 24, 0),
+                                       (2033, 20, 0)])
 def test_tma_ring_edges_match_oracle(tmp_path, H, W, bands):
     from oracle import oracle as orc
     from paper_1603_03590_b200.params import VarParams
