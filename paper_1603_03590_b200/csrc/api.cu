@@ -228,7 +228,7 @@ void make_plan(const dis_params_t* p, int B, int H, int W, Plan* pl) {
   {
     size_t mx = 0;
     for (int s = pl->sf; s <= pl->ss; ++s) {
-      size_t r = patch_search_scratch_bytes(B, pl->ax[s].n * pl->ay[s].n);
+      size_t r = patch_search_scratch_bytes(B, pl->ax[s].n * pl->ay[s].n, pl->ws[s], pl->hs[s]);
       if (r > mx) mx = r;
     }
     pl->off_search = take(cur, mx);
@@ -1122,7 +1122,7 @@ size_t dis_patch_search_workspace_bytes(int32_t B, int32_t W, int32_t H,
   if (dis_params_validate(p) || W < p->patch_size || H < p->patch_size) return 0;
   const int sp = grid_spacing(p->patch_size, p->overlap);
   return patch_search_scratch_bytes(
-      B, make_axis(W, p->patch_size, sp).n * make_axis(H, p->patch_size, sp).n);
+      B, make_axis(W, p->patch_size, sp).n * make_axis(H, p->patch_size, sp).n, W, H);
 }
 
 int dis_patch_search(const double* ref_img, const double* ref_gx, const double* ref_gy,

@@ -71,8 +71,14 @@ struct SearchArgs {
   int32_t* out_evals; // optional
   unsigned long long* census;  // optional: [0] += evaluations, [1] += patches
   int horizontal;     // stereo: _condition_hessians horizontal_only (259-264)
+  // set by launch_patch_search: the query level with a replicated border
+  // (patch_search.cu, kQPad), read by the lane kernel
+  const double* qpad;
+  int qp_pitch;
 };
-size_t patch_search_scratch_bytes(int B, int P);
+// scratch of one level's search: per-patch prep + parked state + counters +
+// the padded query level (W x H level, P patches per pair)
+size_t patch_search_scratch_bytes(int B, int P, int W, int H);
 void launch_patch_search(const SearchArgs& a, void* scratch, cudaStream_t st);
 
 // stage_search.cu — the reference's inverse-search / init / reset stage

@@ -433,26 +433,65 @@ __device__ __forceinline__ double seg_sample(double i00, double i01, double i10,
   return a + fy * (bb - a);
 }
 
-// Is the window at (bx, by) "regular": its ps sample columns (rows) are the ps
-// consecutive pixels xbase.. (ybase..), each with its right (lower)
-// neighbour unclamped?  Then each sample's bilinear operands are segment
-// entries c, c+1 of the rows ybase.. ybase+ps.  (Not regular: the window is
-// clamped at a border, or a coordinate rounds onto the next integer.)
+// Is the window at (bx, by) "regular": its ps sample columns (rows) are ps
+// consecutive pixels xbase.. (ybase..) with their right (lower) neighbours?
+// Then each sample's bilinear operands are segment entries c, c+1 of the
+// rows ybase.. ybase+ps.  The lane kernel reads the query level from a copy
+// with a replicated border of kQPad pixels (k_pad_query): P[Y][X] = I[clamp(Y)][clamp(X)].  A window
+// is then "regular" whenever its samples' integer parts are consecutive in
+// padded coordinates, clamped or not, and the clamped samples come out as
+// the reference's: where _bilin clamps a coordinate (inverse_search.py:
+// 38-45) its two operands along that axis are the same replicated pixel, so
+// the interpolant is p + f*(p - p) = p + (+0) for the reference's f = 0 and
+// for any other f (the fractions are still taken from the clamped
+// coordinate).  The reference forms p + 0*(q - p) with q its unclamped
+// neighbour, which differs only in the sign of an exactly-zero sample; a
+// sample enters only sums started at +0.0 (which stay +0 under either zero)
+// and e = val - off - t, whose sign of zero is squared, absolute-valued or
+// multiplied into such a sum — so every output is bit-identical.  Only
+// windows reaching more than kQPad pixels past the level still park.
+constexpr int kQPad = 16;
+__host__ __device__ constexpr int qpad_pitch(int W) { return (W + 2 * kQPad + 4 + 3) & ~3; }
+__host__ __device__ constexpr int qpad_rows(int H) { return H + 2 * kQPad; }
+
+__global__ void __launch_bounds__(256) k_pad_query(const double* __restrict__ src, int W, int H,
+                                                   double* __restrict__ dst, int pitch) {
+  const int b = blockIdx.z;
+  const int Y = blockIdx.y;
+  const int y = min(max(Y - kQPad, 0), H - 1);
+  const double* __restrict__ s = src + ((size_t)b * H + y) * W;
+  double2* __restrict__ d =
+      reinterpret_cast<double2*>(dst + ((size_t)b * qpad_rows(H) + Y) * pitch);
+  for (int X2 = blockIdx.x * blockDim.x + threadIdx.x; X2 < pitch / 2;
+       X2 += gridDim.x * blockDim.x) {
+    const int x0 = min(max(2 * X2 - kQPad, 0), W - 1);
+    const int x1 = min(max(2 * X2 + 1 - kQPad, 0), W - 1);
+    d[X2] = make_double2(__ldg(s + x0), __ldg(s + x1));
+  }
+}
+
+// sample coordinate c's fraction with the reference's clamping (0 where
+// _bilin clamps, c - floor(c) elsewhere) and its floor
+__device__ __forceinline__ double clamped_frac(double c, double fl, int n) {
+  return (c < 0.0 || c > n - 1.0) ? 0.0 : c - fl;
+}
+
 template <int PS>
-__device__ __forceinline__ bool window_regular(double bx, double by, int W, int H, double* FX,
-                                               int& xbase, int& ybase) {
+__device__ __forceinline__ bool window_regular_pad(double bx, double by, int W, int H,
+                                                   double* FX, int& xbase, int& ybase) {
+  if (!(bx >= (double)(-kQPad) && bx < (double)(W - 1 + kQPad - PS) &&
+        by >= (double)(-kQPad) && by < (double)(H - 1 + kQPad - PS)))
+    return false;  // (also NaN)
+  const double flx = floor(bx), fly = floor(by);
+  xbase = (int)flx;
+  ybase = (int)fly;
   bool regular = true;
 #pragma unroll
   for (int o = 0; o < PS; ++o) {
-    const Axis1 ax = axis_sample(bx + o, W);
-    const Axis1 ay = axis_sample(by + o, H);
-    if (o == 0) {
-      xbase = ax.i0;
-      ybase = ay.i0;
-    }
-    regular = regular && ax.i0 == xbase + o && ax.i1 == ax.i0 + 1 && ay.i0 == ybase + o &&
-              ay.i1 == ay.i0 + 1;
-    FX[o] = ax.f;
+    const double cx = bx + o, cy = by + o;
+    const double fx = floor(cx), fy = floor(cy);
+    regular = regular && fx - flx == (double)o && fy - fly == (double)o;
+    FX[o] = clamped_frac(cx, fx, W);
   }
   return regular;
 }
@@ -471,8 +510,9 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
                                              const double* __restrict__ ref,
                                              const double* __restrict__ rgx,
                                              const double* __restrict__ rgy, int W, int H,
-                                             int x0i, int y0i, double by, const double* FX,
-                                             int xbase, int ybase, double mean_t, bool mean_norm,
+                                             int Wq, int x0i, int y0i, double by,
+                                             const double* FX, int xbase, int ybase,
+                                             double mean_t, bool mean_norm,
                                              double hb, bool tmpl128, bool tmpl256, double& off,
                                              double& ssd, double& b0, double& b1, double& mar) {
   constexpr int S1 = PS + 1;
@@ -482,7 +522,7 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
   // read as 256-bit loads from the 32-byte aligned element at or below idx
   // (one sector per lane per load instead of one per element) and shifted
   // into place by the lane's offset o = idx mod 4 (two select levels)
-  auto load_row = [&](size_t idx, double* s) {
+  auto load_row = [&](ptrdiff_t idx, double* s) {
     if (PS > 12) {  // (wider rows: the shift registers cost more than the loads save;
                     // measured at 12: c4's patch search 46.8 -> 39.0 ms)
 #pragma unroll
@@ -494,12 +534,12 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
   double wsum = 0.0;
 #if DIS_GN_PREFETCH & 2
   {  // all window rows into L1 at once (their misses overlap)
-    const double* wp = qry + (size_t)ybase * W + xbase;
+    const double* wp = qry + (ptrdiff_t)ybase * Wq + xbase;
 #pragma unroll
     for (int oy = 0; oy <= PS; ++oy) {
       asm volatile("prefetch.global.L1 [%0];" ::"l"(wp));
       asm volatile("prefetch.global.L1 [%0];" ::"l"(wp + PS));
-      wp += W;
+      wp += Wq;
     }
   }
 #endif
@@ -523,11 +563,11 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
   }
 #endif
   {
-    size_t idx = (size_t)ybase * W + xbase;
+    ptrdiff_t idx = (ptrdiff_t)ybase * Wq + xbase;
     double A[PS], s1[S1], s2[kPre ? S1 : 1];
     load_row(idx, s1);
     if (kPre) {
-      idx += W;
+      idx += Wq;
       load_row(idx, s2);
     }
 #pragma unroll
@@ -538,11 +578,11 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
 #pragma unroll
         for (int c = 0; c < S1; ++c) s1[c] = s2[c];
         if (oy + 1 < PS) {  // row oy + 2 in flight during this row's arithmetic
-          idx += W;
+          idx += Wq;
           load_row(idx, s2);
         }
       } else {
-        idx += W;
+        idx += Wq;
         load_row(idx, s1);
       }
       const double fy = axis_sample(by + oy, H).f;
@@ -568,11 +608,11 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
     b1 += gyv * et;
   };
   {
-    size_t idx = (size_t)ybase * W + xbase;
+    ptrdiff_t idx = (ptrdiff_t)ybase * Wq + xbase;
     double A[PS], s1[S1], s2[kPre ? S1 : 1];
     load_row(idx, s1);
     if (kPre) {
-      idx += W;
+      idx += Wq;
       load_row(idx, s2);
     }
 #pragma unroll
@@ -586,11 +626,11 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
 #pragma unroll
         for (int c = 0; c < S1; ++c) s1[c] = s2[c];
         if (oy + 1 < PS) {
-          idx += W;
+          idx += Wq;
           load_row(idx, s2);
         }
       } else {
-        idx += W;
+        idx += Wq;
         load_row(idx, s1);
       }
       const double fy = axis_sample(by + oy, H).f;
@@ -647,18 +687,18 @@ __device__ __forceinline__ void eval_regular(const double* __restrict__ qry,
 template <int CODE>
 __device__ __forceinline__ void eval_regular8_t256(
     const double* __restrict__ qry, const double* __restrict__ ref,
-    const double* __restrict__ rgx, const double* __restrict__ rgy, int W, int H, int x0i,
-    int y0i, double by, const double* FX, int xbase, int ybase, double mean_t, bool mean_norm,
-    double hb, double& off, double& ssd, double& b0, double& b1, double& mar) {
+    const double* __restrict__ rgx, const double* __restrict__ rgy, int W, int H, int Wq,
+    int x0i, int y0i, double by, const double* FX, int xbase, int ybase, double mean_t,
+    bool mean_norm, double hb, double& off, double& ssd, double& b0, double& b1, double& mar) {
   constexpr int PS = 8, S1 = PS + 1;
   const double dn = (double)(PS * PS);
   double V[PS * PS];
   double wsum = 0.0;
   {
-    size_t idx = (size_t)ybase * W + xbase;
+    ptrdiff_t idx = (ptrdiff_t)ybase * Wq + xbase;
     double A[PS], s1[S1], s2[S1];
     load_run256<S1>(qry + idx, s1);
-    idx += W;
+    idx += Wq;
     load_run256<S1>(qry + idx, s2);
 #pragma unroll
     for (int c = 0; c < PS; ++c) A[c] = s1[c] + FX[c] * (s1[c + 1] - s1[c]);
@@ -667,7 +707,7 @@ __device__ __forceinline__ void eval_regular8_t256(
 #pragma unroll
       for (int c = 0; c < S1; ++c) s1[c] = s2[c];
       if (oy + 1 < PS) {
-        idx += W;
+        idx += Wq;
         load_run256<S1>(qry + idx, s2);
       }
       const double fy = axis_sample(by + oy, H).f;
@@ -785,6 +825,8 @@ __global__ void __launch_bounds__(256, MINB) k_patch_gn(SearchArgs a,
   const unsigned N = (unsigned)(a.B * P);
   const int W = a.W, H = a.H;
   const size_t plane = (size_t)W * H;
+  const int Wq = a.qp_pitch;
+  const size_t qplane = (size_t)qpad_rows(H) * Wq;
   const bool mean_norm = a.mean_norm != 0;
   // the lane's Gauss-Newton state lives in shared memory (touched a few
   // times per window evaluation): the registers go to the window rows
@@ -846,7 +888,7 @@ __global__ void __launch_bounds__(256, MINB) k_patch_gn(SearchArgs a,
     const double bx = (double)L.x0i + L.u, by = (double)L.y0i + L.v;
     double FX[PS];
     int xbase, ybase;
-    if (!window_regular<PS>(bx, by, W, H, FX, xbase, ybase)) {
+    if (!window_regular_pad<PS>(bx, by, W, H, FX, xbase, ybase)) {
       const unsigned slot = atomicAdd(spill_count, 1u);
       lane_park(L, spill + (size_t)slot * kSpillStride);
       L.pid = -1;
@@ -859,15 +901,17 @@ __global__ void __launch_bounds__(256, MINB) k_patch_gn(SearchArgs a,
     const unsigned am = __activemask();
     const bool tmpl128 = (PS & 1) == 0 && __all_sync(am, ((toff | (size_t)W) & 1) == 0);
     const bool tmpl256 = (PS & 3) == 0 && __all_sync(am, ((toff | (size_t)W) & 3) == 0);
+    // the pair's padded query level, at its pixel (0, 0)
+    const double* qp = a.qpad + (size_t)L.b * qplane + (size_t)kQPad * Wq + kQPad;
     double off, ssd, b0, b1, mar;
     if (PS == 8 && tmpl256)
-      eval_regular8_t256<CODE>(a.qry + po, a.ref + po, a.rgx + po, a.rgy + po, W, H, L.x0i,
-                               L.y0i, by, FX, xbase, ybase, L.mean_t, mean_norm, a.hb, off, ssd,
-                               b0, b1, mar);
+      eval_regular8_t256<CODE>(qp, a.ref + po, a.rgx + po, a.rgy + po, W, H, Wq, L.x0i, L.y0i,
+                               by, FX, xbase, ybase, L.mean_t, mean_norm, a.hb, off, ssd, b0,
+                               b1, mar);
     else
       eval_regular<PS, CODE, (PS == 8 ? PS : (MINB == 1 ? 2 : 1))>(
-          a.qry + po, a.ref + po, a.rgx + po, a.rgy + po, W, H, L.x0i, L.y0i, by, FX, xbase,
-          ybase, L.mean_t, mean_norm, a.hb, tmpl128, tmpl256, off, ssd, b0, b1, mar);
+          qp, a.ref + po, a.rgx + po, a.rgy + po, W, H, Wq, L.x0i, L.y0i, by, FX, xbase, ybase,
+          L.mean_t, mean_norm, a.hb, tmpl128, tmpl256, off, ssd, b0, b1, mar);
     gn_update(L, a, PS, off, ssd, b0, b1, mar);
   }
 }
@@ -1162,9 +1206,13 @@ static void launch_gn_lane(const SearchArgs& a, const double* prep, unsigned* co
 constexpr size_t kGroupLanes8 = (size_t)148 * 2048 * 2;
 constexpr size_t kGroupLanes12 = (size_t)148 * 2048 * 4;
 
-size_t patch_search_scratch_bytes(int B, int P) {
-  return ((size_t)(kPrep + kSpillStride) * B * P) * sizeof(double) +
-         (kRangeCounters + kMaxGnBlocks) * sizeof(unsigned) + 256;
+static size_t search_state_bytes(int B, int P) {
+  return (((size_t)(kPrep + kSpillStride) * B * P) * sizeof(double) +
+          (kRangeCounters + kMaxGnBlocks) * sizeof(unsigned) + 255) & ~size_t(255);
+}
+
+size_t patch_search_scratch_bytes(int B, int P, int W, int H) {
+  return search_state_bytes(B, P) + (size_t)B * qpad_rows(H) * qpad_pitch(W) * sizeof(double);
 }
 
 void launch_patch_search(const SearchArgs& a, void* scratch, cudaStream_t st) {
@@ -1192,10 +1240,23 @@ void launch_patch_search(const SearchArgs& a, void* scratch, cudaStream_t st) {
       launch_gn_group<12, 16>(a, prep, counter, n, st);
     note_launch();
   } else if (a.ps == 8 || a.ps == 12) {
+    // the query level with its replicated border (see kQPad)
+    SearchArgs al = a;
+    double* qpad = reinterpret_cast<double*>(static_cast<char*>(scratch) +
+                                             search_state_bytes(a.B, a.ax.n * a.ay.n));
+    al.qpad = qpad;
+    al.qp_pitch = qpad_pitch(a.W);
+    {
+      const int half = al.qp_pitch / 2;
+      const unsigned bx = (unsigned)((half + 255) / 256);
+      k_pad_query<<<dim3(bx, (unsigned)qpad_rows(a.H), (unsigned)a.B), 256, 0, st>>>(
+          a.qry, a.W, a.H, qpad, al.qp_pitch);
+      note_launch();
+    }
     if (a.ps == 8)
-      launch_gn_lane<8>(a, prep, counter, spill, spill_count, n, st);
+      launch_gn_lane<8>(al, prep, counter, spill, spill_count, n, st);
     else
-      launch_gn_lane<12>(a, prep, counter, spill, spill_count, n, st);
+      launch_gn_lane<12>(al, prep, counter, spill, spill_count, n, st);
     note_launch();
     // parked (irregular-window) patches: a lane group per patch
     if (a.ps == 8)
