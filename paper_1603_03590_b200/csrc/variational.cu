@@ -809,12 +809,18 @@ static int sor_group_size(int hc, int ctas) {
   return p < S ? p : S;
 }
 
+// dynamic shared memory of a band of hc rows padded to hp (the kernel's
+// carve-out: ring slots of sor_ring_rows(hc) rows (+ the below-mode slot),
+// exchange rows, group-boundary du phases, barriers).  Exact, so two CTAs
+// of small bands still fit one SM (a 49-row band at P = 1 needs 93 KB; the
+// hp + 4 row bound it replaces came to 116 KB and cost c2's 1024x436 level
+// its second CTA per SM: 1.67 -> 2.35 ms)
 template <int S>
-static size_t sor_rows_smem_bytes(int hp, int P = 1) {
+static size_t sor_rows_smem_bytes(int hc, int hp, int P = 1) {
   const int G = (S + P - 1) / P;
-  // (TMA ring rows = sor_ring_rows(band) <= hp + 4 for any band of <= hp rows)
-  const size_t rrows = (size_t)hp + 4, xrows = (size_t)hp + 2;
-  return (size_t)ring_slots<S>() * (kChunks * rrows * 16 + kBelowSlot) + (size_t)2 * S * xrows * 16 +
+  const size_t rrows = (size_t)sor_ring_rows(hc), xrows = (size_t)hp + 2;
+  const size_t slot = kChunks * rrows * 16 + (sor_below_mode(hc) ? (size_t)kBelowSlot : 0);
+  return (size_t)ring_slots<S>() * slot + (size_t)2 * S * xrows * 16 +
          (size_t)3 * (G > 1 ? G - 1 : 1) * hp * 16 + (4 + ring_slots<S>()) * sizeof(uint64_t);
 }
 
@@ -831,7 +837,7 @@ static int choose_cluster(int B, int H) {
   const int max_rows = kMaxBandRows;
   int C = 1;
   while (C < 16 && ((H + C - 1) / C > max_rows || hp(C) > kMaxBandRows ||
-                    sor_rows_smem_bytes<S>(hp(C)) > kMaxSmem))
+                    sor_rows_smem_bytes<S>((H + C - 1) / C, hp(C)) > kMaxSmem))
     ++C;
   const int sms = device_sm_count();
   // while the batch leaves SMs idle, split the rows further (bands of >= 32
@@ -842,7 +848,8 @@ static int choose_cluster(int B, int H) {
   // bands of 60 rows run 12 % faster than 5 of 108)
   if (B * C > sms) {
     const int C64 = (H + 63) / 64;
-    if (C64 <= 16 && (long)C64 * 64 <= (long)C * hp(C) && sor_rows_smem_bytes<S>(64) * 2 <= kMaxSmem)
+    if (C64 <= 16 && (long)C64 * 64 <= (long)C * hp(C) &&
+        sor_rows_smem_bytes<S>((H + C64 - 1) / C64, 64) * 2 <= kMaxSmem)
       C = C64;
   }
   return C;
@@ -882,7 +889,7 @@ static int launch_sor_t(const RefineArgs& a, size_t Ls, const double* dui, const
   const int P = sor_group_size<S>(Hc, a.B * C);
   const int G = (S + P - 1) / P;
   const int threads = hp * G + 32;  // + the producer warp
-  const size_t smem = sor_rows_smem_bytes<S>(hp, P);
+  const size_t smem = sor_rows_smem_bytes<S>(Hc, hp, P);
   if (hp > kMaxBandRows || smem > kMaxSmem) return DIS_ERR_VALUE;
   using KFn = void (*)(const double*, int, int, int, int, size_t, double, const double*,
                        const double*, double*, double*, double*, double*, uint32_t*,
