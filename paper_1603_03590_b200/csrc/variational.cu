@@ -141,8 +141,37 @@ __device__ __forceinline__ void pixel_system(const RefineArgs& a, int b, int x, 
         wyp < 0.0 || wyp > H - 1.0)) {
     const BilinAt bl = bilin_at(W, H, wxp, wyp);
     const double iw = bilin_raster(qry, W, bl);
-    const double gxw = bilin_raster(qgx, W, bl);
-    const double gyw = bilin_raster(qgy, W, bl);
+    // a query gradient raster at the warped position, with its two second
+    // derivatives there: bilin_mix of dx_at / dy_at at the four corners.
+    // The corners' central differences share their operands, so the 16
+    // differences read 12 distinct pixels: rows y0, y1 at columns xL, x0,
+    // x1, xR and rows yT, yB at columns x0, x1 (xL = max(x0-1, 0), xR =
+    // min(x1+1, W-1), ...; at a clamped corner x1 == x0 the difference at
+    // x1 is the one at x0, as dx_at's own clamping gives).  Same operands,
+    // same operations: bit-identical to calling dx_at / dy_at per corner.
+    const int xL = bl.x0 > 0 ? bl.x0 - 1 : 0, xR = bl.x1 < W - 1 ? bl.x1 + 1 : W - 1;
+    const int yT = bl.y0 > 0 ? bl.y0 - 1 : 0, yB = bl.y1 < H - 1 ? bl.y1 + 1 : H - 1;
+    const bool cx = bl.x1 == bl.x0, cy = bl.y1 == bl.y0;
+    auto grad_at = [&](const double* __restrict__ f, double& fw, double& fxx, double& fxy) {
+      const double* r0 = f + (size_t)bl.y0 * W;
+      const double* r1 = f + (size_t)bl.y1 * W;
+      const double* rT = f + (size_t)yT * W;
+      const double* rB = f + (size_t)yB * W;
+      const double a0L = __ldg(r0 + xL), a00 = __ldg(r0 + bl.x0), a01 = __ldg(r0 + bl.x1),
+                   a0R = __ldg(r0 + xR);
+      const double a1L = __ldg(r1 + xL), a10 = __ldg(r1 + bl.x0), a11 = __ldg(r1 + bl.x1),
+                   a1R = __ldg(r1 + xR);
+      const double aT0 = __ldg(rT + bl.x0), aT1 = __ldg(rT + bl.x1);
+      const double aB0 = __ldg(rB + bl.x0), aB1 = __ldg(rB + bl.x1);
+      fw = bilin_mix(bl, a00, a01, a10, a11);
+      fxx = bilin_mix(bl, 0.5 * (a01 - a0L), 0.5 * (a0R - (cx ? a0L : a00)),
+                      0.5 * (a11 - a1L), 0.5 * (a1R - (cx ? a1L : a10)));
+      fxy = bilin_mix(bl, 0.5 * (a10 - aT0), 0.5 * (a11 - aT1), 0.5 * (aB0 - (cy ? aT0 : a00)),
+                      0.5 * (aB1 - (cy ? aT1 : a01)));
+    };
+    double gxw, qxx, qxy, gyw, qyx, qyy;
+    grad_at(qgx, gxw, qxx, qxy);
+    grad_at(qgy, gyw, qyx, qyy);
     const double rgxp = rgx[p], rgyp = rgy[p];
     const double ix = 0.5 * (rgxp + gxw);
     const double iy = 0.5 * (rgyp + gyw);
@@ -154,18 +183,6 @@ __device__ __forceinline__ void pixel_system(const RefineArgs& a, int b, int x, 
     t0yy = b0 * iy * iy;
     t0yz = b0 * iy * iz;
     t0zz = b0 * iz * iz;
-    // second derivatives: reference level at the pixel, query level sampled
-    // at the warped position from its four corners
-    const double qxx = bilin_mix(bl, dx_at(qgx, W, bl.x0, bl.y0), dx_at(qgx, W, bl.x1, bl.y0),
-                                 dx_at(qgx, W, bl.x0, bl.y1), dx_at(qgx, W, bl.x1, bl.y1));
-    const double qxy =
-        bilin_mix(bl, dy_at(qgx, W, H, bl.x0, bl.y0), dy_at(qgx, W, H, bl.x1, bl.y0),
-                  dy_at(qgx, W, H, bl.x0, bl.y1), dy_at(qgx, W, H, bl.x1, bl.y1));
-    const double qyx = bilin_mix(bl, dx_at(qgy, W, bl.x0, bl.y0), dx_at(qgy, W, bl.x1, bl.y0),
-                                 dx_at(qgy, W, bl.x0, bl.y1), dx_at(qgy, W, bl.x1, bl.y1));
-    const double qyy =
-        bilin_mix(bl, dy_at(qgy, W, H, bl.x0, bl.y0), dy_at(qgy, W, H, bl.x1, bl.y0),
-                  dy_at(qgy, W, H, bl.x0, bl.y1), dy_at(qgy, W, H, bl.x1, bl.y1));
     const double ixx = 0.5 * (dx_at(rgx, W, x, y) + qxx);
     const double ixy = 0.5 * (dy_at(rgx, W, H, x, y) + qxy);
     const double ixz = gxw - rgxp;
@@ -195,20 +212,15 @@ __device__ __forceinline__ void pixel_system(const RefineArgs& a, int b, int x, 
   r[6] = -(wi * t0yz + wg * tgyz);  // r1
 }
 
-// the smoothness weight of _assemble_system (variational.py:113-121)
-__device__ __forceinline__ double pixel_ws(const RefineArgs& a, int b, int x, int y) {
-  const int W = a.W, H = a.H;
-  const size_t plane = (size_t)W * H;
-  const double* __restrict__ u = a.fu + b * plane;
-  const double* __restrict__ v = a.fv + b * plane;
-  const int xm = x > 0 ? x - 1 : 0;
-  const int xp = x < W - 1 ? x + 1 : W - 1;
-  const int ym = y > 0 ? y - 1 : 0;
-  const int yp = y < H - 1 ? y + 1 : H - 1;
-  const double ux = 0.5 * (u[(size_t)y * W + xp] - u[(size_t)y * W + xm]);
-  const double uy = 0.5 * (u[(size_t)yp * W + x] - u[(size_t)ym * W + x]);
-  const double vx = 0.5 * (v[(size_t)y * W + xp] - v[(size_t)y * W + xm]);
-  const double vy = 0.5 * (v[(size_t)yp * W + x] - v[(size_t)ym * W + x]);
+// the smoothness weight of _assemble_system (variational.py:113-121) from
+// the flow at the pixel's four neighbours (clamped to the level like
+// image_gradients' one-sided forms: (x+1, x-1) -> (1, 0) at x = 0)
+__device__ __forceinline__ double pixel_ws(const RefineArgs& a, double2 l, double2 r, double2 t,
+                                          double2 d) {
+  const double ux = 0.5 * (r.x - l.x);
+  const double uy = 0.5 * (d.x - t.x);
+  const double vx = 0.5 * (r.y - l.y);
+  const double vy = 0.5 * (d.y - t.y);
   const double grad2 = ux * ux + uy * uy + vx * vx + vy * vy;
   const double eps2 = a.eps * a.eps;
   return a.alpha * 0.5 / sqrt(grad2 + eps2);
@@ -222,8 +234,10 @@ __device__ __forceinline__ double pixel_ws(const RefineArgs& a, int b, int x, in
 // 3 -> 4 blocks: c1 0.62 -> 0.57 ms, c3 10.7 -> 9.7 ms (5 blocks spill)
 __global__ void __launch_bounds__(256, 4) k_tensor_assemble(RefineArgs a, size_t Ls) {
   constexpr int HX = kTTX + 2, HY = kTTY + 2;
+  constexpr int FX = kTTX + 4, FY = kTTY + 4;
   constexpr int kPad = kChunks + 1;  // 7 x 16 B per staged record: conflict-free writes
   __shared__ double ws_t[HY][HX];
+  __shared__ double2 uv_t[FY][FX];  // the flow with a 2-pixel ring, clamped to the level
   __shared__ double2 rs[kTTY * kTTX][kPad];
   const int W = a.W, H = a.H;
   const int b = blockIdx.z;
@@ -231,20 +245,34 @@ __global__ void __launch_bounds__(256, 4) k_tensor_assemble(RefineArgs a, size_t
   const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
   const int x = X0 + lx, y = Y0 + ly;
   const bool inside = x < W && y < H;
-  // the pixel's flow first: its loads are in flight while the smoothness
-  // ring's are issued, and the system's warped gathers need only it (one
-  // memory latency fewer on each thread's chain than ring -> barrier ->
-  // system)
+  // the pixel's flow first: its loads are in flight while the flow tile's
+  // are issued, and the system's warped gathers need only it (one memory
+  // latency fewer on each thread's chain than tile -> barrier -> system)
   double up_ = 0.0, vp_ = 0.0;
   if (inside) {
     const size_t p = (size_t)b * W * H + (size_t)y * W + x;
     up_ = a.fu[p];
     vp_ = a.fv[p];
   }
+  {  // flow tile: each pixel read once (the ring's smoothness weights read
+     // their four neighbours from here instead of 8 gathers each)
+    const double* __restrict__ u = a.fu + (size_t)b * W * H;
+    const double* __restrict__ v = a.fv + (size_t)b * W * H;
+    for (int i = threadIdx.x; i < FX * FY; i += 256) {
+      const int fy = i / FX, fx = i - fy * FX;
+      const int xx = min(max(X0 - 2 + fx, 0), W - 1), yy = min(max(Y0 - 2 + fy, 0), H - 1);
+      const size_t q = (size_t)yy * W + xx;
+      uv_t[fy][fx] = make_double2(u[q], v[q]);
+    }
+  }
+  __syncthreads();
   for (int i = threadIdx.x; i < HX * HY; i += 256) {
     const int hy = i / HX, hx = i - hy * HX;
     const int xx = X0 - 1 + hx, yy = Y0 - 1 + hy;
-    ws_t[hy][hx] = (xx >= 0 && xx < W && yy >= 0 && yy < H) ? pixel_ws(a, b, xx, yy) : 0.0;
+    ws_t[hy][hx] = (xx >= 0 && xx < W && yy >= 0 && yy < H)
+                       ? pixel_ws(a, uv_t[hy + 1][hx], uv_t[hy + 1][hx + 2], uv_t[hy][hx + 1],
+                                  uv_t[hy + 2][hx + 1])
+                       : 0.0;
   }
   double r[7];
   if (inside) pixel_system(a, b, x, y, up_, vp_, r);
