@@ -185,6 +185,29 @@ DIS_API int dis_stereo_batch_host(const void* host_left, const void* host_right,
                                   const dis_params_t* p, double* host_flow_out,
                                   void* workspace, size_t workspace_bytes, void* stream);
 
+/* The same calls split in two, for callers that keep several batches in
+ * flight (the reference's dis_flow, pipeline.py:150-163, is one blocking call
+ * per pair; a streaming caller double-buffers): *_async enqueues the whole
+ * call (copies in, kernels, copies out, ordered after prior work on
+ * `stream`) and returns without waiting; dis_host_batch_finish waits for
+ * `stream` and converts the call's status words (copied to pinned host
+ * memory behind the flow) into the return code dis_flow_batch_host would
+ * have given.  Between the two the host buffers and the workspace belong to
+ * the call.  Calls in flight at the same time need their own workspace, host
+ * buffers and stream each; their copies share the PCIe link in call order
+ * and their kernels overlap, so one call's copy-out hides the next call's
+ * copy-in and compute.  dis_flow_batch_host == *_async + finish. */
+DIS_API int dis_flow_batch_host_async(const void* host_frame1, const void* host_frame2,
+                                      int32_t dtype, int32_t B, int32_t H, int32_t W,
+                                      const dis_params_t* p, double* host_flow_out,
+                                      void* workspace, size_t workspace_bytes, void* stream);
+DIS_API int dis_stereo_batch_host_async(const void* host_left, const void* host_right,
+                                        int32_t dtype, int32_t B, int32_t H, int32_t W,
+                                        const dis_params_t* p, double* host_flow_out,
+                                        void* workspace, size_t workspace_bytes, void* stream);
+DIS_API int dis_host_batch_finish(const void* workspace, int32_t B, int32_t H, int32_t W,
+                                  int32_t dtype, const dis_params_t* p, void* stream);
+
 /* sparse_correspondences (pipeline.py:230-287) for one pair: displacements
  * at `n_seeds` seed locations (host (n, 2) x, y in full-resolution pixels)
  * -> host (n, 2) displacements and (n) validity flags.  Seeds outside the

@@ -44,6 +44,7 @@ EXPORTED = (
     "dis_sparse_correspondences", "dis_flow_batch_levels", "dis_profile_log",
     "dis_precompute_patch_set", "dis_optimize_patch_set", "dis_refresh_patch_stats",
     "dis_init_patches", "dis_reset_outliers",
+    "dis_flow_batch_host_async", "dis_stereo_batch_host_async", "dis_host_batch_finish",
 )
 
 KERNEL_CLASSES = ("pyramid", "patch_search", "densify", "tensor_assemble", "sor", "upsample")
@@ -106,6 +107,12 @@ def lib() -> ctypes.CDLL:
     L.dis_stereo_batch.restype = ctypes.c_int
     L.dis_stereo_batch_host.argtypes = L.dis_flow_batch_host.argtypes
     L.dis_stereo_batch_host.restype = ctypes.c_int
+    L.dis_flow_batch_host_async.argtypes = L.dis_flow_batch_host.argtypes
+    L.dis_flow_batch_host_async.restype = ctypes.c_int
+    L.dis_stereo_batch_host_async.argtypes = L.dis_flow_batch_host.argtypes
+    L.dis_stereo_batch_host_async.restype = ctypes.c_int
+    L.dis_host_batch_finish.argtypes = [_vp, _i32, _i32, _i32, _i32, _pp, _vp]
+    L.dis_host_batch_finish.restype = ctypes.c_int
     L.dis_densify_bidirectional_workspace_bytes.argtypes = [_i32, _i32, _i32, _pp]
     L.dis_densify_bidirectional_workspace_bytes.restype = _sz
     L.dis_densify_bidirectional.argtypes = [_vp, _vp, _i32, _i32, _i32, _pp] + [_vp] * 9 + [

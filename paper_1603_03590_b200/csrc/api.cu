@@ -668,6 +668,30 @@ struct HostStreams {
 };
 std::mutex g_host_mu;
 HostStreams g_host[16];
+// The chunks' status words of a host-buffer call land in a small pinned
+// array owned by the library (one per workspace address), copied on the
+// out stream behind each chunk's flow: finishing a call then needs no
+// device read of its own (a blocking 4-byte copy would queue behind the
+// flow copies of another call in flight).
+struct HostStatus {
+  const void* ws;
+  uint32_t* pinned;
+};
+std::vector<HostStatus> g_host_status;  // guarded by g_host_mu
+uint32_t* host_status_for(const void* ws, bool create) {
+  for (const HostStatus& h : g_host_status)
+    if (h.ws == ws) return h.pinned;
+  if (!create) return nullptr;
+  uint32_t* pinned = nullptr;
+  if (cudaHostAlloc(reinterpret_cast<void**>(&pinned), kHostChunksMax * sizeof(uint32_t),
+                    cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  std::memset(pinned, 0, kHostChunksMax * sizeof(uint32_t));
+  g_host_status.push_back({ws, pinned});
+  return pinned;
+}
 }  // namespace
 
 size_t dis_host_workspace_bytes(int32_t B, int32_t H, int32_t W, int32_t dtype,
@@ -711,7 +735,10 @@ int flow_batch_impl(const void* frame1, const void* frame2, int32_t dtype, int32
 
 int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dtype, int32_t B,
                     int32_t H, int32_t W, const dis_params_t* p, double* host_flow_out,
-                    void* workspace, size_t workspace_bytes, void* stream, bool stereo);
+                    void* workspace, size_t workspace_bytes, void* stream, bool stereo,
+                    bool wait = true);
+int host_batch_finish(const void* workspace, int32_t B, int32_t H, int32_t W, int32_t dtype,
+                      const dis_params_t* p, void* stream);
 }  // namespace
 
 extern "C" {
@@ -804,6 +831,28 @@ int dis_stereo_batch_host(const void* host_left, const void* host_right, int32_t
                          workspace_bytes, stream, true);
 }
 
+
+int dis_flow_batch_host_async(const void* host_frame1, const void* host_frame2, int32_t dtype,
+                              int32_t B, int32_t H, int32_t W, const dis_params_t* p,
+                              double* host_flow_out, void* workspace, size_t workspace_bytes,
+                              void* stream) {
+  return host_batch_impl(host_frame1, host_frame2, dtype, B, H, W, p, host_flow_out, workspace,
+                         workspace_bytes, stream, false, false);
+}
+
+int dis_stereo_batch_host_async(const void* host_left, const void* host_right, int32_t dtype,
+                                int32_t B, int32_t H, int32_t W, const dis_params_t* p,
+                                double* host_flow_out, void* workspace, size_t workspace_bytes,
+                                void* stream) {
+  return host_batch_impl(host_left, host_right, dtype, B, H, W, p, host_flow_out, workspace,
+                         workspace_bytes, stream, true, false);
+}
+
+int dis_host_batch_finish(const void* workspace, int32_t B, int32_t H, int32_t W, int32_t dtype,
+                          const dis_params_t* p, void* stream) {
+  return host_batch_finish(workspace, B, H, W, dtype, p, stream);
+}
+
 }  // extern "C"
 
 namespace {
@@ -889,7 +938,8 @@ void host_trace_print() {
 
 int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dtype, int32_t B,
                     int32_t H, int32_t W, const dis_params_t* p, double* host_flow_out,
-                    void* workspace, size_t workspace_bytes, void* stream, bool stereo) {
+                    void* workspace, size_t workspace_bytes, void* stream, bool stereo,
+                    bool wait) {
   int rc = dis_params_validate(p);
   if (rc) return rc;
   if (!stereo && p->mode == 1)
@@ -904,7 +954,7 @@ int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dt
   const size_t per = host_chunk_bytes(cp.bmax, H, W, dtype, p);
   int dev = 0;
   cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> guard(g_host_mu);
+  std::unique_lock<std::mutex> guard(g_host_mu);
   HostStreams& hs = g_host[dev & 15];
   if (hs.dev != dev) {
     // the first (small) chunks get the highest stream priority: the flow's
@@ -990,15 +1040,46 @@ int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dt
                             workspace, st, stereo, cp, per, &used);
     if (rc) return rc;
   }
-  cudaError_t e = cudaStreamSynchronize(st);
+  (void)used;
+  if (!wait) return DIS_OK;  // the caller finishes the call with dis_host_batch_finish
+  guard.unlock();
+  return host_batch_finish(workspace, B, H, W, dtype, p, stream);
+}
+
+// The blocking half of a host-buffer call: wait for the stream the call was
+// enqueued on (its flow copies have then landed in the host buffer) and turn
+// the chunks' status words into a return code.
+int host_batch_finish(const void* workspace, int32_t B, int32_t H, int32_t W, int32_t dtype,
+                      const dis_params_t* p, void* stream) {
+  int rc = dis_params_validate(p);
+  if (rc) return rc;
+  if (!workspace) return fail(DIS_ERR_VALUE, "workspace is NULL");
+  rc = check_dims(p, B, H, W);
+  if (rc) return rc;
+  const ChunkPlan cp = host_chunks(B);
+  const size_t per = host_chunk_bytes(cp.bmax, H, W, dtype, p);
+  int used = 0;
+  for (int c = 0; c < cp.n; ++c)
+    if (cp.first[c + 1] - cp.first[c] > 0) ++used;
+  cudaError_t e = cudaStreamSynchronize(as_stream(stream));
   if (e != cudaSuccess) return fail(DIS_ERR_CUDA, "dis_flow_batch_host: %s", cudaGetErrorString(e));
   if (host_trace_on()) host_trace_print();
   uint32_t any = 0;
+  const uint32_t* hst = nullptr;
+  {
+    std::lock_guard<std::mutex> guard(g_host_mu);
+    hst = host_status_for(workspace, false);
+  }
   for (int c = 0; c < used; ++c) {
     uint32_t status = 0;
-    e = cudaMemcpy(&status, static_cast<char*>(workspace) + (size_t)c * per, sizeof(uint32_t),
-                   cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) return fail(DIS_ERR_CUDA, "dis_flow_batch_host: %s", cudaGetErrorString(e));
+    if (hst) {
+      status = hst[c];
+    } else {
+      e = cudaMemcpy(&status, static_cast<const char*>(workspace) + (size_t)c * per,
+                     sizeof(uint32_t), cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess)
+        return fail(DIS_ERR_CUDA, "dis_flow_batch_host: %s", cudaGetErrorString(e));
+    }
     any |= status;
   }
   return dis_status_to_error(any);
@@ -1021,6 +1102,7 @@ int host_batch_enqueue(const void* host_frame1, const void* host_frame2, int32_t
   // engine interleaving the chunks); each chunk's kernels on its own stream
   // so that they overlap each other and the copies
   const int Bc = cp.bmax;
+  uint32_t* hst = host_status_for(workspace, true);  // (the caller holds g_host_mu)
   cudaStreamWaitEvent(hs.in, hs.start, 0);
   cudaStreamWaitEvent(hs.out, hs.start, 0);
   for (int c = 0; c < cp.n; ++c) {
@@ -1051,6 +1133,8 @@ int host_batch_enqueue(const void* host_frame1, const void* host_frame2, int32_t
     cudaStreamWaitEvent(hs.out, hs.computed[c], 0);
     cudaMemcpyAsync(host_flow_out + (size_t)b0 * px * 2, dout, obytes, cudaMemcpyDeviceToHost,
                     hs.out);
+    if (hst)
+      cudaMemcpyAsync(hst + c, wsc, sizeof(uint32_t), cudaMemcpyDeviceToHost, hs.out);
     if (host_trace_on()) host_trace_mark(c, hs.in, cs, hs.out);
   }
   cudaEventRecord(hs.done[0], hs.out);

@@ -118,6 +118,7 @@ class FlowEngine:
         self.workspace = torch.empty(self.workspace_bytes, dtype=torch.uint8,
                                      device=self.device)
         self._host_ws = None
+        self._pending = None  # (frames, out, dtype code, stream) of a submitted host batch
 
     # -- device-resident path ------------------------------------------------
     def run(self, frames1, frames2, out=None, stream=None, check: bool = True,
@@ -214,10 +215,12 @@ class FlowEngine:
 
     # -- host-buffer path (the e2e boundary) ---------------------------------
     def run_host(self, frames1: np.ndarray, frames2: np.ndarray, out: np.ndarray | None = None,
-                 stream=None) -> np.ndarray:
+                 stream=None, submit_only: bool = False) -> np.ndarray:
         """dis_flow_batch_host: host frames in, host flow out (copies
         included).  Pinned host buffers (torch ``pin_memory``) are fastest."""
         torch = _torch()
+        if self._pending is not None:
+            raise RuntimeError("run_host: a submitted batch is still in flight (finish_host)")
         a, b = _promote_pair_np(np.asarray(frames1), np.asarray(frames2))
         if a.ndim == 2:
             a = a[None]
@@ -242,10 +245,46 @@ class FlowEngine:
                                            ctypes.byref(self.cparams))
             if self._host_ws is None or self._host_ws.numel() < n:
                 self._host_ws = torch.empty(int(n), dtype=torch.uint8, device=self.device)
-            fn = L.dis_stereo_batch_host if self.stereo else L.dis_flow_batch_host
+            if submit_only:
+                fn = L.dis_stereo_batch_host_async if self.stereo else L.dis_flow_batch_host_async
+            else:
+                fn = L.dis_stereo_batch_host if self.stereo else L.dis_flow_batch_host
             rc = fn(a.ctypes.data, b.ctypes.data, code, self.B, self.H, self.W,
                     ctypes.byref(self.cparams), out.ctypes.data, self._host_ws.data_ptr(),
                     int(n), _lib.stream_handle(stream))
+        _lib.check(rc)
+        if submit_only:
+            # the call owns its buffers until finish_host: keep them alive
+            self._pending = (a, b, out, code, stream)
+        return out
+
+    def submit_host(self, frames1: np.ndarray, frames2: np.ndarray, out: np.ndarray,
+                    stream=None) -> None:
+        """dis_flow_batch_host_async: enqueue a host-buffer batch (copies in,
+        kernels, copies out, ordered after prior work on ``stream``) and return
+        without waiting.  ``out`` (and the frames) belong to the call until
+        ``finish_host`` returns.  Engines submitted on different streams run
+        concurrently: a streaming caller keeps two engines in flight so one
+        batch's copy-out overlaps the next batch's copy-in and kernels.  An
+        engine has one workspace, hence one call in flight."""
+        if self._pending is not None:
+            raise RuntimeError("submit_host: the engine's previous batch was not finished "
+                               "(finish_host)")
+        if out is None:
+            raise ValueError("submit_host needs the output buffer")
+        self.run_host(frames1, frames2, out=out, stream=stream, submit_only=True)
+
+    def finish_host(self) -> np.ndarray:
+        """dis_host_batch_finish: wait for the submitted batch, raise what
+        ``run_host`` would have raised, return its ``out``."""
+        if self._pending is None:
+            raise RuntimeError("finish_host: nothing was submitted")
+        _a, _b, out, code, stream = self._pending
+        self._pending = None
+        L = _lib.lib()
+        with _torch().cuda.device(self.device):
+            rc = L.dis_host_batch_finish(self._host_ws.data_ptr(), self.B, self.H, self.W, code,
+                                         ctypes.byref(self.cparams), _lib.stream_handle(stream))
         _lib.check(rc)
         return out
 
