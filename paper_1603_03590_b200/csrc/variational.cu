@@ -314,14 +314,31 @@ __global__ void __launch_bounds__(256, 4) k_tensor_assemble(RefineArgs a, size_t
   double2* __restrict__ out = reinterpret_cast<double2*>(a.rec + (size_t)b * Ls * kRec);
   const int wy = threadIdx.x & 7;
   const int oy = Y0 + wy;
-  for (int m = (threadIdx.x >> 3); m < npairs; m += 32) {
-    const int dd = m / kChunks;
-    const int c = m - dd * kChunks;
-    const int lxx = dd - wy;
-    const int ox = X0 + lxx;
-    if (lxx < 0 || lxx >= kTTX || ox >= W || oy >= H) continue;
-    const size_t d = (size_t)(ox + oy);
-    out[(d * kChunks + c) * H + oy] = rs[wy * kTTX + lxx][c];
+  if (oy < H) {
+    // (diagonal, chunk) pair m = dd * kChunks + c of the tile: its global run
+    // starts at ((X0 + Y0) * kChunks + m) * H — linear in m, so the output
+    // pointer advances by a constant; dd and c step by 32 = 5 * kChunks + 2
+    static_assert(kChunks == 6, "pair stepping below");
+    const int m0 = threadIdx.x >> 3;
+    int dd = m0 / kChunks;
+    int c = m0 - dd * kChunks;
+    const unsigned xlim = (unsigned)min(kTTX, W - X0);  // tile columns inside the level
+    double2* __restrict__ o = out + ((size_t)(X0 + Y0) * kChunks + m0) * H + oy;
+    const double2* src = &rs[wy * kTTX][0] + (dd - wy) * kPad + c;
+    const size_t ostep = (size_t)32 * H;
+#pragma unroll 2
+    for (int m = m0; m < npairs; m += 32) {
+      if ((unsigned)(dd - wy) < xlim) *o = *src;
+      o += ostep;
+      c += 2;
+      dd += 5;
+      src += 5 * kPad + 2;
+      if (c >= kChunks) {
+        c -= kChunks;
+        dd += 1;
+        src += kPad - kChunks;
+      }
+    }
   }
 }
 
