@@ -655,6 +655,26 @@ def measure(cfg, params, args, dev, rank, world, steps, e2e_steps, tag):
                        "blocking": blocking}
             elif pipe and "error" in pipe:
                 e2e["pipelined_error"] = pipe["error"]
+            # side number, NOT the headline: the same float64 computation with the
+            # flow rounded to float32 on the device before the copy-out (opt-in
+            # DIS_HOST_FLOW_F32; the copy-out bounds this path, this halves it)
+            if ok and p_s > 0 and not args.no_f32_out:
+                try:
+                    p32 = e2e_pipelined(cfg, params, dev, eng, B, h1, h2, ho,
+                                        out if eng else None, max(2 * e2e_steps, 6), f32=True)
+                except Exception as exc:
+                    p32 = {"error": f"{type(exc).__name__}: {exc}"}
+                s32 = sharding.max_over_ranks(p32.get("s_per_step", 0.0), device=dev)
+                ok32 = sharding.max_over_ranks(0.0 if "s_per_step" in p32 else 1.0,
+                                               device=dev) == 0.0
+                if ok32 and s32 > 0:
+                    e2e["float32_flow_out"] = {
+                        "value": total / s32, "unit": UNIT, "ms_per_step": 1e3 * s32,
+                        "d2h_bytes_per_step": int(d2h) // 2,
+                        "note": "not the headline: same float64 pipeline, flow rounded to "
+                                "float32 on the device before the copy-out "
+                                "(out=float32, DIS_HOST_FLOW_F32; == flow.astype(float32)); "
+                                "two calls in flight"}
     res = {"value": value, "ms_per_step": ms_step, "pairs_rank": B, "pairs_total": total,
            "e2e": e2e, "roofline": roofline, "kernels": kernels, "clocks": clk,
            "gpu_launches": launches_per_step * steps,
@@ -671,7 +691,7 @@ def measure(cfg, params, args, dev, rank, world, steps, e2e_steps, tag):
     return res
 
 
-def e2e_pipelined(cfg, params, dev, eng, B, h1, h2, ho, dev_out, steps):
+def e2e_pipelined(cfg, params, dev, eng, B, h1, h2, ho, dev_out, steps, f32=False):
     """Host-buffer calls with two in flight (FlowEngine.submit_host /
     finish_host).  Engines of the config's batch when two of their workspaces
     fit comfortably beside what is resident, else of half the batch (two
@@ -700,8 +720,11 @@ def e2e_pipelined(cfg, params, dev, eng, B, h1, h2, ho, dev_out, steps):
     calls_per_step = B // Be
     engs = [FlowEngine(Be, cfg.height, cfg.width, params, device=dev) for _ in range(2)]
     streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+    if f32:  # the opt-in float32 flow (DIS_HOST_FLOW_F32): its own pinned outputs
+        ho = torch.empty(ho.shape, dtype=torch.float32).pin_memory().numpy()
+    odt = torch.float32 if f32 else torch.float64
     if Be == B:  # each slot its own pinned output; the (read-only) frames are shared
-        outs = [ho, torch.empty(ho.shape, dtype=torch.float64).pin_memory().numpy()]
+        outs = [ho, torch.empty(ho.shape, dtype=odt).pin_memory().numpy()]
         ins = [(h1, h2), (h1, h2)]
     else:        # each slot one half of the pinned buffers
         outs = [ho[:Be], ho[Be:]]
@@ -733,7 +756,8 @@ def e2e_pipelined(cfg, params, dev, eng, B, h1, h2, ho, dev_out, steps):
     for k in range(2):  # first and last pair of each slot against the device-path flow
         base = 0 if Be == B else k * Be
         for i in (0, Be - 1):
-            same = same and np.array_equal(outs[k][i], dev_out[base + i].cpu().numpy())
+            want = dev_out[base + i].cpu().numpy()
+            same = same and np.array_equal(outs[k][i], want.astype(np.float32) if f32 else want)
     assert same, "pipelined host path != device path"
     del engs
     torch.cuda.empty_cache()
@@ -868,6 +892,8 @@ def main(argv=None):
     ap.add_argument("--batch", type=int, default=0,
                     help="pairs per GPU (weak configs) / in total (strong); default: config")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-f32-out", action="store_true",
+                    help="e2e: skip the float32-flow-out side measurement")
     ap.add_argument("--no-pipelined", action="store_true",
                     help="e2e: blocking calls only (skip the two-in-flight measurement)")
     ap.add_argument("--no-graph", action="store_true",

@@ -208,6 +208,26 @@ DIS_API int dis_stereo_batch_host_async(const void* host_left, const void* host_
 DIS_API int dis_host_batch_finish(const void* workspace, int32_t B, int32_t H, int32_t W,
                                   int32_t dtype, const dis_params_t* p, void* stream);
 
+/* The general host-buffer entry point: dis_flow_batch_host with flags.
+ *   DIS_HOST_ASYNC     enqueue only (finish with dis_host_batch_finish)
+ *   DIS_HOST_STEREO    dis_stereo (pipeline.py:166-183) instead of dis_flow
+ *   DIS_HOST_FLOW_F32  host_flow_out is float32 (B, H, W, 2): the float64 flow
+ *                      of the same computation, rounded to nearest on the
+ *                      device before the copy-out (== numpy's
+ *                      flow.astype(float32); rounding error <= 2^-18 px for
+ *                      |flow| < 64 px).  Halves the device->host bytes, which
+ *                      bound the host path; not the reference's return type,
+ *                      so opt-in.
+ * flags = 0 is dis_flow_batch_host. */
+#define DIS_HOST_ASYNC 1u
+#define DIS_HOST_FLOW_F32 2u
+#define DIS_HOST_STEREO 4u
+DIS_API int dis_flow_batch_host_ex(const void* host_frame1, const void* host_frame2,
+                                   int32_t dtype, int32_t B, int32_t H, int32_t W,
+                                   const dis_params_t* p, void* host_flow_out,
+                                   void* workspace, size_t workspace_bytes, void* stream,
+                                   uint32_t flags);
+
 /* sparse_correspondences (pipeline.py:230-287) for one pair: displacements
  * at `n_seeds` seed locations (host (n, 2) x, y in full-resolution pixels)
  * -> host (n, 2) displacements and (n) validity flags.  Seeds outside the

@@ -28,6 +28,8 @@ DIS_ERR_CUDA = -5
 DIS_ERR_WORKSPACE = -6
 
 DTYPE_F32, DTYPE_F64, DTYPE_U8 = 0, 1, 2
+# dis_flow_batch_host_ex flags
+HOST_ASYNC, HOST_FLOW_F32, HOST_STEREO = 1, 2, 4
 
 # every symbol include/dis_b200.h declares
 EXPORTED = (
@@ -45,6 +47,7 @@ EXPORTED = (
     "dis_precompute_patch_set", "dis_optimize_patch_set", "dis_refresh_patch_stats",
     "dis_init_patches", "dis_reset_outliers",
     "dis_flow_batch_host_async", "dis_stereo_batch_host_async", "dis_host_batch_finish",
+    "dis_flow_batch_host_ex",
 )
 
 KERNEL_CLASSES = ("pyramid", "patch_search", "densify", "tensor_assemble", "sor", "upsample")
@@ -111,6 +114,8 @@ def lib() -> ctypes.CDLL:
     L.dis_flow_batch_host_async.restype = ctypes.c_int
     L.dis_stereo_batch_host_async.argtypes = L.dis_flow_batch_host.argtypes
     L.dis_stereo_batch_host_async.restype = ctypes.c_int
+    L.dis_flow_batch_host_ex.argtypes = L.dis_flow_batch_host.argtypes + [ctypes.c_uint32]
+    L.dis_flow_batch_host_ex.restype = ctypes.c_int
     L.dis_host_batch_finish.argtypes = [_vp, _i32, _i32, _i32, _i32, _pp, _vp]
     L.dis_host_batch_finish.restype = ctypes.c_int
     L.dis_densify_bidirectional_workspace_bytes.argtypes = [_i32, _i32, _i32, _pp]

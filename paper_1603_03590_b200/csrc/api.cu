@@ -736,7 +736,7 @@ int flow_batch_impl(const void* frame1, const void* frame2, int32_t dtype, int32
 int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dtype, int32_t B,
                     int32_t H, int32_t W, const dis_params_t* p, double* host_flow_out,
                     void* workspace, size_t workspace_bytes, void* stream, bool stereo,
-                    bool wait = true);
+                    bool wait = true, bool f32 = false);
 int host_batch_finish(const void* workspace, int32_t B, int32_t H, int32_t W, int32_t dtype,
                       const dis_params_t* p, void* stream);
 }  // namespace
@@ -853,6 +853,18 @@ int dis_host_batch_finish(const void* workspace, int32_t B, int32_t H, int32_t W
   return host_batch_finish(workspace, B, H, W, dtype, p, stream);
 }
 
+int dis_flow_batch_host_ex(const void* host_frame1, const void* host_frame2, int32_t dtype,
+                           int32_t B, int32_t H, int32_t W, const dis_params_t* p,
+                           void* host_flow_out, void* workspace, size_t workspace_bytes,
+                           void* stream, uint32_t flags) {
+  if (flags & ~(uint32_t)(DIS_HOST_ASYNC | DIS_HOST_FLOW_F32 | DIS_HOST_STEREO))
+    return fail(DIS_ERR_VALUE, "dis_flow_batch_host_ex: unknown flags 0x%x", flags);
+  return host_batch_impl(host_frame1, host_frame2, dtype, B, H, W, p,
+                         static_cast<double*>(host_flow_out), workspace, workspace_bytes, stream,
+                         (flags & DIS_HOST_STEREO) != 0, !(flags & DIS_HOST_ASYNC),
+                         (flags & DIS_HOST_FLOW_F32) != 0);
+}
+
 }  // extern "C"
 
 namespace {
@@ -870,6 +882,7 @@ struct HostGraph {
   void* stream = nullptr;
   int32_t dtype = -1, B = 0, H = 0, W = 0;
   bool stereo = false;
+  bool f32 = false;
   int dev = -1;
   dis_params_t p{};
   int seen = 0;
@@ -900,7 +913,7 @@ bool is_pinned(const void* ptr) {
 int host_batch_enqueue(const void* host_frame1, const void* host_frame2, int32_t dtype,
                        int32_t B, int32_t H, int32_t W, const dis_params_t* p,
                        double* host_flow_out, void* workspace, cudaStream_t st, bool stereo,
-                       const ChunkPlan& cp, size_t per, int* used_out);
+                       const ChunkPlan& cp, size_t per, int* used_out, bool f32);
 
 // experiments only (DIS_HOST_TRACE=1 with DIS_HOST_GRAPH=0): per-chunk event
 // times (frames landed, kernels done, flow copied) printed after each call
@@ -939,7 +952,7 @@ void host_trace_print() {
 int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dtype, int32_t B,
                     int32_t H, int32_t W, const dis_params_t* p, double* host_flow_out,
                     void* workspace, size_t workspace_bytes, void* stream, bool stereo,
-                    bool wait) {
+                    bool wait, bool f32) {
   int rc = dis_params_validate(p);
   if (rc) return rc;
   if (!stereo && p->mode == 1)
@@ -983,7 +996,7 @@ int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dt
       HostGraph& g = g_hgraph[i];
       if (g.f1 == host_frame1 && g.f2 == host_frame2 && g.out == host_flow_out &&
           g.ws == workspace && g.stream == stream && g.dtype == dtype && g.B == B && g.H == H &&
-          g.W == W && g.stereo == stereo && g.dev == dev &&
+          g.W == W && g.stereo == stereo && g.f32 == f32 && g.dev == dev &&
           std::memcmp(&g.p, p, sizeof(dis_params_t)) == 0) {
         hg = &g;
         break;
@@ -1004,6 +1017,7 @@ int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dt
       hg->H = H;
       hg->W = W;
       hg->stereo = stereo;
+      hg->f32 = f32;
       hg->dev = dev;
       hg->p = *p;
     }
@@ -1019,7 +1033,7 @@ int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dt
     if (cudaStreamBeginCapture(hs.cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
       return fail(DIS_ERR_CUDA, "dis_flow_batch_host: stream capture failed");
     rc = host_batch_enqueue(host_frame1, host_frame2, dtype, B, H, W, p, host_flow_out,
-                            workspace, hs.cap, stereo, cp, per, &used);
+                            workspace, hs.cap, stereo, cp, per, &used, f32);
     const cudaError_t ce = cudaStreamEndCapture(hs.cap, &graph);
     if (rc) {
       if (graph) cudaGraphDestroy(graph);
@@ -1037,7 +1051,7 @@ int host_batch_impl(const void* host_frame1, const void* host_frame2, int32_t dt
   } else {
     if (hg) ++hg->seen;
     rc = host_batch_enqueue(host_frame1, host_frame2, dtype, B, H, W, p, host_flow_out,
-                            workspace, st, stereo, cp, per, &used);
+                            workspace, st, stereo, cp, per, &used, f32);
     if (rc) return rc;
   }
   (void)used;
@@ -1087,7 +1101,7 @@ int host_batch_finish(const void* workspace, int32_t B, int32_t H, int32_t W, in
 int host_batch_enqueue(const void* host_frame1, const void* host_frame2, int32_t dtype,
                        int32_t B, int32_t H, int32_t W, const dis_params_t* p,
                        double* host_flow_out, void* workspace, cudaStream_t st, bool stereo,
-                       const ChunkPlan& cp, size_t per, int* used_out) {
+                       const ChunkPlan& cp, size_t per, int* used_out, bool f32) {
   int dev = 0;
   cudaGetDevice(&dev);
   HostStreams& hs = g_host[dev & 15];
@@ -1131,8 +1145,21 @@ int host_batch_enqueue(const void* host_frame1, const void* host_frame2, int32_t
     launches += g_launches.load();
     cudaEventRecord(hs.computed[c], cs);
     cudaStreamWaitEvent(hs.out, hs.computed[c], 0);
-    cudaMemcpyAsync(host_flow_out + (size_t)b0 * px * 2, dout, obytes, cudaMemcpyDeviceToHost,
-                    hs.out);
+    if (f32) {
+      // the flow rounded to float32 on the device (round to nearest, like
+      // numpy's astype): half the copy-out.  The staging area is the head of
+      // the chunk's pipeline workspace, free once its kernels are done.
+      float* d32 = reinterpret_cast<float*>(wsc + 256);
+      launch_flow_to_f32(dout, d32, (size_t)bn * px * 2, cs);
+      ++launches;
+      cudaEventRecord(hs.computed[c], cs);
+      cudaStreamWaitEvent(hs.out, hs.computed[c], 0);
+      cudaMemcpyAsync(reinterpret_cast<float*>(host_flow_out) + (size_t)b0 * px * 2, d32,
+                      obytes / 2, cudaMemcpyDeviceToHost, hs.out);
+    } else {
+      cudaMemcpyAsync(host_flow_out + (size_t)b0 * px * 2, dout, obytes, cudaMemcpyDeviceToHost,
+                      hs.out);
+    }
     if (hst)
       cudaMemcpyAsync(hst + c, wsc, sizeof(uint32_t), cudaMemcpyDeviceToHost, hs.out);
     if (host_trace_on()) host_trace_mark(c, hs.in, cs, hs.out);

@@ -143,6 +143,7 @@ void launch_upsample(const double* iu, const double* iv, int B, int W, int H, do
                      cudaStream_t st);
 void launch_interleave(const double* u, const double* v, int B, int W, int H, double* out,
                        cudaStream_t st);
+void launch_flow_to_f32(const double* in, float* out, size_t n, cudaStream_t st);
 
 // sparse.cu — sparse_correspondences (pipeline.py:202-287)
 struct SparseChainArgs {

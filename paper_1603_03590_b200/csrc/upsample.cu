@@ -118,4 +118,23 @@ void launch_interleave(const double* u, const double* v, int B, int W, int H, do
   note_launch();
 }
 
+// the flow rounded to float32 (round to nearest even, numpy's astype) for
+// the host path's half-size copy-out; n doubles, n even
+__global__ void __launch_bounds__(256) k_flow_to_f32(const double2* __restrict__ in,
+                                                     float2* __restrict__ out, size_t n2) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const double2 v = in[i];
+    out[i] = make_float2(__double2float_rn(v.x), __double2float_rn(v.y));
+  }
+}
+
+void launch_flow_to_f32(const double* in, float* out, size_t n, cudaStream_t st) {
+  prof_begin(KC_UPSAMPLE, st);
+  k_flow_to_f32<<<blocks_for(n / 2), 256, 0, st>>>(reinterpret_cast<const double2*>(in),
+                                                    reinterpret_cast<float2*>(out), n / 2);
+  prof_end(KC_UPSAMPLE, st);
+  note_launch();
+}
+
 }  // namespace disb200

@@ -233,9 +233,14 @@ class FlowEngine:
         if out is None:
             out = np.empty((self.B, self.H, self.W, 2), dtype=np.float64)
         elif (not isinstance(out, np.ndarray) or out.shape != want + (2,)
-              or out.dtype != np.float64 or not out.flags.c_contiguous or not out.flags.writeable):
-            raise ValueError(f"out must be a writeable C-contiguous float64 array of shape "
-                             f"{want + (2,)}")
+              or out.dtype not in (np.float64, np.float32) or not out.flags.c_contiguous
+              or not out.flags.writeable):
+            raise ValueError(f"out must be a writeable C-contiguous float64 (or, opt-in, "
+                             f"float32) array of shape {want + (2,)}")
+        # a float32 `out` asks for the float64 flow rounded on the device before
+        # the copy-out (DIS_HOST_FLOW_F32: == flow.astype(float32), half the
+        # device->host bytes); the default float64 is the reference's return type
+        f32 = out.dtype == np.float32
         code = {np.dtype(np.float32): 0, np.dtype(np.float64): 1, np.dtype(np.uint8): 2}[a.dtype]
         L = _lib.lib()
         with torch.cuda.device(self.device):
@@ -245,13 +250,19 @@ class FlowEngine:
                                            ctypes.byref(self.cparams))
             if self._host_ws is None or self._host_ws.numel() < n:
                 self._host_ws = torch.empty(int(n), dtype=torch.uint8, device=self.device)
-            if submit_only:
-                fn = L.dis_stereo_batch_host_async if self.stereo else L.dis_flow_batch_host_async
-            else:
-                fn = L.dis_stereo_batch_host if self.stereo else L.dis_flow_batch_host
-            rc = fn(a.ctypes.data, b.ctypes.data, code, self.B, self.H, self.W,
+            args = (a.ctypes.data, b.ctypes.data, code, self.B, self.H, self.W,
                     ctypes.byref(self.cparams), out.ctypes.data, self._host_ws.data_ptr(),
                     int(n), _lib.stream_handle(stream))
+            if f32:
+                flags = (_lib.HOST_FLOW_F32 | (_lib.HOST_ASYNC if submit_only else 0)
+                         | (_lib.HOST_STEREO if self.stereo else 0))
+                rc = L.dis_flow_batch_host_ex(*args, flags)
+            elif submit_only:
+                fn = L.dis_stereo_batch_host_async if self.stereo else L.dis_flow_batch_host_async
+                rc = fn(*args)
+            else:
+                fn = L.dis_stereo_batch_host if self.stereo else L.dis_flow_batch_host
+                rc = fn(*args)
         _lib.check(rc)
         if submit_only:
             # the call owns its buffers until finish_host: keep them alive

@@ -67,3 +67,32 @@ def test_pageable_buffers_and_error_at_finish():
         eng.finish_host()
     eng.submit_host(f1, f2, out)  # the engine is usable again
     assert np.array_equal(eng.finish_host(), want)
+
+
+def test_float32_flow_out_is_the_rounded_float64_flow():
+    """DIS_HOST_FLOW_F32: same computation, the flow rounded to nearest on the
+    device (== astype(float32)); blocking, in flight and stereo."""
+    h, w, n = 109, 256, 5
+    params = DisParams(patch_size=8, overlap=0.5, iterations=32, finest_scale=1,
+                       coarsest_scale=3, variational=VarParams(outer_iters_fixed=1))
+    f1, f2 = _pairs(n, h, w, 21)
+    eng = FlowEngine(n, h, w, params)
+    want = eng.run_host(f1, f2).copy()
+    out32 = np.empty((n, h, w, 2), np.float32)
+    for _ in range(3):  # eager, captured (pageable: stays eager), repeated
+        out32[...] = np.nan
+        got = eng.run_host(f1, f2, out=out32)
+        assert got is out32 and np.array_equal(out32, want.astype(np.float32))
+    pin1, pin2 = (torch.from_numpy(x).pin_memory().numpy() for x in (f1, f2))
+    pout = torch.empty((n, h, w, 2), dtype=torch.float32).pin_memory().numpy()
+    for _ in range(3):  # pinned: eager, captured, replayed
+        pout[...] = np.nan
+        eng.submit_host(pin1, pin2, pout)
+        assert np.array_equal(eng.finish_host(), want.astype(np.float32))
+    # the float64 path on the same engine afterwards is untouched
+    assert np.array_equal(eng.run_host(f1, f2), want)
+    seng = FlowEngine(n, h, w, params, stereo=True)
+    swant = seng.run_host(f1, f2).copy()
+    assert np.array_equal(seng.run_host(f1, f2, out=out32), swant.astype(np.float32))
+    with pytest.raises(ValueError):
+        eng.run_host(f1, f2, out=np.empty((n, h, w, 2), np.float16))
