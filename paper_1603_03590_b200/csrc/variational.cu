@@ -500,7 +500,11 @@ __global__ void __launch_bounds__(((S + P - 1) / P) * kMaxBandRows + 32, 1)
   const bool below = sor_below_mode(Hc);  // the row below has its own 16 bytes
   const unsigned below_off = (unsigned)(kChunks * rrows * 16);  // (after the slot's chunks)
   const unsigned slot_bytes = below_off + (below ? (unsigned)kBelowSlot : 0u);
-  const unsigned ring_s = (unsigned)__cvta_generic_to_shared(smem);
+  // (opaque: the compiler otherwise rebuilds the shared-window address from
+  // SR_CgaCtaId, an S2R on every step's ring wrap)
+  unsigned ring_s_v = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("" : "+r"(ring_s_v));
+  const unsigned ring_s = ring_s_v;
   const unsigned ring_end = ring_s + (unsigned)R * slot_bytes;
   const unsigned xuv_s = ring_end;
   const unsigned xd_s = xuv_s + (unsigned)(2 * S * xrows * 16);
