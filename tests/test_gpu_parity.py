@@ -374,7 +374,9 @@ def test_engine_rejects_mismatched_buffers(torch):
     with pytest.raises(ValueError):
         eng.run_host(f[:1], f[:1])
     with pytest.raises(ValueError):
-        eng.run_host(f, f, out=np.empty((2, 64, 96, 2), dtype=np.float32))
+        eng.run_host(f, f, out=np.empty((2, 64, 96, 2), dtype=np.float16))  # (float32: opt-in)
+    with pytest.raises(ValueError):
+        eng.run_host(f, f, out=np.empty((2, 64, 96, 2), dtype=np.int64))
     with pytest.raises(ValueError):
         eng.run_host(f, f, out=np.empty((1, 64, 96, 2)))
     d = torch.zeros((2, 64, 96), device="cuda")

@@ -33,9 +33,9 @@ PROF = os.path.join(REPO, "profiles")
 CLASS_OF = [
     (r"k_sor", "sor"),
     (r"k_tensor_assemble", "tensor_assemble"),
-    (r"k_patch|k_bidir_prep", "patch_search"),
+    (r"k_patch|k_bidir_prep|k_pad_query", "patch_search"),
     (r"k_densify", "densify"),
-    (r"k_upsample|k_interleave", "upsample"),
+    (r"k_upsample|k_interleave|k_flow_to_f32", "upsample"),
     (r"k_level1|k_downsample|k_gradients|k_convert|k_level0|k_pyr_", "pyramid"),
 ]
 
