@@ -889,7 +889,7 @@ struct HostGraph {
   cudaGraphExec_t exec = nullptr;
   long long launches = 0;
 };
-constexpr int kHostGraphs = 4;
+constexpr int kHostGraphs = 8;  // (blocking, two in flight, float32 variants of two problems)
 HostGraph g_hgraph[kHostGraphs];
 int g_hgraph_next = 0;
 
