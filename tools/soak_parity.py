@@ -105,12 +105,19 @@ def main():
     ap.add_argument("--only", type=int, default=-1, help="replay one case index")
     a = ap.parse_args()
     bad = skipped = 0
+    stats = {"stereo": 0, "bidirectional": 0, "host": 0, "refined": 0, "pairs": 0, "pixels": 0}
     t0 = time.time()
     for k in range(a.cases):
         if a.only >= 0 and k != a.only:
             continue
         rng = np.random.default_rng([a.seed, k])
         c = draw_case(rng, a.max_px)
+        stats["stereo"] += c["stereo"]
+        stats["bidirectional"] += c["params"].bidirectional
+        stats["host"] += c["host"]
+        stats["refined"] += c["params"].variational is not None
+        stats["pairs"] += c["batch"]
+        stats["pixels"] += c["batch"] * c["h"] * c["w"]
         tag = (f"case {k} (seed {a.seed}): {c['batch']}x{c['h']}x{c['w']} {c['dtype']} "
                f"{'host' if c['host'] else 'dev'} {c['params']}")
         try:
@@ -128,7 +135,7 @@ def main():
             bad += 1
             print("MISMATCH", tag, "->", msg, flush=True)
     print(f"soak: {a.cases} cases, {bad} mismatches, {skipped} rejected by both sides, "
-          f"{time.time() - t0:.0f} s", flush=True)
+          f"{time.time() - t0:.0f} s; {stats}", flush=True)
     return 1 if bad else 0
 
 
