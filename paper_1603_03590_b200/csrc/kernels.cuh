@@ -75,6 +75,9 @@ struct SearchArgs {
   // (patch_search.cu, kQPad), read by the lane kernel
   const double* qpad;
   int qp_pitch;
+  // lane kernel: once the work queue is empty, a warp with at most this many
+  // patches still running hands them to the lane-group kernel (0: never)
+  int stragglers;
 };
 // scratch of one level's search: per-patch prep + parked state + counters +
 // the padded query level (W x H level, P patches per pair)

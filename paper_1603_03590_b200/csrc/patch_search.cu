@@ -99,6 +99,7 @@ __device__ __forceinline__ void load_run256(const double* p, double* s) {
 #ifndef DIS_GN_CARVEOUT
 #define DIS_GN_CARVEOUT -1  // experiments: the lane kernel's shared-memory carveout (%)
 #endif
+constexpr int kStragglers = 10;  // lane kernel: see SearchArgs::stragglers
 constexpr int kRangeCounters = 4;     // counter[4 ..]: consumed patches per block range
 constexpr int kMaxGnBlocks = 1024;
 
@@ -834,6 +835,7 @@ __global__ void __launch_bounds__(256, MINB) k_patch_gn(SearchArgs a,
   Lane& L = lanes[threadIdx.x];
   L.pid = -1;
   bool done = false;
+  bool drained = false;  // warp-uniform: the work queue had nothing left for this warp
   unsigned pool_next = 0, pool_end = 0;  // warp-uniform
   // block ranges (see kRangeCounters); victim = the range refills come from
   const unsigned nb = gridDim.x;
@@ -866,7 +868,10 @@ __global__ void __launch_bounds__(256, MINB) k_patch_gn(SearchArgs a,
           tried = DIS_GN_RANGES ? tried + 1 : nb;
           victim = victim + 1 == nb ? 0 : victim + 1;
         }
-        if (!got) break;
+        if (!got) {
+          drained = true;
+          break;
+        }
       }
       const unsigned avail = pool_end - pool_next;
       const unsigned rank = (unsigned)__popc(mask & ((1u << lane) - 1u));
@@ -883,6 +888,23 @@ __global__ void __launch_bounds__(256, MINB) k_patch_gn(SearchArgs a,
         lane_start(L, a, prep, N, P, nx, g);
     }
     if (__all_sync(FULL, done)) break;
+    // Stragglers: with the queue empty, a warp whose last few patches keep
+    // iterating (mean 3-5.5 evaluations, p99 22) runs at a
+    // few lanes of 32 and one evaluation of its serial chain takes as long
+    // as ever.  Such a warp parks its running patches (the same exact
+    // park/resume as the irregular windows: the state is complete between
+    // evaluations) for the lane-group kernel, whose 8 / 16 lanes per patch
+    // finish an evaluation several times sooner and spread over all SMs.
+    if (drained && a.stragglers > 0) {
+      const unsigned act = __ballot_sync(FULL, !done);
+      if (__popc(act) <= a.stragglers) {
+        if (!done) {
+          const unsigned slot = atomicAdd(spill_count, 1u);
+          lane_park(L, spill + (size_t)slot * kSpillStride);
+        }
+        break;
+      }
+    }
     if (done) continue;
 
     const double bx = (double)L.x0i + L.u, by = (double)L.y0i + L.v;
@@ -1242,6 +1264,11 @@ void launch_patch_search(const SearchArgs& a, void* scratch, cudaStream_t st) {
   } else if (a.ps == 8 || a.ps == 12) {
     // the query level with its replicated border (see kQPad)
     SearchArgs al = a;
+    static const int stragglers = [] {
+      const char* e = getenv("DIS_GN_STRAGGLERS");  // experiments only
+      return e ? atoi(e) : kStragglers;
+    }();
+    al.stragglers = stragglers;
     double* qpad = reinterpret_cast<double*>(static_cast<char*>(scratch) +
                                              search_state_bytes(a.B, a.ax.n * a.ay.n));
     al.qpad = qpad;
