@@ -71,6 +71,31 @@ def draw_case(rng, max_px):
                 stereo=stereo, disp=disp)
 
 
+def draw_big_case(rng):
+    """Batches whose finest level runs on the lane kernel (more than ~76k
+    patches over the batch): work queue, padded query
+    level, parked border windows and the straggler hand-off."""
+    ps = int(rng.choice([8, 8, 12]))
+    ov = float(rng.choice([0.5, 0.5, 0.75]))
+    finest = int(rng.choice([0, 1]))
+    coarsest = finest + int(rng.integers(1, 3))
+    h = int(rng.integers(90, 230)) * (2 ** finest)
+    w = int(rng.integers(180, 520)) * (2 ** finest)
+    sp = max(1, int(ps * (1.0 - ov)))
+    per_pair = ((h >> finest) // sp) * ((w >> finest) // sp)
+    need = 80000  # > 148 * 2048 * 2 / 8 = 148 * 2048 * 4 / 16 patches
+    batch = int(min(64, max(8, need // max(1, per_pair) + 2)))
+    refine = rng.random() < 0.6
+    vp = VarParams(outer_iters_fixed=1) if refine else None
+    p = DisParams(patch_size=ps, overlap=ov, iterations=int(rng.choice([8, 32, 64])),
+                  finest_scale=finest, coarsest_scale=coarsest,
+                  use_mean_normalization=bool(rng.random() < 0.85),
+                  residual_norm=str(rng.choice(["l2", "l2", "l1", "huber"])), variational=vp,
+                  mode="flow")
+    return dict(h=h, w=w, params=p, batch=batch, dtype="f32", host=bool(rng.random() < 0.2),
+                stereo=False, disp=float(rng.choice([3.0, 10.0, 25.0])))
+
+
 def run_case(c, seed):
     h, w, p, B = c["h"], c["w"], c["params"], c["batch"]
     f1 = np.empty((B, h, w), np.float32)
@@ -103,6 +128,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--max-px", type=int, default=40000)
     ap.add_argument("--only", type=int, default=-1, help="replay one case index")
+    ap.add_argument("--big", action="store_true",
+                    help="large batches whose finest level runs on the lane kernel")
     a = ap.parse_args()
     bad = skipped = 0
     stats = {"stereo": 0, "bidirectional": 0, "host": 0, "refined": 0, "pairs": 0, "pixels": 0}
@@ -111,7 +138,7 @@ def main():
         if a.only >= 0 and k != a.only:
             continue
         rng = np.random.default_rng([a.seed, k])
-        c = draw_case(rng, a.max_px)
+        c = draw_big_case(rng) if a.big else draw_case(rng, a.max_px)
         stats["stereo"] += c["stereo"]
         stats["bidirectional"] += c["params"].bidirectional
         stats["host"] += c["host"]
